@@ -1,0 +1,198 @@
+/* oracle/bfp_oracle.c -- TEST INFRASTRUCTURE ONLY (the checker, never the
+ * product).  Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline
+ * leg may load the library built from this file (oracle/liboracle.so).
+ *
+ * A plain-C, value-level restatement of the reference's bitslice FP path:
+ *
+ *   orc_encode   <- encode_scalar   format.hpp:125-188 (binary64 -> format)
+ *   orc_decode   <- decode_scalar   format.hpp:101-123 (format -> binary64)
+ *   orc_add/sub/mul/div/mul_add <- bfp_add/bfp_sub/bfp_mul/bfp_div
+ *                                   (arith.hpp:235-444), restated by value:
+ *       decode both operands exactly, combine them in binary64 under
+ *       fesetround(FE_TONEAREST | FE_TOWARDZERO), encode the result.
+ *       This is exact-then-rounded for every format with s <= 24:
+ *         - products of two (s+1)-bit significands are exact in binary64;
+ *         - RN double rounding is innocuous since 53 >= 2(s+1)+2;
+ *         - RZ truncation composes with RZ truncation.
+ *       The IEEE conventions of the circuits are all carried by encode /
+ *       binary64: canonical positive NaN (format.hpp:49-52), +0 from exact
+ *       cancellation and -0 only for (-0)+(-0) (arith.hpp:312-316), overflow
+ *       to Inf under RN / max-finite under RZ (arith.hpp:143-146), FTZ after
+ *       rounding with no input DAZ (arith.hpp:135-141).
+ *   orc_pack_planes / orc_unpack_planes <- field_from_elements / element_of
+ *       (bitfield.hpp:33-52): element i, plane j -> u32 word
+ *       ((i>>10)*n + j)*32 + ((i>>5)&31), bit i&31.
+ *
+ * Parity pin: tests/test_oracle.py checks this file against the reference
+ * headers compiled in place (oracle/_ref, see oracle/Makefile) exhaustively
+ * for the <= 9-bit formats and on seeded random + directed operands for the
+ * rest, and against the golden fixtures in tests/golden/.
+ *
+ * Build: gcc -O2 -std=c11 -frounding-math -ffp-contract=off -fPIC -shared.
+ */
+#include <fenv.h>
+#include <math.h>
+#include <stddef.h>
+#include <stdint.h>
+#include <string.h>
+
+#pragma STDC FENV_ACCESS ON
+
+typedef struct {
+  unsigned e, s;
+  int rn, ftz;
+} orc_fmt;
+
+static uint64_t make_enc(const orc_fmt* f, unsigned sign, uint64_t bexp, uint64_t frac) {
+  return ((uint64_t)(sign & 1u) << (f->e + f->s)) | (bexp << f->s) | frac;
+}
+static uint64_t exp_field_max(const orc_fmt* f) { return (1ull << f->e) - 1; }
+static int bias_of(const orc_fmt* f) { return (1 << (f->e - 1)) - 1; }
+
+static int clz64(uint64_t v) { return v ? __builtin_clzll(v) : 64; }
+
+/* encode_scalar, format.hpp:125-188 */
+uint64_t orc_encode(double x, unsigned e, unsigned s, int rn, int ftz) {
+  orc_fmt F = {e, s, rn, ftz};
+  const orc_fmt* f = &F;
+  uint64_t bits;
+  memcpy(&bits, &x, sizeof bits);
+  const unsigned sign = (unsigned)(bits >> 63);
+  const uint64_t e64 = (bits >> 52) & 0x7ff;
+  const uint64_t f64 = bits & ((1ull << 52) - 1);
+  if (e64 == 0x7ff) {
+    if (f64) return make_enc(f, 0, exp_field_max(f), 1ull << (s - 1)); /* canonical NaN */
+    return make_enc(f, sign, exp_field_max(f), 0);                      /* Inf */
+  }
+  if (e64 == 0 && f64 == 0) return make_enc(f, sign, 0, 0);
+  const uint64_t sig = e64 ? ((1ull << 52) | f64) : f64;
+  const int exp2 = e64 ? (int)e64 - 1023 - 52 : -1022 - 52;
+  const int msb = 63 - clz64(sig);
+  const int unb = exp2 + msb; /* floor(log2|x|) */
+  const int emin = 1 - bias_of(f), emax = bias_of(f);
+  const int ulp_exp = (unb >= emin ? unb : emin) - (int)s;
+  const int shift = ulp_exp - exp2;
+  uint64_t kept;
+  int guard = 0, sticky = 0;
+  if (shift <= 0) {
+    kept = sig << -shift;
+  } else if (shift > 64) {
+    kept = 0;
+    sticky = 1;
+  } else {
+    kept = shift == 64 ? 0 : sig >> shift;
+    guard = (int)((sig >> (shift - 1)) & 1u);
+    if (shift > 1) sticky = (sig & ((1ull << (shift - 1)) - 1)) != 0;
+  }
+  if (rn && guard && (sticky || (kept & 1u))) ++kept;
+  int res_exp = ulp_exp + (int)s;
+  if (kept >= (2ull << s)) {
+    kept >>= 1;
+    ++res_exp;
+  }
+  if (kept == 0) return make_enc(f, sign, 0, 0);
+  if (kept < (1ull << s)) {
+    if (ftz) return make_enc(f, sign, 0, 0);
+    return make_enc(f, sign, 0, kept);
+  }
+  if (res_exp > emax)
+    return rn ? make_enc(f, sign, exp_field_max(f), 0)
+              : make_enc(f, sign, exp_field_max(f) - 1, (1ull << s) - 1);
+  return make_enc(f, sign, (uint64_t)(res_exp + bias_of(f)), kept & ((1ull << s) - 1));
+}
+
+/* decode_scalar, format.hpp:101-123 (exact: every finite value of a legal
+ * format is a binary64 value) */
+double orc_decode(uint64_t enc, unsigned e, unsigned s) {
+  orc_fmt F = {e, s, 1, 0};
+  const orc_fmt* f = &F;
+  const unsigned sign = (unsigned)((enc >> (e + s)) & 1u);
+  const uint64_t bexp = (enc >> s) & exp_field_max(f);
+  const uint64_t frac = enc & ((1ull << s) - 1);
+  const double sg = sign ? -1.0 : 1.0;
+  if (bexp == exp_field_max(f)) return frac ? NAN : sg * INFINITY;
+  if (bexp == 0) {
+    if (!frac) return sg * 0.0;
+    return sg * ldexp((double)frac, 1 - bias_of(f) - (int)s);
+  }
+  return sg * ldexp((double)((1ull << s) | frac), (int)bexp - bias_of(f) - (int)s);
+}
+
+enum { ORC_ADD = 0, ORC_SUB = 1, ORC_MUL = 2, ORC_DIV = 3, ORC_MUL_ADD = 4 };
+
+static double rounded_op(int op, double a, double b, int rn) {
+  volatile double va = a, vb = b, r;
+  const int old = fegetround();
+  fesetround(rn ? FE_TONEAREST : FE_TOWARDZERO);
+  switch (op) {
+    case ORC_ADD: r = va + vb; break;
+    case ORC_SUB: r = va - vb; break;
+    case ORC_MUL: r = va * vb; break;
+    default: r = va / vb; break;
+  }
+  fesetround(old);
+  return r;
+}
+
+/* Value-level bfp_add / bfp_sub / bfp_mul / bfp_div (arith.hpp:235-444). */
+uint64_t orc_binop(int op, unsigned e, unsigned s, int rn, int ftz, uint64_t x, uint64_t y) {
+  const double a = orc_decode(x, e, s), b = orc_decode(y, e, s);
+  return orc_encode(rounded_op(op, a, b, rn), e, s, rn, ftz);
+}
+
+/* The chain bfp_add(bfp_mul(a, b), c): two roundings. */
+uint64_t orc_mul_add(unsigned e, unsigned s, int rn, int ftz, uint64_t a, uint64_t b, uint64_t c) {
+  const uint64_t p = orc_binop(ORC_MUL, e, s, rn, ftz, a, b);
+  return orc_binop(ORC_ADD, e, s, rn, ftz, p, c);
+}
+
+/* field_from_elements (bitfield.hpp:33-43), one 1024-element block at a time;
+ * the tail of the last block is zero-filled like pack.hpp:50. */
+void orc_pack_planes(const uint64_t* enc, size_t n, uint32_t* planes, unsigned nbits) {
+  const size_t blocks = (n + 1023) / 1024;
+  memset(planes, 0, blocks * nbits * 128);
+  for (size_t i = 0; i < n; ++i) {
+    const size_t blk = i >> 10;
+    const unsigned w = (unsigned)((i >> 5) & 31), bit = (unsigned)(i & 31);
+    for (unsigned j = 0; j < nbits; ++j)
+      planes[(blk * nbits + j) * 32 + w] |= (uint32_t)((enc[i] >> j) & 1u) << bit;
+  }
+}
+
+/* element_of (bitfield.hpp:45-52) */
+void orc_unpack_planes(const uint32_t* planes, size_t n, uint64_t* enc, unsigned nbits) {
+  for (size_t i = 0; i < n; ++i) {
+    const size_t blk = i >> 10;
+    const unsigned w = (unsigned)((i >> 5) & 31), bit = (unsigned)(i & 31);
+    uint64_t v = 0;
+    for (unsigned j = 0; j < nbits; ++j)
+      v |= (uint64_t)((planes[(blk * nbits + j) * 32 + w] >> bit) & 1u) << j;
+    enc[i] = v;
+  }
+}
+
+/* Array forms over encodings (u64 per element). */
+void orc_binop_array(int op, unsigned e, unsigned s, int rn, int ftz, const uint64_t* x,
+                     const uint64_t* y, const uint64_t* c, uint64_t* z, size_t n) {
+  if (op == ORC_MUL_ADD) {
+    for (size_t i = 0; i < n; ++i) z[i] = orc_mul_add(e, s, rn, ftz, x[i], y[i], c[i]);
+  } else {
+    for (size_t i = 0; i < n; ++i) z[i] = orc_binop(op, e, s, rn, ftz, x[i], y[i]);
+  }
+}
+
+void orc_encode_f32_array(const float* in, size_t n, uint64_t* out, unsigned e, unsigned s,
+                          int rn, int ftz) {
+  for (size_t i = 0; i < n; ++i) out[i] = orc_encode((double)in[i], e, s, rn, ftz);
+}
+
+void orc_decode_f32_array(const uint64_t* enc, size_t n, float* out, unsigned e, unsigned s) {
+  for (size_t i = 0; i < n; ++i) out[i] = (float)orc_decode(enc[i], e, s);
+}
+
+/* All (x, y) pairs of an n-bit format in row-major order: z[x * 2^n + y]. */
+void orc_binop_exhaustive(int op, unsigned e, unsigned s, int rn, int ftz, uint64_t* z) {
+  const uint64_t cnt = 1ull << (1 + e + s);
+  for (uint64_t x = 0; x < cnt; ++x)
+    for (uint64_t y = 0; y < cnt; ++y) z[x * cnt + y] = orc_binop(op, e, s, rn, ftz, x, y);
+}

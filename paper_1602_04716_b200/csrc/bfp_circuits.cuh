@@ -1,0 +1,510 @@
+// bfp_circuits.cuh -- bitslice floating-point circuits for sm_100a.
+//
+// One uint32_t word ("w32") carries bit k of 32 elements: the device form of
+// the reference's lane<W> (lane.hpp:28-117) at W = 32 per register.  Every
+// function below is a fixed, data-independent network of AND/OR/XOR/NOT over
+// such words; with the format a compile-time template (exponent bits E,
+// fraction bits S, RN/RZ, gradual/FTZ) every loop unrolls and every constant
+// folds, and ptxas maps the network onto 3-input LOP3 instructions.
+//
+// The networks are NOT a transcription of the reference circuits
+// (circuits.hpp / arith.hpp).  They compute the same function -- correctly
+// rounded IEEE-style add/sub/mul with the reference's conventions (canonical
+// positive NaN format.hpp:49-52, +0 from cancellation arith.hpp:312-316,
+// overflow to Inf/max-finite arith.hpp:143-146, FTZ after rounding with no
+// input DAZ arith.hpp:135-141) -- with fewer gates:
+//   * add: the alignment shift amount saturates instead of clearing the field,
+//     the normaliser is budget-limited at the effective exponent of the larger
+//     operand so subnormal sums land directly in place (no second shifter, no
+//     exponent-range test), and exponent/fraction are rounded as one packed
+//     integer so the significand carry, subnormal->normal and overflow->Inf
+//     transitions fall out of one increment chain;
+//   * mul: an exact (S+1)x(S+1) array product, full normalise, a narrow
+//     (S+3)-bit subnormal shifter driven by a (E+2)-bit exponent, packed
+//     rounding as above;
+//   * special values come from the larger-magnitude operand (add) or four
+//     class masks (mul) and are applied with one LOP3 per output plane.
+// Bit-exactness against the reference is established by tests, not by
+// structural similarity (tests/test_circuits_host.py exhaustively on the CPU,
+// tests/test_gpu_parity.py on the B200).
+//
+// The same header compiles for the host (g++) so the networks can be checked
+// exhaustively without a GPU.
+#pragma once
+#include <stdint.h>
+
+#if defined(__CUDACC__)
+#define BFP_HD __host__ __device__ __forceinline__
+#define BFP_UNROLL _Pragma("unroll")
+#else
+#define BFP_HD inline
+#define BFP_UNROLL
+#endif
+
+namespace bfpg {
+
+typedef uint32_t w32;
+constexpr w32 ONES = 0xffffffffu;
+
+template <int E_, int S_, bool RN_, bool FTZ_>
+struct Format {
+  static constexpr int E = E_;
+  static constexpr int S = S_;
+  static constexpr int N = 1 + E_ + S_;  // planes
+  static constexpr bool RN = RN_;
+  static constexpr bool FTZ = FTZ_;
+  static constexpr int BIAS = (1 << (E_ - 1)) - 1;
+};
+
+constexpr int clog2(int n) {
+  int k = 0;
+  while ((1 << k) < n) ++k;
+  return k;
+}
+constexpr int imax(int a, int b) { return a > b ? a : b; }
+constexpr int imin(int a, int b) { return a < b ? a : b; }
+
+// ---------------------------------------------------------------- gates
+BFP_HD w32 mux(w32 s, w32 a, w32 b) { return (s & a) | (~s & b); }  // s ? a : b
+BFP_HD w32 maj(w32 a, w32 b, w32 c) { return (a & b) | (c & (a | b)); }
+
+// a >= v for an unsigned K-bit field a (LSB first) and a constant v.
+template <int K>
+BFP_HD w32 ge_const(const w32* a, int v) {
+  if (v <= 0) return ONES;
+  if (v >= (1 << K)) return 0;
+  w32 r = ONES;
+  BFP_UNROLL for (int i = 0; i < K; ++i) r = ((v >> i) & 1) ? (a[i] & r) : (a[i] | r);
+  return r;
+}
+
+// ------------------------------------------------------- shifters
+// Right shift of f[0..W) by `dist` where sel is set; bit 0 is a jam (sticky)
+// position that absorbs every bit shifted through it.
+template <int W, int DIST>
+BFP_HD void shr_jam_stage(w32 (&f)[W], w32 sel) {
+  if constexpr (DIST < W) {
+    w32 t = 0;
+    BFP_UNROLL for (int i = 1; i <= DIST && i < W; ++i) t |= f[i];
+    w32 nf[W];
+    nf[0] = f[0] | (sel & t);
+    BFP_UNROLL for (int i = 1; i < W; ++i) nf[i] = mux(sel, (i + DIST < W) ? f[i + DIST] : 0u, f[i]);
+    BFP_UNROLL for (int i = 0; i < W; ++i) f[i] = nf[i];
+  } else {
+    w32 t = 0;
+    BFP_UNROLL for (int i = 1; i < W; ++i) t |= f[i];
+    f[0] = f[0] | (sel & t);
+    BFP_UNROLL for (int i = 1; i < W; ++i) f[i] = f[i] & ~sel;
+  }
+}
+
+template <int W, int K, int KK = 0>
+BFP_HD void shr_jam(w32 (&f)[W], const w32* amt) {
+  if constexpr (KK < K) {
+    shr_jam_stage<W, (1 << KK)>(f, amt[KK]);
+    shr_jam<W, K, KK + 1>(f, amt);
+  }
+}
+
+// Left shift of f[0..W) by DIST where sel is set (zero fill).
+template <int W, int DIST>
+BFP_HD void shl_stage(w32 (&f)[W], w32 sel) {
+  w32 nf[W];
+  BFP_UNROLL for (int i = 0; i < W; ++i) nf[i] = mux(sel, (i >= DIST) ? f[i - DIST] : 0u, f[i]);
+  BFP_UNROLL for (int i = 0; i < W; ++i) f[i] = nf[i];
+}
+
+// Unlimited leading-zero normaliser over f[0..W): stage k (descending) shifts
+// left by 2^k when the top 2^k bits are all zero; cnt[k] records it.
+template <int W, int K, int KK>
+BFP_HD void normalize_stages(w32 (&f)[W], w32* cnt) {
+  if constexpr (KK >= 0) {
+    constexpr int D = 1 << KK;
+    if constexpr (D < W) {
+      w32 any = 0;
+      BFP_UNROLL for (int i = W - D; i < W; ++i) any |= f[i];
+      const w32 c = ~any;
+      shl_stage<W, D>(f, c);
+      cnt[KK] = c;
+    } else {
+      cnt[KK] = 0;
+    }
+    normalize_stages<W, K, KK - 1>(f, cnt);
+  }
+}
+
+// ------------------------------------------------ integer arithmetic
+// r = a + b + cin over K bits; returns carry out.
+template <int K>
+BFP_HD w32 add_k(const w32* a, const w32* b, w32 cin, w32* r) {
+  w32 c = cin;
+  BFP_UNROLL for (int i = 0; i < K; ++i) {
+    const w32 ai = a[i], bi = b[i];
+    r[i] = ai ^ bi ^ c;
+    c = maj(ai, bi, c);
+  }
+  return c;
+}
+
+// r = a - b over K bits (a + ~b + 1); returns the borrow (a < b).
+template <int K>
+BFP_HD w32 sub_k(const w32* a, const w32* b, w32* r) {
+  w32 c = ONES;
+  BFP_UNROLL for (int i = 0; i < K; ++i) {
+    const w32 ai = a[i], nbi = ~b[i];
+    r[i] = ai ^ nbi ^ c;
+    c = maj(ai, nbi, c);
+  }
+  return ~c;
+}
+
+// ------------------------------------------------------- final assembly
+// Packs [expfield (EW bits, may be wider than E) : frac(S)] with the hidden
+// bit added at position S and the rounding increment at position 0:
+//   out = frac + rnd, exp = expf + hidden + carry(frac + rnd).
+// Returns the E+1 bits of the exponent sum in ex[] (bit E = overflow past
+// 2^E) and the final S fraction bits in fr[].
+template <int E, int S, int EW>
+BFP_HD void pack_round(const w32* expf, const w32* sig /*S+1*/, w32 rnd, w32* fr, w32* ex) {
+  w32 c = rnd;
+  BFP_UNROLL for (int i = 0; i < S; ++i) {
+    const w32 v = sig[i];
+    fr[i] = v ^ c;
+    c = v & c;
+  }
+  // position S: expf[0] + hidden + carry
+  {
+    const w32 h = sig[S], v = expf[0];
+    ex[0] = v ^ h ^ c;
+    c = maj(v, h, c);
+  }
+  BFP_UNROLL for (int i = 1; i <= E; ++i) {
+    const w32 v = (i < EW) ? expf[i] : 0u;
+    ex[i] = v ^ c;
+    c = v & c;
+  }
+}
+
+// ================================================================= ADD
+// Z = X + Y (SUB: X - Y).  bfp_add / bfp_sub semantics, arith.hpp:235-328.
+template <class F, bool SUB>
+BFP_HD void add_w(const w32* X, const w32* Y, w32* Z) {
+  constexpr int E = F::E, S = F::S, M = E + S;
+  const w32 sx = X[M];
+  const w32 sy = SUB ? ~Y[M] : Y[M];
+
+  // Order by magnitude: swap = |X| < |Y| as (E+S)-bit encodings (borrow of X-Y).
+  w32 bw = 0;
+  BFP_UNROLL for (int i = 0; i < M; ++i) bw = maj(~X[i], Y[i], bw);
+  const w32 swap = bw;
+  w32 A[M], B[M];
+  BFP_UNROLL for (int i = 0; i < M; ++i) {
+    A[i] = mux(swap, Y[i], X[i]);
+    B[i] = mux(swap, X[i], Y[i]);
+  }
+  const w32 sa = mux(swap, sy, sx);
+  const w32 sb = mux(swap, sx, sy);
+  const w32 eff = sx ^ sy;  // effective subtraction
+
+  // Hidden bits (exponent nonzero) and effective exponents (subnormals at 1).
+  w32 ha = 0, hb = 0;
+  BFP_UNROLL for (int i = 0; i < E; ++i) {
+    ha |= A[S + i];
+    hb |= B[S + i];
+  }
+  w32 ea[E], eb[E];
+  BFP_UNROLL for (int i = 0; i < E; ++i) {
+    ea[i] = A[S + i];
+    eb[i] = B[S + i];
+  }
+  ea[0] |= ~ha;
+  eb[0] |= ~hb;
+
+  // Alignment distance d = ea - eb >= 0.
+  w32 d[E];
+  (void)sub_k<E>(ea, eb, d);
+
+  // Align B: [jam, r, g, frac(S), hidden] right by d.  Distances >= WA-1 put
+  // everything in the jam bit, so the amount saturates at 2^KA - 1 >= WA - 1.
+  constexpr int WA = S + 4;
+  constexpr int KA = clog2(WA);
+  constexpr int KS = imin(KA, E);
+  w32 f[WA];
+  f[0] = 0;
+  f[1] = 0;
+  f[2] = 0;
+  BFP_UNROLL for (int j = 0; j < S; ++j) f[3 + j] = B[j];
+  f[S + 3] = hb;
+  w32 amt[KS];
+  {
+    w32 big = 0;
+    BFP_UNROLL for (int k = KA; k < E; ++k) big |= d[k];
+    BFP_UNROLL for (int k = 0; k < KS; ++k) amt[k] = d[k] | big;
+  }
+  shr_jam<WA, KS>(f, amt);
+
+  // One adder for both effective operations: A + (B ^ eff) + eff.
+  constexpr int WN = WA + 1;
+  w32 x[WN];
+  {
+    w32 ma[WA];
+    ma[0] = 0;
+    ma[1] = 0;
+    ma[2] = 0;
+    BFP_UNROLL for (int j = 0; j < S; ++j) ma[3 + j] = A[j];
+    ma[S + 3] = ha;
+    w32 c = eff;
+    BFP_UNROLL for (int i = 0; i < WA; ++i) {
+      const w32 t = f[i] ^ eff;
+      x[i] = ma[i] ^ t ^ c;
+      c = maj(ma[i], t, c);
+    }
+    x[WA] = c & ~eff;  // only an effective add carries out
+  }
+
+  // Budget-limited normalise: shift left by sh = min(lz(x), ea) so results
+  // below the smallest normal stop at the subnormal position.  The budget r
+  // starts at min(ea, 2^KN - 1) and is decremented by every shift taken.
+  constexpr int KN = clog2(WN);  // 2^KN - 1 >= WN - 1
+  w32 r[KN];
+  {
+    w32 big = 0;
+    BFP_UNROLL for (int k = KN; k < E; ++k) big |= ea[k];
+    BFP_UNROLL for (int k = 0; k < KN; ++k) r[k] = (k < E ? ea[k] : 0u) | big;
+  }
+  w32 sh[KN];
+  BFP_UNROLL for (int k = KN - 1; k >= 0; --k) {
+    const int D = 1 << k;
+    w32 ok = 0;
+    BFP_UNROLL for (int j = k; j < KN; ++j) ok |= r[j];
+    w32 any = 0;
+    BFP_UNROLL for (int i = WN - D; i < WN; ++i) any |= (i >= 0 ? x[i] : 0u);
+    const w32 c = ok & ~any;
+    sh[k] = c;
+    w32 nx[WN];
+    BFP_UNROLL for (int i = 0; i < WN; ++i) nx[i] = mux(c, (i >= D) ? x[i - D] : 0u, x[i]);
+    BFP_UNROLL for (int i = 0; i < WN; ++i) x[i] = nx[i];
+    if (k > 0) {
+      // r -= c << k (r >= 2^k whenever c is set)
+      w32 bo = c;
+      BFP_UNROLL for (int j = k; j < KN; ++j) {
+        const w32 rj = r[j];
+        r[j] = rj ^ bo;
+        bo = bo & ~rj;
+      }
+    }
+  }
+
+  // sig = x[4..S+4], guard x[3], sticky x[0..2].
+  const w32* sig = x + 4;
+  w32 rnd = 0;
+  if constexpr (F::RN) rnd = x[3] & (x[0] | x[1] | x[2] | sig[0]);
+
+  // D = ea - sh; exponent field = D + hidden (+ rounding carry).
+  w32 Dx[E];
+  {
+    w32 shx[E];
+    BFP_UNROLL for (int i = 0; i < E; ++i) shx[i] = (i < KN) ? sh[i] : 0u;
+    (void)sub_k<E>(ea, shx, Dx);
+  }
+  w32 fr[S], ex[E + 1];
+  pack_round<E, S, E>(Dx, sig, rnd, fr, ex);
+
+  // Exact zero: +0 from cancellation, -0 only for (-0) + (-0).
+  w32 nz = 0;
+  BFP_UNROLL for (int i = 0; i <= S; ++i) nz |= sig[i];
+  const w32 hidden = sig[S];
+
+  // Specials: the larger-magnitude operand is Inf/NaN whenever either is.
+  w32 as = ONES, bs = ONES, afz = 0;
+  BFP_UNROLL for (int i = 0; i < E; ++i) {
+    as &= A[S + i];
+    bs &= B[S + i];
+  }
+  BFP_UNROLL for (int i = 0; i < S; ++i) afz |= A[i];
+  const w32 use_nan = as & (afz | (bs & eff));
+
+  // Overflow: exponent sum >= 2^E - 1.
+  w32 eall = ONES;
+  BFP_UNROLL for (int i = 0; i < E; ++i) eall &= ex[i];
+  const w32 ovf = ex[E] | eall;
+
+  // Fraction mask: keep unless special, overflow (RN: Inf) or FTZ flush.
+  w32 keep = ~as;
+  if constexpr (F::RN) keep &= ~ovf;
+  if constexpr (F::FTZ) keep &= hidden;  // add: subnormal results are exact
+  w32 setf = 0;
+  if constexpr (!F::RN) setf = ovf & ~as;  // RZ overflow -> max finite
+  BFP_UNROLL for (int j = 0; j < S; ++j) Z[j] = (fr[j] & keep) | setf;
+  Z[S - 1] |= use_nan;
+
+  // Exponent plane: zero results clear, specials / RN overflow set all.
+  w32 setx = as;
+  if constexpr (F::RN) setx |= ex[E];
+  BFP_UNROLL for (int j = 0; j < E; ++j) {
+    w32 v = ex[j] & nz;
+    if constexpr (!F::RN)
+      if (j == 0) v &= ~ovf;  // RZ overflow -> exponent 2^E - 2
+    Z[S + j] = v | setx;
+  }
+  // Sign: specials take A's sign (NaN positive); zero sums sa & sb.
+  Z[M] = sa & mux(as, ~use_nan, sb | nz);
+}
+
+// ================================================================= MUL
+// Z = X * Y.  bfp_mul semantics, arith.hpp:330-373.
+template <class F>
+BFP_HD void mul_w(const w32* X, const w32* Y, w32* Z) {
+  constexpr int E = F::E, S = F::S, M = E + S;
+  constexpr int EW = E + 2;  // signed working exponent
+  const w32 sign = X[M] ^ Y[M];
+
+  w32 hx = 0, hy = 0, xs = ONES, ys = ONES, xf = 0, yf = 0;
+  BFP_UNROLL for (int i = 0; i < E; ++i) {
+    hx |= X[S + i];
+    hy |= Y[S + i];
+    xs &= X[S + i];
+    ys &= Y[S + i];
+  }
+  BFP_UNROLL for (int i = 0; i < S; ++i) {
+    xf |= X[i];
+    yf |= Y[i];
+  }
+
+  // Exact product of the (S+1)-bit significands: shift-add rows.
+  constexpr int WP = 2 * S + 2;
+  w32 P[WP];
+  {
+    w32 mx[S + 1], my[S + 1];
+    BFP_UNROLL for (int i = 0; i < S; ++i) {
+      mx[i] = X[i];
+      my[i] = Y[i];
+    }
+    mx[S] = hx;
+    my[S] = hy;
+    BFP_UNROLL for (int j = 0; j <= S; ++j) P[j] = mx[j] & my[0];
+    BFP_UNROLL for (int j = S + 1; j < WP; ++j) P[j] = 0;
+    BFP_UNROLL for (int i = 1; i <= S; ++i) {
+      w32 c = 0;
+      BFP_UNROLL for (int j = 0; j <= S; ++j) {
+        const w32 pp = mx[j] & my[i];
+        const w32 a = P[i + j];
+        P[i + j] = a ^ pp ^ c;
+        c = maj(a, pp, c);
+      }
+      P[i + S + 1] = c;
+    }
+  }
+
+  // Normalise: leading one to position 2S+1.
+  constexpr int KP = clog2(WP);
+  w32 lz[KP];
+  normalize_stages<WP, KP, KP - 1>(P, lz);
+
+  // Ezm1 = ex_eff + ey_eff - bias - lz  (EW-bit two's complement); the
+  // biased result exponent is Ezm1 + 1 when positive.
+  w32 ez[EW];
+  {
+    w32 a[EW], b[EW];
+    BFP_UNROLL for (int i = 0; i < EW; ++i) {
+      a[i] = (i < E) ? X[S + i] : 0u;
+      b[i] = (i < E) ? Y[S + i] : 0u;
+    }
+    a[0] |= ~hx;
+    b[0] |= ~hy;
+    // ex + ey + (-bias): add the constant two's complement of bias
+    w32 t[EW];
+    (void)add_k<EW>(a, b, 0, t);
+    w32 nb[EW];
+    constexpr int NB = (1 << EW) - F::BIAS;  // -bias mod 2^EW
+    BFP_UNROLL for (int i = 0; i < EW; ++i) nb[i] = ((NB >> i) & 1) ? ONES : 0u;
+    w32 u[EW];
+    (void)add_k<EW>(t, nb, 0, u);
+    w32 l[EW];
+    BFP_UNROLL for (int i = 0; i < EW; ++i) l[i] = (i < KP) ? lz[i] : 0u;
+    (void)sub_k<EW>(u, l, ez);
+  }
+  const w32 sub = ez[EW - 1];  // Ezm1 < 0: subnormal range
+
+  // Rounding field [jam, guard, sig(S+1)]; shift right by -Ezm1 when sub.
+  constexpr int WR = S + 3;
+  w32 R[WR];
+  {
+    w32 st = 0;
+    BFP_UNROLL for (int i = 0; i < S; ++i) st |= P[i];
+    R[0] = st;
+    R[1] = P[S];
+    BFP_UNROLL for (int i = 0; i <= S; ++i) R[2 + i] = P[S + 1 + i];
+  }
+  {
+    // amt = -Ezm1 = ~Ezm1 + 1, live only on sub; saturate at 2^KR - 1 >= WR - 1.
+    constexpr int KR = clog2(WR);
+    constexpr int KRS = imin(KR, EW - 1);
+    w32 ng[EW];
+    w32 c = ONES;
+    BFP_UNROLL for (int i = 0; i < EW; ++i) {
+      const w32 v = ~ez[i];
+      ng[i] = v ^ c;
+      c = v & c;
+    }
+    w32 big = 0;
+    BFP_UNROLL for (int k = KR; k < EW - 1; ++k) big |= ng[k];
+    w32 amt[KRS];
+    BFP_UNROLL for (int k = 0; k < KRS; ++k) amt[k] = (ng[k] | big) & sub;
+    shr_jam<WR, KRS>(R, amt);
+  }
+  const w32* sig = R + 2;
+  w32 rnd = 0;
+  if constexpr (F::RN) rnd = R[1] & (R[0] | sig[0]);
+
+  // exponent field: Ezm1 masked to 0 in the subnormal range (E+1 bits kept
+  // for overflow detection), + hidden, + rounding carry.
+  w32 em[E + 1];
+  BFP_UNROLL for (int i = 0; i <= E; ++i) em[i] = ez[i] & ~sub;
+  w32 fr[S], ex[E + 2];
+  pack_round<E + 1, S, E + 1>(em, sig, rnd, fr, ex);
+  w32 eall = ONES;
+  BFP_UNROLL for (int i = 0; i < E; ++i) eall &= ex[i];
+  const w32 ovf = ex[E] | ex[E + 1] | eall;
+
+  // Special-value classes (mul rules, arith.hpp:193-199).
+  const w32 xz = ~hx & ~xf, yz = ~hy & ~yf;
+  const w32 Zr = xz | yz;   // a zero operand
+  const w32 SP = xs | ys;   // an Inf/NaN operand
+  const w32 use_nan = (xs & xf) | (ys & yf) | (xs & yz) | (ys & xz);
+
+  w32 flush = 0;
+  if constexpr (F::FTZ) flush = sub & ~ex[0];  // still below the smallest normal
+  const w32 quiet = ~(Zr | SP);
+  w32 keep, setf = 0;
+  if constexpr (F::RN) {
+    keep = quiet & ~ovf & ~flush;
+  } else {
+    keep = quiet & ~flush;
+    setf = quiet & ovf;
+  }
+  BFP_UNROLL for (int j = 0; j < S; ++j) Z[j] = (fr[j] & keep) | setf;
+  Z[S - 1] |= use_nan;
+  const w32 hset = SP | (~Zr & ovf);
+  BFP_UNROLL for (int j = 0; j < E; ++j) {
+    w32 v = ex[j];
+    if constexpr (!F::RN)
+      if (j == 0) {
+        Z[S] = (v & ~Zr & ~ovf) | SP;
+        continue;
+      }
+    Z[S + j] = (v & ~Zr) | hset;
+  }
+  Z[M] = sign & ~use_nan;
+}
+
+// z = round(round(a * b) + c) -- the reference chain bfp_add(bfp_mul(a,b),c),
+// fused in registers (config 5).
+template <class F>
+BFP_HD void mul_add_w(const w32* A, const w32* B, const w32* Cc, w32* Z) {
+  w32 p[F::N];
+  mul_w<F>(A, B, p);
+  add_w<F, false>(p, Cc, Z);
+}
+
+}  // namespace bfpg
