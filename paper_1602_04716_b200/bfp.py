@@ -1,0 +1,304 @@
+"""Host-side mirror of the reference operator API over device-resident planes.
+
+Same names, argument meaning and error behaviour as the reference headers
+(/root/reference/proj/include/bfp/), with the lane width replaced by
+device-resident slice-major planes of any length:
+
+  reference                                   here
+  ------------------------------------------  --------------------------------------
+  rounding_mode, subnormal_policy             rounding_mode, subnormal_policy
+    format.hpp:16-17
+  format_spec, validate, make_spec            format_spec, validate, make_spec
+    format.hpp:23-73                            (ValueError == std::invalid_argument)
+  bfp_vector<L>  pack.hpp:20-26               bfp_vector (spec, planes, count)
+  pack / unpack  pack.hpp:41-76               pack / unpack  (documented layout)
+  encode_scalar + pack, unpack + decode       pack_f32 / unpack_f32
+  bfp_add / bfp_sub / bfp_mul / bfp_div       bfp_add / bfp_sub / bfp_mul / bfp_div
+    arith.hpp:235-444                           (require_same_shape incl. name)
+  bfp_add(bfp_mul(a, b), c)                   bfp_mul_add (one fused kernel)
+  encode_scalar / decode_scalar               encode_scalar / decode_scalar (host)
+    format.hpp:101-188
+
+All device work goes through libbfpgpu.so (include/bfpgpu.h) on the current
+torch CUDA stream.  Planes are stored as torch.int32 (bit patterns).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import math
+import struct
+from dataclasses import dataclass, field
+
+import torch
+
+from ._lib import BfpFormat, check, lib
+
+
+class rounding_mode(enum.IntEnum):  # format.hpp:16
+    rz = 0
+    rn = 1
+
+
+class subnormal_policy(enum.IntEnum):  # format.hpp:17
+    gradual = 0
+    ftz = 1
+
+
+OP_ADD, OP_SUB, OP_MUL, OP_DIV, OP_MUL_ADD = 0, 1, 2, 3, 4
+
+
+@dataclass(frozen=True)
+class format_spec:
+    """format.hpp:23-55."""
+
+    exp_bits: int = 0
+    sig_bits: int = 0
+    rounding: rounding_mode = rounding_mode.rn
+    subnormals: subnormal_policy = subnormal_policy.gradual
+    name: str = ""
+    _c: BfpFormat = field(default=None, init=False, repr=False, compare=False, hash=False)
+
+    def __post_init__(self):
+        object.__setattr__(self, "_c", BfpFormat(self.exp_bits, self.sig_bits, int(self.rounding),
+                                                 int(self.subnormals), self.name.encode()))
+
+    def total_bits(self) -> int:
+        return 1 + self.exp_bits + self.sig_bits
+
+    def bias(self) -> int:
+        return (1 << (self.exp_bits - 1)) - 1
+
+    def emax(self) -> int:
+        return self.bias()
+
+    def emin(self) -> int:
+        return 1 - self.bias()
+
+    def exp_field_max(self) -> int:
+        return (1 << self.exp_bits) - 1
+
+    def sign_mask(self) -> int:
+        return 1 << (self.exp_bits + self.sig_bits)
+
+    def frac_mask(self) -> int:
+        return (1 << self.sig_bits) - 1
+
+    def make(self, sign: int, biased_exp: int, fraction: int) -> int:
+        return ((sign & 1) << (self.exp_bits + self.sig_bits)) | (biased_exp << self.sig_bits) | fraction
+
+    def inf(self, sign: int) -> int:
+        return self.make(sign, self.exp_field_max(), 0)
+
+    def max_finite(self, sign: int) -> int:
+        return self.make(sign, self.exp_field_max() - 1, self.frac_mask())
+
+    def canonical_nan(self) -> int:
+        return self.make(0, self.exp_field_max(), 1 << (self.sig_bits - 1))
+
+    @property
+    def c(self) -> C.POINTER(BfpFormat):
+        return C.byref(self._c)
+
+    def plane_bytes(self, count: int) -> int:
+        return ((count + 1023) // 1024) * self.total_bits() * 128
+
+    def enc_bytes(self) -> int:
+        n = self.total_bits()
+        return 1 if n <= 8 else 2 if n <= 16 else 4 if n <= 32 else 8
+
+
+def validate(f: format_spec) -> None:
+    """format.hpp:57-64 (raises ValueError where the reference throws invalid_argument)."""
+    if f.exp_bits < 2 or f.exp_bits > 11:
+        raise ValueError("exp_bits must be in [2, 11]")
+    if f.sig_bits < 1 or f.sig_bits > 52:
+        raise ValueError("sig_bits must be in [1, 52]")
+    if f.total_bits() > 64:
+        raise ValueError("1 + exp_bits + sig_bits must not exceed 64")
+
+
+def make_spec(exp_bits: int, sig_bits: int, rounding: rounding_mode = rounding_mode.rn,
+              subnormals: subnormal_policy = subnormal_policy.gradual, name: str = "") -> format_spec:
+    """format.hpp:66-73."""
+    f = format_spec(exp_bits, sig_bits, rounding_mode(rounding), subnormal_policy(subnormals), name)
+    validate(f)
+    return f
+
+
+def require_same_shape(a: format_spec, b: format_spec) -> None:
+    """arith.hpp:228-231 -- compares the whole spec, name included."""
+    check(lib().bfp_same_shape(a.c, b.c), "require_same_shape")
+
+
+@dataclass
+class bfp_vector:
+    """pack.hpp:20-26: a format plus its bitslice field -- here `count` elements
+    in device-resident planes (torch.int32, bfp_plane_bytes / 4 words)."""
+
+    spec: format_spec
+    planes: torch.Tensor
+    count: int
+
+    @property
+    def width(self) -> int:
+        return self.count
+
+    def clone(self) -> "bfp_vector":
+        return bfp_vector(self.spec, self.planes.clone(), self.count)
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def empty(spec: format_spec, count: int, device=None) -> bfp_vector:
+    words = spec.plane_bytes(count) // 4
+    planes = torch.empty(words, dtype=torch.int32, device=device or "cuda")
+    return bfp_vector(spec, planes, count)
+
+
+def _enc_dtype(spec: format_spec) -> torch.dtype:
+    return {1: torch.uint8, 2: torch.int16, 4: torch.int32, 8: torch.int64}[spec.enc_bytes()]
+
+
+def pack(encs: torch.Tensor, spec: format_spec) -> bfp_vector:
+    """Encodings (sign:exp:frac, one integer per element, on the device) ->
+    bitslice planes in the documented layout (pack.hpp:13-15, 41-58)."""
+    validate(spec)
+    encs = encs.to(_enc_dtype(spec)).contiguous()
+    out = empty(spec, encs.numel(), encs.device)
+    check(lib().bfp_pack_enc(spec.c, encs.data_ptr(), out.planes.data_ptr(), encs.numel(), _stream()),
+          "pack")
+    return out
+
+
+def unpack(v: bfp_vector, count: int | None = None) -> torch.Tensor:
+    """pack.hpp:60-76: planes -> `count` encodings (device tensor of the
+    format's encoding width; bit patterns, see to_u64)."""
+    count = v.count if count is None else count
+    if count > v.count:
+        raise ValueError("unpack: count exceeds vector width")
+    out = torch.empty(count, dtype=_enc_dtype(v.spec), device=v.planes.device)
+    check(lib().bfp_unpack_enc(v.spec.c, v.planes.data_ptr(), out.data_ptr(), count, _stream()),
+          "unpack")
+    return out
+
+
+def to_u64(encs: torch.Tensor, spec: format_spec) -> torch.Tensor:
+    """Bit patterns of `unpack` as non-negative int64."""
+    mask = (1 << spec.total_bits()) - 1
+    return encs.to(torch.int64) & mask
+
+
+def pack_f32(x: torch.Tensor, spec: format_spec) -> bfp_vector:
+    """float32 -> encode_scalar((double)x) -> planes."""
+    validate(spec)
+    x = x.to(torch.float32).contiguous()
+    out = empty(spec, x.numel(), x.device)
+    check(lib().bfp_pack_f32(spec.c, x.data_ptr(), out.planes.data_ptr(), x.numel(), _stream()),
+          "pack_f32")
+    return out
+
+
+def unpack_f32(v: bfp_vector, count: int | None = None) -> torch.Tensor:
+    """planes -> (float)decode_scalar."""
+    count = v.count if count is None else count
+    if count > v.count:
+        raise ValueError("unpack_f32: count exceeds vector width")
+    out = torch.empty(count, dtype=torch.float32, device=v.planes.device)
+    check(lib().bfp_unpack_f32(v.spec.c, v.planes.data_ptr(), out.data_ptr(), count, _stream()),
+          "unpack_f32")
+    return out
+
+
+def _binop(op: int, x: bfp_vector, y: bfp_vector, c: bfp_vector | None = None,
+           out: bfp_vector | None = None) -> bfp_vector:
+    require_same_shape(x.spec, y.spec)
+    if c is not None:
+        require_same_shape(x.spec, c.spec)
+    if x.count != y.count or (c is not None and c.count != x.count):
+        raise ValueError("operands must have the same element count")
+    z = out if out is not None else empty(x.spec, x.count, x.planes.device)
+    check(lib().bfp_arith(op, x.spec.c, x.planes.data_ptr(), y.planes.data_ptr(),
+                          c.planes.data_ptr() if c is not None else None, z.planes.data_ptr(),
+                          x.count, _stream()), ("add", "sub", "mul", "div", "mul_add")[op])
+    return z
+
+
+def bfp_add(x: bfp_vector, y: bfp_vector, out: bfp_vector | None = None) -> bfp_vector:
+    """arith.hpp:235-320."""
+    return _binop(OP_ADD, x, y, out=out)
+
+
+def bfp_sub(x: bfp_vector, y: bfp_vector, out: bfp_vector | None = None) -> bfp_vector:
+    """arith.hpp:322-328."""
+    return _binop(OP_SUB, x, y, out=out)
+
+
+def bfp_mul(x: bfp_vector, y: bfp_vector, out: bfp_vector | None = None) -> bfp_vector:
+    """arith.hpp:330-373."""
+    return _binop(OP_MUL, x, y, out=out)
+
+
+def bfp_div(x: bfp_vector, y: bfp_vector, out: bfp_vector | None = None) -> bfp_vector:
+    """arith.hpp:375-444."""
+    return _binop(OP_DIV, x, y, out=out)
+
+
+def bfp_mul_add(a: bfp_vector, b: bfp_vector, c: bfp_vector,
+                out: bfp_vector | None = None) -> bfp_vector:
+    """bfp_add(bfp_mul(a, b), c) -- two roundings, one kernel."""
+    return _binop(OP_MUL_ADD, a, b, c, out=out)
+
+
+# --------------------------------------------------------------------- host codec
+def encode_scalar(x: float, f: format_spec) -> int:
+    """format.hpp:125-188: correctly rounded binary64 -> format (host, scalar)."""
+    bits = struct.unpack("<Q", struct.pack("<d", float(x)))[0]
+    sign = bits >> 63
+    e64 = (bits >> 52) & 0x7FF
+    f64 = bits & ((1 << 52) - 1)
+    if e64 == 0x7FF:
+        return f.canonical_nan() if f64 else f.inf(sign)
+    if e64 == 0 and f64 == 0:
+        return f.make(sign, 0, 0)
+    sig = ((1 << 52) | f64) if e64 else f64
+    exp2 = (e64 - 1023 - 52) if e64 else (-1022 - 52)
+    unb = exp2 + sig.bit_length() - 1
+    s = f.sig_bits
+    ulp_exp = max(unb, f.emin()) - s
+    shift = ulp_exp - exp2
+    guard = sticky = 0
+    if shift <= 0:
+        kept = sig << -shift
+    else:
+        kept = sig >> shift
+        guard = (sig >> (shift - 1)) & 1
+        sticky = int((sig & ((1 << (shift - 1)) - 1)) != 0)
+    if f.rounding == rounding_mode.rn and guard and (sticky or (kept & 1)):
+        kept += 1
+    res_exp = ulp_exp + s
+    if kept >= (2 << s):
+        kept >>= 1
+        res_exp += 1
+    if kept == 0:
+        return f.make(sign, 0, 0)
+    if kept < (1 << s):
+        return f.make(sign, 0, 0) if f.subnormals == subnormal_policy.ftz else f.make(sign, 0, kept)
+    if res_exp > f.emax():
+        return f.inf(sign) if f.rounding == rounding_mode.rn else f.max_finite(sign)
+    return f.make(sign, res_exp + f.bias(), kept & f.frac_mask())
+
+
+def decode_scalar(enc: int, f: format_spec) -> float:
+    """format.hpp:101-123: exact value of an encoding (host, scalar)."""
+    sign = (enc >> (f.exp_bits + f.sig_bits)) & 1
+    be = (enc >> f.sig_bits) & f.exp_field_max()
+    fr = enc & f.frac_mask()
+    sg = -1.0 if sign else 1.0
+    if be == f.exp_field_max():
+        return math.nan if fr else sg * math.inf
+    if be == 0:
+        return sg * 0.0 if fr == 0 else sg * math.ldexp(float(fr), f.emin() - f.sig_bits)
+    return sg * math.ldexp(float((1 << f.sig_bits) | fr), be - f.bias() - f.sig_bits)

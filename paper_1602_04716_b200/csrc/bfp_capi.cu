@@ -1,0 +1,380 @@
+// bfp_capi.cu -- the C ABI (include/bfpgpu.h): validation, dispatch to the
+// compiled per-format networks, the host-buffer pipeline.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/bfpgpu.h"
+#include "bfp_formats.h"
+#include "bfp_kernels.cuh"
+
+namespace bfpg {
+#define DECLARE_IMPL(E_, S_) const Impl* impl_##E_##_##S_(int rn, int ftz);
+BFP_FORMAT_LIST(DECLARE_IMPL)
+#undef DECLARE_IMPL
+}  // namespace bfpg
+
+using bfpg::Impl;
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<uint64_t> g_launches{0};
+
+bfp_status fail(bfp_status s, const char* what) {
+  g_err = what;
+  return s;
+}
+
+bfp_status cuda_status(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return BFP_OK;
+  if (e == cudaErrorNotSupported) return fail(BFP_EUNSUPPORTED, what);
+  g_err = std::string(what) + ": " + cudaGetErrorString(e);
+  return BFP_ECUDA;
+}
+
+// validate(), format.hpp:57-64
+bfp_status validate(const bfp_format* f) {
+  if (!f) return fail(BFP_EARG, "null format");
+  if (f->exp_bits < 2 || f->exp_bits > 11) return fail(BFP_EFORMAT, "exp_bits must be in [2, 11]");
+  if (f->sig_bits < 1 || f->sig_bits > 52) return fail(BFP_EFORMAT, "sig_bits must be in [1, 52]");
+  if (1 + f->exp_bits + f->sig_bits > 64)
+    return fail(BFP_EFORMAT, "1 + exp_bits + sig_bits must not exceed 64");
+  if (f->rounding > 1 || f->subnormals > 1) return fail(BFP_EFORMAT, "bad rounding / subnormal policy");
+  return BFP_OK;
+}
+
+const Impl* lookup(const bfp_format* f) {
+  const int rn = f->rounding == 1, ftz = f->subnormals == 1;
+#define LOOKUP(E_, S_) \
+  if (f->exp_bits == E_ && f->sig_bits == S_) return bfpg::impl_##E_##_##S_(rn, ftz);
+  BFP_FORMAT_LIST(LOOKUP)
+#undef LOOKUP
+  return nullptr;
+}
+
+bfp_status resolve(const bfp_format* f, const Impl** out) {
+  const bfp_status s = validate(f);
+  if (s != BFP_OK) return s;
+  const Impl* impl = lookup(f);
+  if (!impl) return fail(BFP_EUNSUPPORTED, "format has no compiled network");
+  *out = impl;
+  return BFP_OK;
+}
+
+size_t nplanes(const bfp_format* f) { return 1 + f->exp_bits + f->sig_bits; }
+size_t nblocks(size_t count) { return (count + 1023) / 1024; }
+
+}  // namespace
+
+extern "C" {
+
+const char* bfp_status_string(bfp_status s) {
+  switch (s) {
+    case BFP_OK: return "ok";
+    case BFP_EFORMAT: return "invalid format";
+    case BFP_EMISMATCH: return "operands must share one format spec";
+    case BFP_ESIZE: return "bad element count or length";
+    case BFP_EUNSUPPORTED: return "format not instantiated";
+    case BFP_ECUDA: return "CUDA error";
+    case BFP_EARG: return "bad argument";
+  }
+  return "unknown";
+}
+
+const char* bfp_last_error(void) { return g_err.c_str(); }
+
+bfp_status bfp_validate(const bfp_format* f) { return validate(f); }
+
+// require_same_shape compares the whole format_spec including its name
+// (format.hpp:54, arith.hpp:228-231).
+bfp_status bfp_same_shape(const bfp_format* a, const bfp_format* b) {
+  if (!a || !b) return fail(BFP_EARG, "null format");
+  const char* na = a->name ? a->name : "";
+  const char* nb = b->name ? b->name : "";
+  if (a->exp_bits != b->exp_bits || a->sig_bits != b->sig_bits || a->rounding != b->rounding ||
+      a->subnormals != b->subnormals || std::strcmp(na, nb) != 0)
+    return fail(BFP_EMISMATCH, "operands must share one format spec");
+  return BFP_OK;
+}
+
+int bfp_is_supported(const bfp_format* f) {
+  return validate(f) == BFP_OK && lookup(f) != nullptr;
+}
+
+size_t bfp_plane_bytes(const bfp_format* f, size_t count) {
+  if (validate(f) != BFP_OK) return 0;
+  return nblocks(count) * nplanes(f) * 128;
+}
+
+size_t bfp_enc_bytes(const bfp_format* f) {
+  if (validate(f) != BFP_OK) return 0;
+  const size_t n = nplanes(f);
+  return n <= 8 ? 1 : (n <= 16 ? 2 : (n <= 32 ? 4 : 8));
+}
+
+bfp_status bfp_arith(int op, const bfp_format* f, const uint32_t* d_x, const uint32_t* d_y,
+                     const uint32_t* d_c, uint32_t* d_z, size_t count, void* stream) {
+  const Impl* impl = nullptr;
+  const bfp_status s = resolve(f, &impl);
+  if (s != BFP_OK) return s;
+  if (op < 0 || op > 4) return fail(BFP_EARG, "bad op");
+  if (op == 3) return fail(BFP_EUNSUPPORTED, "div not compiled");
+  if (count == 0) return BFP_OK;
+  if (!d_x || !d_y || !d_z || (op == 4 && !d_c)) return fail(BFP_EARG, "null operand");
+  ++g_launches;
+  return cuda_status(impl->arith(op, d_x, d_y, d_c, d_z, nblocks(count),
+                                 static_cast<cudaStream_t>(stream)),
+                     "arith launch");
+}
+
+bfp_status bfp_add(const bfp_format* f, const uint32_t* x, const uint32_t* y, uint32_t* z,
+                   size_t count, void* stream) {
+  return bfp_arith(0, f, x, y, nullptr, z, count, stream);
+}
+bfp_status bfp_sub(const bfp_format* f, const uint32_t* x, const uint32_t* y, uint32_t* z,
+                   size_t count, void* stream) {
+  return bfp_arith(1, f, x, y, nullptr, z, count, stream);
+}
+bfp_status bfp_mul(const bfp_format* f, const uint32_t* x, const uint32_t* y, uint32_t* z,
+                   size_t count, void* stream) {
+  return bfp_arith(2, f, x, y, nullptr, z, count, stream);
+}
+bfp_status bfp_div(const bfp_format* f, const uint32_t* x, const uint32_t* y, uint32_t* z,
+                   size_t count, void* stream) {
+  return bfp_arith(3, f, x, y, nullptr, z, count, stream);
+}
+bfp_status bfp_mul_add(const bfp_format* f, const uint32_t* a, const uint32_t* b,
+                       const uint32_t* c, uint32_t* z, size_t count, void* stream) {
+  return bfp_arith(4, f, a, b, c, z, count, stream);
+}
+
+bfp_status bfp_pack_enc(const bfp_format* f, const void* d_enc, uint32_t* d_planes,
+                        size_t count, void* stream) {
+  const Impl* impl = nullptr;
+  const bfp_status s = resolve(f, &impl);
+  if (s != BFP_OK) return s;
+  if (count == 0) return BFP_OK;
+  if (!d_enc || !d_planes) return fail(BFP_EARG, "null buffer");
+  ++g_launches;
+  return cuda_status(impl->pack_enc(d_enc, d_planes, count, static_cast<cudaStream_t>(stream)),
+                     "pack_enc launch");
+}
+
+bfp_status bfp_unpack_enc(const bfp_format* f, const uint32_t* d_planes, void* d_enc,
+                          size_t count, void* stream) {
+  const Impl* impl = nullptr;
+  const bfp_status s = resolve(f, &impl);
+  if (s != BFP_OK) return s;
+  if (count == 0) return BFP_OK;
+  if (!d_enc || !d_planes) return fail(BFP_EARG, "null buffer");
+  ++g_launches;
+  return cuda_status(impl->unpack_enc(d_planes, d_enc, count, static_cast<cudaStream_t>(stream)),
+                     "unpack_enc launch");
+}
+
+bfp_status bfp_pack_f32(const bfp_format* f, const float* d_in, uint32_t* d_planes,
+                        size_t count, void* stream) {
+  const Impl* impl = nullptr;
+  const bfp_status s = resolve(f, &impl);
+  if (s != BFP_OK) return s;
+  if (count == 0) return BFP_OK;
+  if (!d_in || !d_planes) return fail(BFP_EARG, "null buffer");
+  ++g_launches;
+  return cuda_status(impl->pack_f32(d_in, d_planes, count, static_cast<cudaStream_t>(stream)),
+                     "pack_f32 launch");
+}
+
+bfp_status bfp_unpack_f32(const bfp_format* f, const uint32_t* d_planes, float* d_out,
+                          size_t count, void* stream) {
+  const Impl* impl = nullptr;
+  const bfp_status s = resolve(f, &impl);
+  if (s != BFP_OK) return s;
+  if (count == 0) return BFP_OK;
+  if (!d_out || !d_planes) return fail(BFP_EARG, "null buffer");
+  ++g_launches;
+  return cuda_status(impl->unpack_f32(d_planes, d_out, count, static_cast<cudaStream_t>(stream)),
+                     "unpack_f32 launch");
+}
+
+bfp_status bfp_kernel_attrs(const bfp_format* f, int kernel, int* regs, int* ctas_per_sm,
+                            int* threads_per_cta) {
+  const Impl* impl = nullptr;
+  const bfp_status s = resolve(f, &impl);
+  if (s != BFP_OK) return s;
+  const void* k = impl->kernel(kernel);
+  if (!k) return fail(BFP_EARG, "bad kernel id");
+  cudaFuncAttributes a;
+  cudaError_t e = cudaFuncGetAttributes(&a, k);
+  if (e != cudaSuccess) return cuda_status(e, "cudaFuncGetAttributes");
+  if (regs) *regs = a.numRegs;
+  if (threads_per_cta) *threads_per_cta = bfpg::kThreads;
+  if (ctas_per_sm) {
+    int occ = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, bfpg::kThreads, 0);
+    if (e != cudaSuccess) return cuda_status(e, "occupancy");
+    *ctas_per_sm = occ;
+  }
+  return BFP_OK;
+}
+
+uint64_t bfp_launch_count(void) { return g_launches.load(); }
+
+// ------------------------------------------------------------ host pipeline
+struct bfp_host_ctx {
+  static constexpr int kDepth = 3;
+  size_t chunk_blocks = 0;
+  size_t cap_bytes = 0;  // per buffer
+  cudaStream_t st[kDepth] = {};
+  void* in[kDepth][3] = {};
+  void* out[kDepth] = {};
+  int dev = 0;
+};
+
+bfp_host_ctx* bfp_host_ctx_create(size_t chunk_elems) {
+  if (!chunk_elems) chunk_elems = size_t(1) << 22;
+  auto* c = new bfp_host_ctx;
+  c->chunk_blocks = (chunk_elems + 1023) / 1024;
+  // sized for the widest case: 32 planes or float32 elements
+  c->cap_bytes = c->chunk_blocks * 1024 * 4;
+  cudaGetDevice(&c->dev);
+  for (int i = 0; i < bfp_host_ctx::kDepth; ++i) {
+    if (cudaStreamCreateWithFlags(&c->st[i], cudaStreamNonBlocking) != cudaSuccess) goto bad;
+    for (int k = 0; k < 3; ++k)
+      if (cudaMalloc(&c->in[i][k], c->cap_bytes) != cudaSuccess) goto bad;
+    if (cudaMalloc(&c->out[i], c->cap_bytes) != cudaSuccess) goto bad;
+  }
+  return c;
+bad:
+  g_err = "bfp_host_ctx_create: allocation failed";
+  bfp_host_ctx_destroy(c);
+  return nullptr;
+}
+
+void bfp_host_ctx_destroy(bfp_host_ctx* c) {
+  if (!c) return;
+  for (int i = 0; i < bfp_host_ctx::kDepth; ++i) {
+    if (c->st[i]) cudaStreamSynchronize(c->st[i]);
+    for (int k = 0; k < 3; ++k)
+      if (c->in[i][k]) cudaFree(c->in[i][k]);
+    if (c->out[i]) cudaFree(c->out[i]);
+    if (c->st[i]) cudaStreamDestroy(c->st[i]);
+  }
+  delete c;
+}
+
+}  // extern "C"
+
+namespace {
+
+// Generic chunked pipeline: chunk k uses stream/buffer set k % depth, so the
+// H2D of chunk k+1, the kernel of chunk k and the D2H of chunk k-1 overlap.
+// in_stride / out_stride: bytes per 1024-element block on each side.
+template <typename Body>
+bfp_status host_pipeline(bfp_host_ctx* c, size_t count, int n_in, const void* const* h_in,
+                         size_t in_stride, void* h_out, size_t out_stride, bool out_elems,
+                         Body body) {
+  if (!c) return fail(BFP_EARG, "null host context");
+  const size_t blocks = nblocks(count);
+  for (size_t b0 = 0, k = 0; b0 < blocks; b0 += c->chunk_blocks, ++k) {
+    const int i = int(k % bfp_host_ctx::kDepth);
+    const size_t nb = (blocks - b0 < c->chunk_blocks) ? blocks - b0 : c->chunk_blocks;
+    const size_t e0 = b0 * 1024;
+    const size_t ecount = (count - e0 < nb * 1024) ? count - e0 : nb * 1024;
+    for (int a = 0; a < n_in; ++a) {
+      const size_t bytes = in_stride ? nb * in_stride : ecount * 4;
+      const char* src = static_cast<const char*>(h_in[a]) + (in_stride ? b0 * in_stride : e0 * 4);
+      cudaError_t e = cudaMemcpyAsync(c->in[i][a], src, bytes, cudaMemcpyHostToDevice, c->st[i]);
+      if (e != cudaSuccess) return cuda_status(e, "H2D");
+    }
+    const bfp_status s = body(i, ecount, c->st[i]);
+    if (s != BFP_OK) return s;
+    const size_t obytes = out_elems ? ecount * 4 : nb * out_stride;
+    char* dst = static_cast<char*>(h_out) + (out_elems ? e0 * 4 : b0 * out_stride);
+    cudaError_t e = cudaMemcpyAsync(dst, c->out[i], obytes, cudaMemcpyDeviceToHost, c->st[i]);
+    if (e != cudaSuccess) return cuda_status(e, "D2H");
+  }
+  for (int i = 0; i < bfp_host_ctx::kDepth; ++i) {
+    cudaError_t e = cudaStreamSynchronize(c->st[i]);
+    if (e != cudaSuccess) return cuda_status(e, "sync");
+  }
+  return BFP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+bfp_status bfp_arith_host(bfp_host_ctx* c, int op, const bfp_format* f, const uint32_t* h_x,
+                          const uint32_t* h_y, const uint32_t* h_c, uint32_t* h_z,
+                          size_t count) {
+  const Impl* impl = nullptr;
+  bfp_status s = resolve(f, &impl);
+  if (s != BFP_OK) return s;
+  if (op < 0 || op > 4 || op == 3) return fail(BFP_EUNSUPPORTED, "op");
+  if (!h_x || !h_y || !h_z || (op == 4 && !h_c)) return fail(BFP_EARG, "null operand");
+  const size_t stride = nplanes(f) * 128;
+  const void* ins[3] = {h_x, h_y, h_c};
+  return host_pipeline(c, count, op == 4 ? 3 : 2, ins, stride, h_z, stride, false,
+                       [&](int i, size_t ecount, cudaStream_t st) {
+                         ++g_launches;
+                         return cuda_status(
+                             impl->arith(op, static_cast<const uint32_t*>(c->in[i][0]),
+                                         static_cast<const uint32_t*>(c->in[i][1]),
+                                         static_cast<const uint32_t*>(c->in[i][2]),
+                                         static_cast<uint32_t*>(c->out[i]), nblocks(ecount), st),
+                             "arith launch");
+                       });
+}
+
+bfp_status bfp_pack_f32_host(bfp_host_ctx* c, const bfp_format* f, const float* h_in,
+                             uint32_t* h_planes, size_t count) {
+  const Impl* impl = nullptr;
+  bfp_status s = resolve(f, &impl);
+  if (s != BFP_OK) return s;
+  if (!h_in || !h_planes) return fail(BFP_EARG, "null buffer");
+  const void* ins[1] = {h_in};
+  return host_pipeline(c, count, 1, ins, 0, h_planes, nplanes(f) * 128, false,
+                       [&](int i, size_t ecount, cudaStream_t st) {
+                         ++g_launches;
+                         return cuda_status(impl->pack_f32(static_cast<const float*>(c->in[i][0]),
+                                                           static_cast<uint32_t*>(c->out[i]),
+                                                           ecount, st),
+                                            "pack_f32 launch");
+                       });
+}
+
+bfp_status bfp_unpack_f32_host(bfp_host_ctx* c, const bfp_format* f, const uint32_t* h_planes,
+                               float* h_out, size_t count) {
+  const Impl* impl = nullptr;
+  bfp_status s = resolve(f, &impl);
+  if (s != BFP_OK) return s;
+  if (!h_out || !h_planes) return fail(BFP_EARG, "null buffer");
+  const void* ins[1] = {h_planes};
+  return host_pipeline(c, count, 1, ins, nplanes(f) * 128, h_out, 0, true,
+                       [&](int i, size_t ecount, cudaStream_t st) {
+                         ++g_launches;
+                         return cuda_status(
+                             impl->unpack_f32(static_cast<const uint32_t*>(c->in[i][0]),
+                                              static_cast<float*>(c->out[i]), ecount, st),
+                             "unpack_f32 launch");
+                       });
+}
+
+void* bfp_host_alloc(size_t bytes) {
+  void* p = nullptr;
+  if (cudaMallocHost(&p, bytes) != cudaSuccess) {
+    g_err = "cudaMallocHost failed";
+    return nullptr;
+  }
+  return p;
+}
+
+void bfp_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
+}  // extern "C"

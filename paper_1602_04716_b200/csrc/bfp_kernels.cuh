@@ -1,0 +1,343 @@
+// bfp_kernels.cuh -- sm_100a kernels over the slice-major plane layout.
+//
+// Arithmetic (add / sub / mul / mul_add): one thread per 32-element unit.
+// A warp owns one 1024-element block: for every plane the 32 threads read 32
+// consecutive words (one 128-B line), evaluate the format's unrolled LOP3
+// network in registers and write 32 consecutive words.  Loads use the
+// streaming / evict-first path (ld.global.cs): every byte is touched once.
+// The grid is persistent (a multiple of the SM count, from the occupancy
+// calculator) and strides over units.
+//
+// pack / unpack: one thread per unit transposes 32 elements in registers
+// (bfp_layout.cuh); the plane side of every access is coalesced, the element
+// side is a 32..128-B contiguous chunk per thread (vector loads).
+#pragma once
+#include <cuda_runtime.h>
+
+#include "bfp_circuits.cuh"
+#include "bfp_layout.cuh"
+
+namespace bfpg {
+
+enum Op { OP_ADD = 0, OP_SUB = 1, OP_MUL = 2, OP_DIV = 3, OP_MUL_ADD = 4 };
+
+constexpr int kThreads = 128;
+
+__device__ __forceinline__ w32 ld_stream(const w32* p) { return __ldcs(p); }
+__device__ __forceinline__ void st_stream(w32* p, w32 v) { __stcs(p, v); }
+
+template <class F, int OP>
+__global__ void __launch_bounds__(kThreads) k_arith(const w32* __restrict__ x,
+                                                    const w32* __restrict__ y,
+                                                    const w32* __restrict__ c,
+                                                    w32* __restrict__ z, size_t units) {
+  constexpr int N = F::N;
+  const size_t stride = size_t(gridDim.x) * kThreads;
+  for (size_t u = size_t(blockIdx.x) * kThreads + threadIdx.x; u < units; u += stride) {
+    const size_t base = (u >> 5) * (size_t(N) * 32) + (u & 31);
+    w32 X[N], Y[N], Z[N];
+    BFP_UNROLL for (int j = 0; j < N; ++j) {
+      X[j] = ld_stream(x + base + j * 32);
+      Y[j] = ld_stream(y + base + j * 32);
+    }
+    if constexpr (OP == OP_ADD) {
+      add_w<F, false>(X, Y, Z);
+    } else if constexpr (OP == OP_SUB) {
+      add_w<F, true>(X, Y, Z);
+    } else if constexpr (OP == OP_MUL) {
+      mul_w<F>(X, Y, Z);
+    } else {
+      w32 Cc[N];
+      BFP_UNROLL for (int j = 0; j < N; ++j) Cc[j] = ld_stream(c + base + j * 32);
+      mul_add_w<F>(X, Y, Cc, Z);
+    }
+    BFP_UNROLL for (int j = 0; j < N; ++j) st_stream(z + base + j * 32, Z[j]);
+  }
+}
+
+// ------------------------------------------------------------------ pack
+// Loads the 32 encodings of unit u (element width EB bytes) into w32 words,
+// zero beyond n.  Fast path: 16-B vector loads when the unit is complete.
+template <int EB>
+__device__ __forceinline__ void load_unit(const uint8_t* __restrict__ enc, size_t u, size_t n,
+                                          bool aligned, w32* L) {
+  constexpr int WORDS = 32 * EB / 4;
+  const size_t e0 = u * 32;
+  if (aligned && e0 + 32 <= n) {
+    const uint4* p = reinterpret_cast<const uint4*>(enc + e0 * EB);
+    BFP_UNROLL for (int i = 0; i < WORDS / 4; ++i) {
+      const uint4 q = __ldcs(p + i);
+      L[4 * i] = q.x;
+      L[4 * i + 1] = q.y;
+      L[4 * i + 2] = q.z;
+      L[4 * i + 3] = q.w;
+    }
+  } else {
+    BFP_UNROLL for (int i = 0; i < WORDS; ++i) L[i] = 0;
+    for (int k = 0; k < 32; ++k) {
+      if (e0 + k < n) {
+        w32 v = 0;
+        for (int b = 0; b < EB; ++b) v |= w32(enc[(e0 + k) * EB + b]) << (8 * b);
+        const int bit = (k * EB * 8) & 31;
+        L[(k * EB) / 4] |= (EB == 4) ? v : (v << bit);
+      }
+    }
+  }
+}
+
+template <int EB>
+__device__ __forceinline__ void store_unit(uint8_t* __restrict__ enc, size_t u, size_t n,
+                                           bool aligned, const w32* L) {
+  constexpr int WORDS = 32 * EB / 4;
+  const size_t e0 = u * 32;
+  if (e0 >= n) return;
+  if (aligned && e0 + 32 <= n) {
+    uint4* p = reinterpret_cast<uint4*>(enc + e0 * EB);
+    BFP_UNROLL for (int i = 0; i < WORDS / 4; ++i)
+      __stcs(p + i, make_uint4(L[4 * i], L[4 * i + 1], L[4 * i + 2], L[4 * i + 3]));
+  } else {
+    for (int k = 0; k < 32 && e0 + k < n; ++k) {
+      const w32 w = L[(k * EB) / 4] >> ((k * EB * 8) & 31);
+      for (int b = 0; b < EB; ++b) enc[(e0 + k) * EB + b] = uint8_t(w >> (8 * b));
+    }
+  }
+}
+
+// Raw encodings (EB = 1/2/4 bytes each) -> planes.  Every unit of every
+// block is written; elements >= n are zero (pack.hpp:50).
+template <int N, int EB>
+__global__ void __launch_bounds__(kThreads) k_pack_enc(const uint8_t* __restrict__ enc,
+                                                       w32* __restrict__ planes, size_t n,
+                                                       size_t units, bool aligned) {
+  const size_t stride = size_t(gridDim.x) * kThreads;
+  for (size_t u = size_t(blockIdx.x) * kThreads + threadIdx.x; u < units; u += stride) {
+    w32 L[32 * EB / 4];
+    load_unit<EB>(enc, u, n, aligned, L);
+    w32 P[32];
+    if constexpr (EB == 1) {
+      enc8_to_planes(L, P);
+    } else if constexpr (EB == 2) {
+      enc16_to_planes(L, P);
+    } else {
+      BFP_UNROLL for (int i = 0; i < 32; ++i) P[i] = L[i];
+      enc32_to_planes(P);
+    }
+    const size_t base = (u >> 5) * (size_t(N) * 32) + (u & 31);
+    BFP_UNROLL for (int j = 0; j < N; ++j) st_stream(planes + base + j * 32, P[j]);
+  }
+}
+
+template <int N, int EB>
+__global__ void __launch_bounds__(kThreads) k_unpack_enc(const w32* __restrict__ planes,
+                                                         uint8_t* __restrict__ enc, size_t n,
+                                                         size_t units, bool aligned) {
+  const size_t stride = size_t(gridDim.x) * kThreads;
+  for (size_t u = size_t(blockIdx.x) * kThreads + threadIdx.x; u < units; u += stride) {
+    const size_t base = (u >> 5) * (size_t(N) * 32) + (u & 31);
+    w32 P[32];
+    BFP_UNROLL for (int j = 0; j < 32; ++j) P[j] = (j < N) ? ld_stream(planes + base + j * 32) : 0u;
+    w32 L[32 * EB / 4];
+    if constexpr (EB == 1) {
+      planes_to_enc8(P, L);
+    } else if constexpr (EB == 2) {
+      planes_to_enc16(P, L);
+    } else {
+      planes_to_enc32(P);
+      BFP_UNROLL for (int i = 0; i < 32; ++i) L[i] = P[i];
+    }
+    store_unit<EB>(enc, u, n, aligned, L);
+  }
+}
+
+// float32 -> encode_scalar -> planes.
+template <class F>
+__global__ void __launch_bounds__(kThreads) k_pack_f32(const float* __restrict__ in,
+                                                       w32* __restrict__ planes, size_t n,
+                                                       size_t units, bool aligned) {
+  constexpr int N = F::N;
+  const size_t stride = size_t(gridDim.x) * kThreads;
+  const uint8_t* inb = reinterpret_cast<const uint8_t*>(in);
+  for (size_t u = size_t(blockIdx.x) * kThreads + threadIdx.x; u < units; u += stride) {
+    w32 V[32];
+    load_unit<4>(inb, u, n, aligned, V);
+    BFP_UNROLL for (int k = 0; k < 32; ++k) V[k] = encode_f32<F>(V[k]);  // +0 -> 0 on the tail
+    w32 P[32];
+    if constexpr (N <= 8) {
+      w32 L[8];
+      BFP_UNROLL for (int q = 0; q < 8; ++q)
+        L[q] = V[4 * q] | (V[4 * q + 1] << 8) | (V[4 * q + 2] << 16) | (V[4 * q + 3] << 24);
+      enc8_to_planes(L, P);
+    } else if constexpr (N <= 16) {
+      w32 L[16];
+      BFP_UNROLL for (int q = 0; q < 16; ++q) L[q] = V[2 * q] | (V[2 * q + 1] << 16);
+      enc16_to_planes(L, P);
+    } else {
+      BFP_UNROLL for (int i = 0; i < 32; ++i) P[i] = V[i];
+      enc32_to_planes(P);
+    }
+    const size_t base = (u >> 5) * (size_t(N) * 32) + (u & 31);
+    BFP_UNROLL for (int j = 0; j < N; ++j) st_stream(planes + base + j * 32, P[j]);
+  }
+}
+
+// planes -> decode_scalar -> float32.
+template <class F>
+__global__ void __launch_bounds__(kThreads) k_unpack_f32(const w32* __restrict__ planes,
+                                                         float* __restrict__ out, size_t n,
+                                                         size_t units, bool aligned) {
+  constexpr int N = F::N;
+  const size_t stride = size_t(gridDim.x) * kThreads;
+  uint8_t* outb = reinterpret_cast<uint8_t*>(out);
+  for (size_t u = size_t(blockIdx.x) * kThreads + threadIdx.x; u < units; u += stride) {
+    const size_t base = (u >> 5) * (size_t(N) * 32) + (u & 31);
+    w32 P[32];
+    BFP_UNROLL for (int j = 0; j < 32; ++j) P[j] = (j < N) ? ld_stream(planes + base + j * 32) : 0u;
+    w32 V[32];
+    if constexpr (N <= 8) {
+      w32 L[8];
+      planes_to_enc8(P, L);
+      BFP_UNROLL for (int k = 0; k < 32; ++k) V[k] = (L[k >> 2] >> (8 * (k & 3))) & 0xffu;
+    } else if constexpr (N <= 16) {
+      w32 L[16];
+      planes_to_enc16(P, L);
+      BFP_UNROLL for (int k = 0; k < 32; ++k) V[k] = (L[k >> 1] >> (16 * (k & 1))) & 0xffffu;
+    } else {
+      planes_to_enc32(P);
+      BFP_UNROLL for (int k = 0; k < 32; ++k) V[k] = P[k];
+    }
+    BFP_UNROLL for (int k = 0; k < 32; ++k) V[k] = decode_f32<F>(V[k]);
+    store_unit<4>(outb, u, n, aligned, V);
+  }
+}
+
+// ------------------------------------------------------- launch + table
+// Resident CTAs for a full wave of `kernel`: #SM x occupancy.
+template <typename K>
+inline int wave_ctas(K kernel) {
+  int dev = 0, sms = 0, occ = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (sms <= 0) sms = 148;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kThreads, 0);
+  if (occ <= 0) occ = 1;
+  return sms * occ;
+}
+
+inline int grid_for(int wave, size_t units) {
+  const size_t need = (units + kThreads - 1) / kThreads;
+  return int(need < size_t(wave) ? (need ? need : 1) : size_t(wave));
+}
+
+// Per-format entry points (instantiated in inst/fmt_E_S.cu).
+struct Impl {
+  cudaError_t (*arith)(int op, const w32* x, const w32* y, const w32* c, w32* z, size_t nblocks,
+                       cudaStream_t st);
+  cudaError_t (*pack_enc)(const void* enc, w32* planes, size_t n, cudaStream_t st);
+  cudaError_t (*unpack_enc)(const w32* planes, void* enc, size_t n, cudaStream_t st);
+  cudaError_t (*pack_f32)(const float* in, w32* planes, size_t n, cudaStream_t st);
+  cudaError_t (*unpack_f32)(const w32* planes, float* out, size_t n, cudaStream_t st);
+  const void* (*kernel)(int op);  // device function handle (for attribute queries)
+};
+
+template <class F>
+struct FormatImpl {
+  static constexpr int N = F::N;
+  static constexpr int EB = N <= 8 ? 1 : (N <= 16 ? 2 : 4);
+
+  template <int OP>
+  static cudaError_t launch_arith(const w32* x, const w32* y, const w32* c, w32* z, size_t units,
+                                  cudaStream_t st) {
+    auto k = k_arith<F, OP>;
+    static const int wave = wave_ctas(k);
+    k<<<grid_for(wave, units), kThreads, 0, st>>>(x, y, c, z, units);
+    return cudaGetLastError();
+  }
+  static cudaError_t arith(int op, const w32* x, const w32* y, const w32* c, w32* z,
+                           size_t nblocks, cudaStream_t st) {
+    const size_t units = nblocks * 32;
+    if (!units) return cudaSuccess;
+    switch (op) {
+      case OP_ADD: return launch_arith<OP_ADD>(x, y, c, z, units, st);
+      case OP_SUB: return launch_arith<OP_SUB>(x, y, c, z, units, st);
+      case OP_MUL: return launch_arith<OP_MUL>(x, y, c, z, units, st);
+      case OP_MUL_ADD: return launch_arith<OP_MUL_ADD>(x, y, c, z, units, st);
+      default: return cudaErrorInvalidValue;
+    }
+  }
+  static const void* kernel(int op) {
+    switch (op) {
+      case OP_ADD: return reinterpret_cast<const void*>(k_arith<F, OP_ADD>);
+      case OP_SUB: return reinterpret_cast<const void*>(k_arith<F, OP_SUB>);
+      case OP_MUL: return reinterpret_cast<const void*>(k_arith<F, OP_MUL>);
+      case OP_MUL_ADD: return reinterpret_cast<const void*>(k_arith<F, OP_MUL_ADD>);
+      case 10: return reinterpret_cast<const void*>(k_pack_enc<N, EB>);
+      case 11: return reinterpret_cast<const void*>(k_unpack_enc<N, EB>);
+      case 12: return reinterpret_cast<const void*>(k_pack_f32<F>);
+      case 13: return reinterpret_cast<const void*>(k_unpack_f32<F>);
+      default: return nullptr;
+    }
+  }
+  static size_t units_for(size_t n) { return ((n + 1023) / 1024) * 32; }
+  static cudaError_t pack_enc(const void* enc, w32* planes, size_t n, cudaStream_t st) {
+    const size_t units = units_for(n);
+    if (!units) return cudaSuccess;
+    const bool al = (reinterpret_cast<uintptr_t>(enc) & 15) == 0;
+    auto k = k_pack_enc<N, EB>;
+    static const int wave = wave_ctas(k);
+    k<<<grid_for(wave, units), kThreads, 0, st>>>(static_cast<const uint8_t*>(enc), planes, n,
+                                                      units, al);
+    return cudaGetLastError();
+  }
+  static cudaError_t unpack_enc(const w32* planes, void* enc, size_t n, cudaStream_t st) {
+    const size_t units = (n + 31) / 32;
+    if (!units) return cudaSuccess;
+    const bool al = (reinterpret_cast<uintptr_t>(enc) & 15) == 0;
+    auto k = k_unpack_enc<N, EB>;
+    static const int wave = wave_ctas(k);
+    k<<<grid_for(wave, units), kThreads, 0, st>>>(planes, static_cast<uint8_t*>(enc), n, units,
+                                                      al);
+    return cudaGetLastError();
+  }
+  static cudaError_t pack_f32(const float* in, w32* planes, size_t n, cudaStream_t st) {
+    if constexpr (F::E > 8 || F::S > 23) {
+      return cudaErrorNotSupported;
+    } else {
+      const size_t units = units_for(n);
+      if (!units) return cudaSuccess;
+      const bool al = (reinterpret_cast<uintptr_t>(in) & 15) == 0;
+      auto k = k_pack_f32<F>;
+      static const int wave = wave_ctas(k);
+      k<<<grid_for(wave, units), kThreads, 0, st>>>(in, planes, n, units, al);
+      return cudaGetLastError();
+    }
+  }
+  static cudaError_t unpack_f32(const w32* planes, float* out, size_t n, cudaStream_t st) {
+    if constexpr (F::E > 8 || F::S > 23) {
+      return cudaErrorNotSupported;
+    } else {
+      const size_t units = (n + 31) / 32;
+      if (!units) return cudaSuccess;
+      const bool al = (reinterpret_cast<uintptr_t>(out) & 15) == 0;
+      auto k = k_unpack_f32<F>;
+      static const int wave = wave_ctas(k);
+      k<<<grid_for(wave, units), kThreads, 0, st>>>(planes, out, n, units, al);
+      return cudaGetLastError();
+    }
+  }
+  static const Impl* get() {
+    static const Impl impl = {&arith, &pack_enc, &unpack_enc, &pack_f32, &unpack_f32, &kernel};
+    return &impl;
+  }
+};
+
+}  // namespace bfpg
+
+#define BFP_INSTANTIATE(E_, S_)                                                       \
+  namespace bfpg {                                                                    \
+  const Impl* impl_##E_##_##S_(int rn, int ftz) {                                     \
+    if (rn && !ftz) return FormatImpl<Format<E_, S_, true, false>>::get();            \
+    if (rn && ftz) return FormatImpl<Format<E_, S_, true, true>>::get();              \
+    if (!rn && !ftz) return FormatImpl<Format<E_, S_, false, false>>::get();          \
+    return FormatImpl<Format<E_, S_, false, true>>::get();                            \
+  }                                                                                   \
+  }

@@ -1,0 +1,223 @@
+// bfp_layout.cuh -- standard <-> bitslice transposition and the scalar codec.
+//
+// Layout (the memory image of an array of bitfield<lane<1024>>, bitfield.hpp
+// :10-28 / pack.hpp:13-15): element i, plane j lives in u32 word
+//   ((i >> 10) * N + j) * 32 + ((i >> 5) & 31),  bit (i & 31).
+// A "unit" is one 32-element column of a 1024-element block; one thread owns
+// one unit, so its N plane words are 128 B apart and a warp's 32 threads
+// cover a block with one coalesced 128-B access per plane.
+//
+// Transposition is a 32x32 bit-matrix transpose held in one thread's
+// registers: five commuting exchange stages (16, 8, 4, 2, 1), each swapping
+// row-index bit k with column-index bit k (LSB-first indexing: bit c of row r
+// <-> bit r of row c).  The reference's transpose64 (pack.hpp:28-39) uses
+// MSB-first block swaps on LSB-first data and so computes the anti-diagonal
+// transpose; this one is checked against field_from_elements
+// / element_of (bitfield.hpp:33-52).  Byte- and half-word stages are done
+// with PRMT (__byte_perm) when the encodings are 8 or 16 bits wide.
+//
+// The codec follows encode_scalar / decode_scalar (format.hpp:101-188) for
+// binary32 inputs / outputs.
+#pragma once
+#include "bfp_circuits.cuh"
+
+namespace bfpg {
+
+// One exchange stage of distance D over rows [0, R) (R a multiple of 2D).
+template <int D, int R>
+BFP_HD void xpose_stage(w32* v) {
+  constexpr w32 m = D == 16 ? 0x0000ffffu
+                  : D == 8  ? 0x00ff00ffu
+                  : D == 4  ? 0x0f0f0f0fu
+                  : D == 2  ? 0x33333333u
+                            : 0x55555555u;
+  BFP_UNROLL for (int k = 0; k < R; ++k) {
+    if (k & D) continue;
+    const w32 a = v[k], b = v[k + D];
+    v[k] = (a & m) | ((b << D) & ~m);
+    v[k + D] = ((a >> D) & m) | (b & ~m);
+  }
+}
+
+// Full 32x32 transpose (rows known to be zero fold away at compile time).
+BFP_HD void xpose32(w32* v) {
+  xpose_stage<16, 32>(v);
+  xpose_stage<8, 32>(v);
+  xpose_stage<4, 32>(v);
+  xpose_stage<2, 32>(v);
+  xpose_stage<1, 32>(v);
+}
+
+#if defined(__CUDACC__)
+BFP_HD w32 prmt(w32 a, w32 b, w32 sel) {
+#if defined(__CUDA_ARCH__)
+  return __byte_perm(a, b, sel);
+#else
+  const uint64_t x = (uint64_t(b) << 32) | a;
+  w32 r = 0;
+  for (int i = 0; i < 4; ++i) r |= w32((x >> (8 * ((sel >> (4 * i)) & 7))) & 0xff) << (8 * i);
+  return r;
+#endif
+}
+#else
+inline w32 prmt(w32 a, w32 b, w32 sel) {
+  const uint64_t x = (uint64_t(b) << 32) | a;
+  w32 r = 0;
+  for (int i = 0; i < 4; ++i) r |= w32((x >> (8 * ((sel >> (4 * i)) & 7))) & 0xff) << (8 * i);
+  return r;
+}
+#endif
+
+// 32 encodings of <= 8 bits, packed 4 per word (L[q] byte i = element 4q+i)
+// -> planes P[0..8).
+BFP_HD void enc8_to_planes(const w32* L, w32* P) {
+  w32 v[8];
+  BFP_UNROLL for (int k = 0; k < 8; ++k) {
+    const int q = k >> 2, b = k & 3;
+    const w32 sel = w32(b) | (w32(b + 4) << 4);  // byte b of a, byte b of b
+    const w32 r1 = prmt(L[q], L[q + 2], sel);      // e_k, e_{k+8}
+    const w32 r2 = prmt(L[q + 4], L[q + 6], sel);  // e_{k+16}, e_{k+24}
+    v[k] = prmt(r1, r2, 0x5410);
+  }
+  xpose_stage<4, 8>(v);
+  xpose_stage<2, 8>(v);
+  xpose_stage<1, 8>(v);
+  BFP_UNROLL for (int j = 0; j < 8; ++j) P[j] = v[j];
+}
+
+BFP_HD void planes_to_enc8(const w32* P, w32* L) {
+  w32 v[8];
+  BFP_UNROLL for (int j = 0; j < 8; ++j) v[j] = P[j];
+  xpose_stage<1, 8>(v);
+  xpose_stage<2, 8>(v);
+  xpose_stage<4, 8>(v);
+  // v[k] = [e_k, e_{k+8}, e_{k+16}, e_{k+24}]; L[q] = [e_4q .. e_4q+3]
+  BFP_UNROLL for (int q = 0; q < 8; ++q) {
+    const int k0 = (4 * q) & 7, byte = (4 * q) >> 3;  // element 4q is byte `byte` of v[k0]
+    // elements 4q..4q+3 are byte `byte` of v[k0..k0+3]
+    const w32 s = w32(byte) | (w32(byte + 4) << 4);
+    const w32 r1 = prmt(v[k0], v[k0 + 1], s);
+    const w32 r2 = prmt(v[k0 + 2], v[k0 + 3], s);
+    L[q] = prmt(r1, r2, 0x5410);
+  }
+}
+
+// 32 encodings of <= 16 bits, 2 per word (L[q] = e_2q | e_2q+1 << 16)
+// -> planes P[0..16).
+BFP_HD void enc16_to_planes(const w32* L, w32* P) {
+  w32 v[16];
+  BFP_UNROLL for (int k = 0; k < 16; ++k) {
+    const int q = k >> 1;
+    v[k] = (k & 1) ? prmt(L[q], L[q + 8], 0x7632) : prmt(L[q], L[q + 8], 0x5410);
+  }
+  xpose_stage<8, 16>(v);
+  xpose_stage<4, 16>(v);
+  xpose_stage<2, 16>(v);
+  xpose_stage<1, 16>(v);
+  BFP_UNROLL for (int j = 0; j < 16; ++j) P[j] = v[j];
+}
+
+BFP_HD void planes_to_enc16(const w32* P, w32* L) {
+  w32 v[16];
+  BFP_UNROLL for (int j = 0; j < 16; ++j) v[j] = P[j];
+  xpose_stage<1, 16>(v);
+  xpose_stage<2, 16>(v);
+  xpose_stage<4, 16>(v);
+  xpose_stage<8, 16>(v);
+  // v[k] = e_k | e_{k+16} << 16  (k < 16)
+  BFP_UNROLL for (int q = 0; q < 16; ++q) {
+    const int k0 = (2 * q) & 15, hi = (2 * q) >> 4;
+    L[q] = hi ? prmt(v[k0], v[k0 + 1], 0x7632) : prmt(v[k0], v[k0 + 1], 0x5410);
+  }
+}
+
+// 32 encodings of <= 32 bits, one per word -> planes (in place).
+BFP_HD void enc32_to_planes(w32* v) { xpose32(v); }
+BFP_HD void planes_to_enc32(w32* v) { xpose32(v); }
+
+// ------------------------------------------------------------- codec
+// encode_scalar((double)f) for a binary32 input f (format.hpp:125-188):
+// correctly rounded, overflow Inf (RN) / max-finite (RZ), FTZ after rounding,
+// NaN -> canonical (positive, fraction MSB).
+template <class F>
+BFP_HD w32 encode_f32(w32 u) {
+  constexpr int E = F::E, S = F::S;
+  constexpr int EMIN = 1 - F::BIAS, EMAX = F::BIAS;
+  constexpr w32 EMASK = (1u << E) - 1;
+  const w32 sign = (u >> 31) << (E + S);
+  const w32 a = u & 0x7fffffffu;
+  if (a >= 0x7f800000u) {
+    if (a > 0x7f800000u) return (EMASK << S) | (1u << (S - 1));
+    return sign | (EMASK << S);
+  }
+  if (a == 0) return sign;
+  const int ef = int(a >> 23);
+  const w32 sig = ef ? ((a & 0x7fffffu) | 0x800000u) : a;
+  const int exp2 = (ef ? ef : 1) - 150;  // value = sig * 2^exp2
+#if defined(__CUDA_ARCH__)
+  const int msb = 31 - __clz(sig);
+#else
+  const int msb = 31 - __builtin_clz(sig);
+#endif
+  const int unb = exp2 + msb;
+  const int ulp_exp = (unb >= EMIN ? unb : EMIN) - S;
+  const int shift = ulp_exp - exp2;
+  uint64_t kept;
+  w32 guard = 0, sticky = 0;
+  if (shift <= 0) {
+    kept = uint64_t(sig) << (-shift);
+  } else if (shift > 32) {
+    kept = 0;
+    sticky = 1;
+  } else {
+    kept = shift == 32 ? 0 : (sig >> shift);
+    guard = (sig >> (shift - 1)) & 1u;
+    sticky = (shift > 1) ? ((sig & ((1u << (shift - 1)) - 1u)) != 0) : 0u;
+  }
+  if (F::RN && guard && (sticky || (kept & 1u))) ++kept;
+  int res_exp = ulp_exp + S;
+  if (kept >= (uint64_t(2) << S)) {
+    kept >>= 1;
+    ++res_exp;
+  }
+  if (kept == 0) return sign;
+  if (kept < (uint64_t(1) << S)) {
+    if (F::FTZ) return sign;
+    return sign | w32(kept);
+  }
+  if (res_exp > EMAX) {
+    if (F::RN) return sign | (EMASK << S);
+    return sign | ((EMASK - 1) << S) | ((1u << S) - 1u);
+  }
+  return sign | (w32(res_exp + F::BIAS) << S) | (w32(kept) & ((1u << S) - 1u));
+}
+
+// (float)decode_scalar(enc) as binary32 bits (format.hpp:101-123); every
+// value of a format with E <= 8, S <= 23 is exact in binary32.  NaN ->
+// quiet_NaN() -> 0x7fc00000.
+template <class F>
+BFP_HD w32 decode_f32(w32 enc) {
+  constexpr int E = F::E, S = F::S;
+  constexpr w32 EMASK = (1u << E) - 1;
+  const w32 sign = ((enc >> (E + S)) & 1u) << 31;
+  const w32 be = (enc >> S) & EMASK;
+  const w32 fr = enc & ((1u << S) - 1u);
+  if (be == EMASK) return fr ? 0x7fc00000u : (sign | 0x7f800000u);
+  if (be == 0) {
+    if (fr == 0) return sign;
+#if defined(__CUDA_ARCH__)
+    const int p = 31 - __clz(fr);
+#else
+    const int p = 31 - __builtin_clz(fr);
+#endif
+    const int fexp = p + (1 - F::BIAS) - S + 127;  // biased binary32 exponent
+    constexpr int SUBSH = (1 - F::BIAS) - S + 149;  // binary32-subnormal placement
+    if constexpr (SUBSH < 32) {
+      if (fexp < 1) return sign | (fr << SUBSH);
+    }
+    return sign | (w32(fexp) << 23) | ((fr << (23 - p)) & 0x7fffffu);
+  }
+  return sign | (w32(int(be) - F::BIAS + 127) << 23) | (fr << (23 - S));
+}
+
+}  // namespace bfpg

@@ -1,0 +1,141 @@
+"""Shared fixtures.  `-m gpu` tests need a B200; everything else runs on CPU."""
+from __future__ import annotations
+
+import ctypes as C
+import subprocess
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "oracle"))
+
+import oracle as O  # noqa: E402  (test infrastructure: the checker)
+
+# Formats with compiled networks, and all four mode combinations.
+FORMATS = [(3, 2), (4, 3), (5, 3), (5, 7), (5, 10), (6, 9), (8, 7), (8, 15), (8, 23)]
+MODES = [(1, 0), (0, 0), (1, 1), (0, 1)]  # (rn, ftz)
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA device (B200)")
+    config.addinivalue_line("markers", "slow: long-running parity sweep")
+
+
+def _cuda_available() -> bool:
+    try:
+        import torch
+        return torch.cuda.is_available()
+    except Exception:
+        return False
+
+
+def pytest_collection_modifyitems(config, items):
+    if _cuda_available():
+        return
+    skip = pytest.mark.skip(reason="no CUDA device")
+    for it in items:
+        if "gpu" in it.keywords:
+            it.add_marker(skip)
+
+
+@pytest.fixture(scope="session")
+def oracle():
+    O.orc()
+    return O
+
+
+@pytest.fixture(scope="session")
+def ref_oracle():
+    if not O.ref_available():
+        try:
+            O.build(ref=True)
+        except Exception:
+            pass
+    if not O.ref_available():
+        pytest.skip("reference build (oracle/_ref) unavailable on this host")
+    O.ref()
+    return O
+
+
+class HostCircuits:
+    """The device networks compiled for the host (tests/native)."""
+
+    def __init__(self):
+        native = ROOT / "tests" / "native"
+        subprocess.run(["make", "-s", "-C", str(native)], check=True)
+        L = C.CDLL(str(native / "libhostcirc.so"))
+        vp = C.c_void_p
+        L.host_binop.argtypes = [C.c_int, C.c_uint, C.c_uint, C.c_int, C.c_int, vp, vp, vp, vp, C.c_size_t]
+        L.host_codec.argtypes = [C.c_int, C.c_uint, C.c_uint, C.c_int, C.c_int, vp, vp, C.c_size_t]
+        L.host_pack_enc.argtypes = [C.c_int, C.c_uint, vp, C.c_size_t, vp]
+        L.host_unpack_enc.argtypes = [C.c_int, C.c_uint, vp, C.c_size_t, vp]
+        self.L = L
+
+    def binop(self, op: str, fmt, px, py, pc=None):
+        code = {"add": 0, "sub": 1, "mul": 2, "mul_add": 4}[op]
+        nb = 1 + fmt[0] + fmt[1]
+        z = np.zeros_like(px)
+        rc = self.L.host_binop(code, fmt[0], fmt[1], fmt[2], fmt[3], px.ctypes.data, py.ctypes.data,
+                               pc.ctypes.data if pc is not None else None, z.ctypes.data,
+                               len(px) // (nb * 32))
+        assert rc == 0
+        return z
+
+    def codec(self, direction: int, fmt, vals: np.ndarray) -> np.ndarray:
+        vals = np.ascontiguousarray(vals, dtype=np.uint32)
+        out = np.zeros_like(vals)
+        rc = self.L.host_codec(direction, fmt[0], fmt[1], fmt[2], fmt[3], vals.ctypes.data,
+                               out.ctypes.data, len(vals))
+        assert rc == 0
+        return out
+
+    def pack_enc(self, eb: int, nbits: int, enc: np.ndarray) -> np.ndarray:
+        enc = np.ascontiguousarray(enc.astype({1: np.uint8, 2: np.uint16, 4: np.uint32}[eb]))
+        planes = np.zeros(O.nblocks(len(enc)) * nbits * 32, dtype=np.uint32)
+        self.L.host_pack_enc(eb, nbits, enc.ctypes.data, len(enc), planes.ctypes.data)
+        return planes
+
+    def unpack_enc(self, eb: int, nbits: int, planes: np.ndarray, n: int) -> np.ndarray:
+        out = np.zeros(n, dtype={1: np.uint8, 2: np.uint16, 4: np.uint32}[eb])
+        self.L.host_unpack_enc(eb, nbits, np.ascontiguousarray(planes).ctypes.data, n, out.ctypes.data)
+        return out.astype(np.uint64)
+
+
+@pytest.fixture(scope="session")
+def host():
+    return HostCircuits()
+
+
+# ----------------------------------------------------------------- operands
+def all_pairs(nb: int):
+    n = 1 << nb
+    x = np.repeat(np.arange(n, dtype=np.uint64), n)
+    y = np.tile(np.arange(n, dtype=np.uint64), n)
+    return x, y
+
+
+def operands(e: int, s: int, n: int, rng: np.random.Generator) -> np.ndarray:
+    """Random encodings with extra weight on zero/subnormal, near-overflow and
+    special exponents (the places the circuits branch)."""
+    nb = 1 + e + s
+    v = rng.integers(0, 1 << nb, size=n, dtype=np.uint64)
+    k = n // 4
+    sg = rng.integers(0, 2, size=k, dtype=np.uint64) << np.uint64(e + s)
+    fr = rng.integers(0, 1 << s, size=k, dtype=np.uint64)
+    lo = rng.integers(0, 4, size=k, dtype=np.uint64)
+    hi = ((1 << e) - 1 - rng.integers(0, 3, size=k)).astype(np.uint64)
+    v[:k] = sg | (lo << np.uint64(s)) | fr
+    v[k:2 * k] = sg | (hi << np.uint64(s)) | fr
+    return v
+
+
+def related(x: np.ndarray, e: int, s: int, rng: np.random.Generator) -> np.ndarray:
+    """Operands close to x in magnitude (cancellation / tie cases)."""
+    flip = rng.integers(0, 2, size=len(x), dtype=np.uint64) << np.uint64(e + s)
+    d = rng.integers(0, 4, size=len(x), dtype=np.uint64)
+    mask = np.uint64((1 << (1 + e + s)) - 1)
+    return (x ^ flip ^ d) & mask

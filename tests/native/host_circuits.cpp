@@ -1,12 +1,15 @@
 // tests/native/host_circuits.cpp -- TEST HARNESS ONLY.
-// Compiles the device networks (paper_1602_04716_b200/csrc/bfp_circuits.cuh)
-// for the host so tests can check them exhaustively against the oracle on a
-// machine without a GPU.  Operands use the device plane layout.
+// Compiles the device networks, transposes and codec
+// (paper_1602_04716_b200/csrc/bfp_circuits.cuh, bfp_layout.cuh) for the host
+// so tests can check them exhaustively against the oracle without a GPU.
+// Operands use the device plane layout.
 #include <cstddef>
 #include <cstdint>
+#include <cstring>
 
 #include "../../paper_1602_04716_b200/csrc/bfp_circuits.cuh"
 #include "../../paper_1602_04716_b200/csrc/bfp_formats.h"
+#include "../../paper_1602_04716_b200/csrc/bfp_layout.cuh"
 
 using namespace bfpg;
 
@@ -34,17 +37,81 @@ static void run(int op, const uint32_t* x, const uint32_t* y, const uint32_t* c,
     }
 }
 
-extern "C" int host_binop(int op, unsigned e, unsigned s, int rn, int ftz, const uint32_t* x,
-                          const uint32_t* y, const uint32_t* c, uint32_t* z, size_t nblocks) {
-#define DISPATCH(E_, S_)                                                          \
-  if (e == E_ && s == S_) {                                                       \
-    if (rn && !ftz) run<Format<E_, S_, true, false>>(op, x, y, c, z, nblocks);    \
-    if (rn && ftz) run<Format<E_, S_, true, true>>(op, x, y, c, z, nblocks);      \
-    if (!rn && !ftz) run<Format<E_, S_, false, false>>(op, x, y, c, z, nblocks);  \
-    if (!rn && ftz) run<Format<E_, S_, false, true>>(op, x, y, c, z, nblocks);    \
-    return 0;                                                                     \
+template <class F>
+static void codec(int dir, const uint32_t* in, uint32_t* out, size_t n) {
+  for (size_t i = 0; i < n; ++i) out[i] = dir == 0 ? encode_f32<F>(in[i]) : decode_f32<F>(in[i]);
+}
+
+template <int E_, int S_, class Fn>
+static void with_fmt(int rn, int ftz, Fn&& fn) {
+  if (rn && !ftz) fn(Format<E_, S_, true, false>{});
+  if (rn && ftz) fn(Format<E_, S_, true, true>{});
+  if (!rn && !ftz) fn(Format<E_, S_, false, false>{});
+  if (!rn && ftz) fn(Format<E_, S_, false, true>{});
+}
+
+template <class Fn>
+static int dispatch(unsigned e, unsigned s, int rn, int ftz, Fn&& fn) {
+#define DISPATCH(E_, S_)                   \
+  if (e == E_ && s == S_) {                \
+    with_fmt<E_, S_>(rn, ftz, fn);         \
+    return 0;                              \
   }
   BFP_FORMAT_LIST(DISPATCH)
 #undef DISPATCH
   return 4;
+}
+
+extern "C" int host_binop(int op, unsigned e, unsigned s, int rn, int ftz, const uint32_t* x,
+                          const uint32_t* y, const uint32_t* c, uint32_t* z, size_t nblocks) {
+  return dispatch(e, s, rn, ftz, [&](auto f) { run<decltype(f)>(op, x, y, c, z, nblocks); });
+}
+
+// dir 0: float32 bits -> encoding (encode_f32); dir 1: encoding -> float32 bits.
+extern "C" int host_codec(int dir, unsigned e, unsigned s, int rn, int ftz, const uint32_t* in,
+                          uint32_t* out, size_t n) {
+  return dispatch(e, s, rn, ftz, [&](auto f) { codec<decltype(f)>(dir, in, out, n); });
+}
+
+// Encodings (width eb = 1/2/4 bytes) <-> planes of nbits planes, through the
+// same register transposes the kernels use.  n elements, tail zero-filled.
+extern "C" int host_pack_enc(int eb, unsigned nbits, const uint8_t* enc, size_t n,
+                             uint32_t* planes) {
+  const size_t blocks = (n + 1023) / 1024;
+  for (size_t u = 0; u < blocks * 32; ++u) {
+    w32 L[32] = {0};
+    for (int k = 0; k < 32; ++k) {
+      const size_t i = u * 32 + k;
+      if (i >= n) break;
+      w32 v = 0;
+      std::memcpy(&v, enc + i * eb, eb);
+      L[(k * eb) / 4] |= (eb == 4) ? v : (v << ((k * eb * 8) & 31));
+    }
+    w32 P[32];
+    if (eb == 1) enc8_to_planes(L, P);
+    else if (eb == 2) enc16_to_planes(L, P);
+    else { std::memcpy(P, L, sizeof P); enc32_to_planes(P); }
+    for (unsigned j = 0; j < nbits; ++j) planes[((u >> 5) * nbits + j) * 32 + (u & 31)] = P[j];
+  }
+  return 0;
+}
+
+extern "C" int host_unpack_enc(int eb, unsigned nbits, const uint32_t* planes, size_t n,
+                               uint8_t* enc) {
+  const size_t units = (n + 31) / 32;
+  for (size_t u = 0; u < units; ++u) {
+    w32 P[32] = {0};
+    for (unsigned j = 0; j < nbits; ++j) P[j] = planes[((u >> 5) * nbits + j) * 32 + (u & 31)];
+    w32 L[32];
+    if (eb == 1) planes_to_enc8(P, L);
+    else if (eb == 2) planes_to_enc16(P, L);
+    else { planes_to_enc32(P); std::memcpy(L, P, sizeof L); }
+    for (int k = 0; k < 32; ++k) {
+      const size_t i = u * 32 + k;
+      if (i >= n) break;
+      const w32 v = (eb == 4) ? L[k] : (L[(k * eb) / 4] >> ((k * eb * 8) & 31));
+      std::memcpy(enc + i * eb, &v, eb);
+    }
+  }
+  return 0;
 }

@@ -1,0 +1,106 @@
+"""The C-ABI library: loads, exports every symbol include/bfpgpu.h declares,
+and its host-side logic (validation, same-shape, sizes) matches the reference
+-- CPU only, no compute calls.  Plus the host mirror of the reference API."""
+from __future__ import annotations
+
+import ctypes as C
+import math
+import re
+
+import numpy as np
+import pytest
+
+from conftest import FORMATS, MODES, ROOT
+
+import paper_1602_04716_b200 as bfp
+from paper_1602_04716_b200 import _lib
+
+
+def _declared_symbols() -> list[str]:
+    text = (ROOT / "include" / "bfpgpu.h").read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(bfp_[a-z0-9_]+)\s*\(", text)))
+
+
+@pytest.fixture(scope="module")
+def L():
+    if not _lib.LIB_PATH.exists():
+        from paper_1602_04716_b200.build import build
+        build(verbose=False)
+    return _lib.lib()
+
+
+def test_exports_every_declared_symbol(L):
+    syms = _declared_symbols()
+    assert len(syms) >= 25
+    for s in syms:
+        assert hasattr(L, s), s
+    # and the Python binding knows the signature of each of them
+    assert set(syms) <= set(_lib.SIGNATURES), set(syms) - set(_lib.SIGNATURES)
+
+
+def fmt(e, s, rn=1, ftz=0, name=b""):
+    return _lib.BfpFormat(e, s, rn, ftz, name)
+
+
+def test_validate_ranges_match_reference(L, ref_oracle):
+    """validate(): e in [2, 11], s in [1, 52], 1+e+s <= 64 (format.hpp:57-64)."""
+    R = ref_oracle.ref()
+    for e in range(0, 14):
+        for s in range(0, 56):
+            want = R.ref_validate(e, s) == 0
+            got = L.bfp_validate(C.byref(fmt(e, s))) == _lib.BFP_OK
+            assert want == got, (e, s)
+
+
+def test_same_shape_compares_name(L):
+    """require_same_shape compares the whole spec incl. name (arith.hpp:228-231)."""
+    a, b = fmt(4, 3, name=b"fp8"), fmt(4, 3, name=b"fp8")
+    assert L.bfp_same_shape(C.byref(a), C.byref(b)) == _lib.BFP_OK
+    c = fmt(4, 3, name=b"e4m3")
+    assert L.bfp_same_shape(C.byref(a), C.byref(c)) == _lib.BFP_EMISMATCH
+    assert L.bfp_same_shape(C.byref(a), C.byref(fmt(4, 3, rn=0, name=b"fp8"))) == _lib.BFP_EMISMATCH
+    assert L.bfp_same_shape(C.byref(fmt(4, 3)), C.byref(_lib.BfpFormat(4, 3, 1, 0, None))) == _lib.BFP_OK
+
+
+def test_sizes(L):
+    for (e, s) in FORMATS:
+        n = 1 + e + s
+        f = fmt(e, s)
+        assert L.bfp_is_supported(C.byref(f)) == 1
+        for count in (0, 1, 1024, 1025, 5000):
+            assert L.bfp_plane_bytes(C.byref(f), count) == ((count + 1023) // 1024) * n * 128
+        assert L.bfp_enc_bytes(C.byref(f)) == (1 if n <= 8 else 2 if n <= 16 else 4)
+    assert L.bfp_is_supported(C.byref(fmt(7, 20))) == 0  # legal, not instantiated
+    assert L.bfp_is_supported(C.byref(fmt(12, 3))) == 0  # illegal
+
+
+def test_python_mirror_errors():
+    with pytest.raises(ValueError):
+        bfp.make_spec(1, 3)
+    with pytest.raises(ValueError):
+        bfp.make_spec(4, 0)
+    with pytest.raises(ValueError):
+        bfp.make_spec(11, 53)
+    f = bfp.make_spec(4, 3)
+    assert f.rounding == bfp.rounding_mode.rn and f.subnormals == bfp.subnormal_policy.gradual
+    assert (f.bias(), f.emin(), f.emax()) == (7, -6, 7)
+    assert f.canonical_nan() == 0x7C and f.inf(1) == 0xF8 and f.max_finite(0) == 0x77
+    with pytest.raises(ValueError):
+        bfp.require_same_shape(bfp.make_spec(4, 3, name="a"), bfp.make_spec(4, 3, name="b"))
+
+
+def test_host_scalar_codec_matches_oracle(oracle):
+    rng = np.random.default_rng(1)
+    vals = list(rng.standard_normal(300) * 100) + [0.0, -0.0, math.inf, -math.inf, math.nan, 1e-30,
+                                                   65504.0, 65520.0, 2.0 ** -24, 3 * 2.0 ** -26]
+    for (e, s) in FORMATS:
+        for (rn, ftz) in MODES:
+            f = bfp.make_spec(e, s, rn, ftz)
+            for v in vals:
+                assert bfp.encode_scalar(v, f) == oracle.orc().orc_encode(v, e, s, rn, ftz), (e, s, v)
+        f = bfp.make_spec(e, s)
+        for enc in rng.integers(0, 1 << (1 + e + s), size=200):
+            a = bfp.decode_scalar(int(enc), f)
+            b = oracle.orc().orc_decode(int(enc), e, s)
+            assert (math.isnan(a) and math.isnan(b)) or a == b

@@ -1,0 +1,117 @@
+"""The device networks (csrc/bfp_circuits.cuh, bfp_layout.cuh) compiled for
+the host and checked against the oracle -- CPU only, exhaustive where the
+format is small.  The same source is what runs on the B200; the GPU tests
+(test_gpu_parity.py) repeat the checks through the C ABI."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import FORMATS, MODES, all_pairs, operands, related, ROOT
+
+GOLDEN = ROOT / "tests" / "golden"
+
+
+def _check(O, host, op, fmt, x, y, c=None):
+    nb = 1 + fmt[0] + fmt[1]
+    px, py = O.pack_planes(x, nb), O.pack_planes(y, nb)
+    pc = O.pack_planes(c, nb) if c is not None else None
+    got = O.unpack_planes(host.binop(op, fmt, px, py, pc), len(x), nb)
+    want = O.binop(op, fmt, x, y, c)
+    bad = np.nonzero(want != got)[0]
+    assert len(bad) == 0, (op, fmt, len(bad), [(hex(int(x[i])), hex(int(y[i])), hex(int(want[i])),
+                                                hex(int(got[i]))) for i in bad[:5]])
+
+
+@pytest.mark.parametrize("fmt2", [(3, 2), (4, 3), (5, 3)])
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("op", ["add", "sub", "mul"])
+def test_exhaustive_small(oracle, host, fmt2, mode, op):
+    x, y = all_pairs(1 + fmt2[0] + fmt2[1])
+    _check(oracle, host, op, fmt2 + mode, x, y)
+
+
+@pytest.mark.parametrize("op", ["add", "mul"])
+def test_exhaustive_13bit(oracle, host, op):
+    """1/5/7: all 2^26 pairs, RN + gradual."""
+    x, y = all_pairs(13)
+    _check(oracle, host, op, (5, 7, 1, 0), x, y)
+
+
+@pytest.mark.parametrize("fmt2", [f for f in FORMATS if 1 + f[0] + f[1] > 9])
+@pytest.mark.parametrize("mode", MODES)
+def test_random_wide(oracle, host, fmt2, mode):
+    e, s = fmt2
+    rng = np.random.default_rng((e * 64 + s) * 4 + mode[0] * 2 + mode[1])
+    n = 1 << 16
+    x = operands(e, s, n, rng)
+    y = operands(e, s, n, rng)
+    y[: n // 8] = related(x[: n // 8], e, s, rng)
+    c = operands(e, s, n, rng)
+    for op in ("add", "sub", "mul", "mul_add"):
+        _check(oracle, host, op, fmt2 + mode, x, y, c if op == "mul_add" else None)
+
+
+def test_mul_add_small_exhaustive_c(oracle, host):
+    """chain round(round(a*b)+c) for 1/3/2: all (a, b) against 8 c values."""
+    x, y = all_pairs(6)
+    rng = np.random.default_rng(5)
+    for cval in rng.integers(0, 64, size=8):
+        c = np.full_like(x, cval)
+        for mode in MODES:
+            _check(oracle, host, "mul_add", (3, 2) + mode, x, y, c)
+
+
+def test_golden_host(oracle, host):
+    g = np.load(GOLDEN / "arith.npz")
+    for (e, s) in FORMATS:
+        nb = 1 + e + s
+        for (rn, ftz) in MODES:
+            key = f"{e}_{s}_{rn}_{ftz}"
+            x, y, c = (g[f"{k}_{key}"].astype(np.uint64) for k in "xyc")
+            px, py, pc = (oracle.pack_planes(v, nb) for v in (x, y, c))
+            for op in ("add", "sub", "mul", "mul_add"):
+                z = host.binop(op, (e, s, rn, ftz), px, py, pc if op == "mul_add" else None)
+                got = oracle.unpack_planes(z, len(x), nb)
+                assert np.array_equal(got, g[f"{op}_{key}"].astype(np.uint64)), (op, key)
+
+
+# ----------------------------------------------------------------------- codec
+@pytest.mark.parametrize("fmt2", FORMATS)
+def test_codec_host(oracle, host, fmt2):
+    e, s = fmt2
+    rng = np.random.default_rng(e * 100 + s)
+    bits = rng.integers(0, 1 << 32, size=1 << 16, dtype=np.uint64).astype(np.uint32)
+    bits[: 1 << 14] = (bits[: 1 << 14] & 0x807FFFFF) | (
+        rng.integers(90, 165, size=1 << 14, dtype=np.uint64).astype(np.uint32) << 23)
+    for mode in MODES:
+        fmt = fmt2 + mode
+        got = host.codec(0, fmt, bits).astype(np.uint64)
+        want = oracle.encode_f32(fmt, bits.view(np.float32))
+        assert np.array_equal(got, want), (fmt, int((got != want).sum()))
+    nb = 1 + e + s
+    encs = (np.arange(1 << nb, dtype=np.uint64) if nb <= 16
+            else rng.integers(0, 1 << nb, size=1 << 16, dtype=np.uint64))
+    got = host.codec(1, (e, s, 1, 0), encs.astype(np.uint32))
+    want = oracle.decode_f32((e, s, 1, 0), encs).view(np.uint32)
+    assert np.array_equal(got, want)
+
+
+# ---------------------------------------------------------------------- layout
+@pytest.mark.parametrize("eb,nb", [(1, 6), (1, 8), (2, 9), (2, 16), (4, 24), (4, 32)])
+def test_transpose_host(oracle, host, eb, nb):
+    rng = np.random.default_rng(nb)
+    for n in (1, 33, 1024, 2500):
+        enc = rng.integers(0, 1 << nb, size=n, dtype=np.uint64)
+        planes = host.pack_enc(eb, nb, enc)
+        assert np.array_equal(planes, oracle.pack_planes(enc, nb)), (eb, nb, n)
+        assert np.array_equal(host.unpack_enc(eb, nb, planes, n), enc)
+
+
+def test_layout_golden_host(host):
+    g = np.load(GOLDEN / "layout.npz")
+    for (e, s) in [(4, 3), (5, 10), (8, 15), (8, 23)]:
+        nb = 1 + e + s
+        eb = 1 if nb <= 8 else 2 if nb <= 16 else 4
+        enc = g[f"enc_{e}_{s}"].astype(np.uint64)
+        assert np.array_equal(host.pack_enc(eb, nb, enc), g[f"planes_{e}_{s}"])

@@ -1,0 +1,364 @@
+"""Parity of the B200 kernels, called through the C ABI (libbfpgpu.so), with
+the oracle -- bit-exact, since all of this is integer/bit work.
+
+  * arithmetic: exhaustive for every <= 9-bit format (all modes, add / sub /
+    mul / mul_add), all 2^26 pairs of 1/5/7, every x against sampled y for the
+    16-bit formats, seeded random + directed operands for 24 / 32-bit;
+  * the golden fixtures written by the reference itself;
+  * layout: pack / unpack of raw encodings and of float32 against
+    field_from_elements / element_of + encode_scalar / decode_scalar, with
+    ragged counts and unaligned buffers;
+  * BASELINE configs at full size: C1 and C2 fully against the oracle, C3-C5
+    through size-independent properties plus sampled oracle checks.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import FORMATS, MODES, ROOT, all_pairs, operands, related
+
+import paper_1602_04716_b200 as bfp
+from paper_1602_04716_b200 import _lib, workloads as W
+
+pytestmark = pytest.mark.gpu
+GOLDEN = ROOT / "tests" / "golden"
+OPS = {"add": 0, "sub": 1, "mul": 2, "div": 3, "mul_add": 4}
+
+
+def dev(a: np.ndarray) -> torch.Tensor:
+    a = np.ascontiguousarray(a)
+    return torch.from_numpy(a.view(np.int32) if a.dtype == np.uint32 else a).cuda()
+
+
+def cfmt(fmt):
+    return _lib.BfpFormat(fmt[0], fmt[1], fmt[2], fmt[3], b"")
+
+
+def gpu_arith(op: str, fmt, px, py, pc=None) -> np.ndarray:
+    L = _lib.lib()
+    nb = 1 + fmt[0] + fmt[1]
+    count = (len(px) // (nb * 32)) * 1024
+    dx, dy = dev(px), dev(py)
+    dc = dev(pc) if pc is not None else None
+    dz = torch.empty_like(dx)
+    f = cfmt(fmt)
+    rc = L.bfp_arith(OPS[op], C.byref(f), dx.data_ptr(), dy.data_ptr(),
+                     dc.data_ptr() if dc is not None else None, dz.data_ptr(), count,
+                     torch.cuda.current_stream().cuda_stream)
+    assert rc == 0, _lib.lib().bfp_last_error()
+    return dz.cpu().numpy().view(np.uint32)
+
+
+def check(O, op, fmt, x, y, c=None):
+    nb = 1 + fmt[0] + fmt[1]
+    px, py = O.pack_planes(x, nb), O.pack_planes(y, nb)
+    pc = O.pack_planes(c, nb) if c is not None else None
+    got = O.unpack_planes(gpu_arith(op, fmt, px, py, pc), len(x), nb)
+    want = O.binop(op, fmt, x, y, c)
+    bad = np.nonzero(want != got)[0]
+    assert len(bad) == 0, (op, fmt, len(bad), [(hex(int(x[i])), hex(int(y[i])), hex(int(want[i])),
+                                                hex(int(got[i]))) for i in bad[:5]])
+
+
+# ------------------------------------------------------------------ arithmetic
+@pytest.mark.parametrize("fmt2", [(3, 2), (4, 3), (5, 3)])
+@pytest.mark.parametrize("mode", MODES)
+def test_exhaustive_small(oracle, fmt2, mode):
+    e, s = fmt2
+    x, y = all_pairs(1 + e + s)
+    rng = np.random.default_rng(e + s)
+    c = rng.integers(0, 1 << (1 + e + s), size=len(x), dtype=np.uint64)
+    for op in ("add", "sub", "mul", "mul_add"):
+        check(oracle, op, fmt2 + mode, x, y, c if op == "mul_add" else None)
+
+
+@pytest.mark.parametrize("mode", [(1, 0), (0, 1)])
+def test_exhaustive_13bit(oracle, mode):
+    x, y = all_pairs(13)
+    for op in ("add", "mul"):
+        check(oracle, op, (5, 7) + mode, x, y)
+
+
+@pytest.mark.parametrize("fmt2", [(5, 10), (6, 9), (8, 7)])
+def test_16bit_every_x(oracle, fmt2):
+    """every 16-bit x against 48 sampled y (RN + gradual)."""
+    rng = np.random.default_rng(fmt2[0])
+    xs = np.arange(1 << 16, dtype=np.uint64)
+    ys = operands(*fmt2, 48, rng)
+    x = np.repeat(xs, len(ys))
+    y = np.tile(ys, len(xs))
+    for op in ("add", "sub", "mul"):
+        check(oracle, op, fmt2 + (1, 0), x, y)
+
+
+@pytest.mark.parametrize("fmt2", [f for f in FORMATS if 1 + f[0] + f[1] > 9])
+@pytest.mark.parametrize("mode", MODES)
+def test_random_wide(oracle, fmt2, mode):
+    e, s = fmt2
+    rng = np.random.default_rng(1000 + e * 64 + s + 7 * mode[0] + 13 * mode[1])
+    n = 1 << 18
+    x = operands(e, s, n, rng)
+    y = operands(e, s, n, rng)
+    y[: n // 8] = related(x[: n // 8], e, s, rng)
+    c = operands(e, s, n, rng)
+    for op in ("add", "sub", "mul", "mul_add"):
+        check(oracle, op, fmt2 + mode, x, y, c if op == "mul_add" else None)
+
+
+def test_golden_gpu(oracle):
+    g = np.load(GOLDEN / "arith.npz")
+    for (e, s) in FORMATS:
+        nb = 1 + e + s
+        for (rn, ftz) in MODES:
+            key = f"{e}_{s}_{rn}_{ftz}"
+            x, y, c = (g[f"{k}_{key}"].astype(np.uint64) for k in "xyc")
+            px, py, pc = (oracle.pack_planes(v, nb) for v in (x, y, c))
+            for op in ("add", "sub", "mul", "mul_add"):
+                z = gpu_arith(op, (e, s, rn, ftz), px, py, pc if op == "mul_add" else None)
+                got = oracle.unpack_planes(z, len(x), nb)
+                assert np.array_equal(got, g[f"{op}_{key}"].astype(np.uint64)), (op, key)
+
+
+# ---------------------------------------------------------------------- layout
+@pytest.mark.parametrize("fmt2", FORMATS)
+def test_pack_unpack_enc(oracle, fmt2):
+    e, s = fmt2
+    nb = 1 + e + s
+    spec = bfp.make_spec(e, s)
+    rng = np.random.default_rng(nb)
+    for n in (1, 31, 32, 33, 1000, 1024, 1025, 4096, 70001):
+        enc = rng.integers(0, 1 << nb, size=n + 1, dtype=np.uint64)
+        # offset view by one element: unaligned for the vector path
+        for off in (0, 1):
+            e_np = enc[off:off + n]
+            t = torch.from_numpy(e_np.astype(np.int64)).cuda()
+            v = bfp.pack(t, spec)
+            planes = v.planes.cpu().numpy().view(np.uint32)
+            assert np.array_equal(planes, oracle.pack_planes(e_np, nb)), (n, off)
+            back = bfp.to_u64(bfp.unpack(v), spec).cpu().numpy().astype(np.uint64)
+            assert np.array_equal(back, e_np), (n, off)
+
+
+def test_unaligned_buffers(oracle):
+    spec = bfp.make_spec(5, 10)
+    nb = spec.total_bits()
+    n = 5000
+    rng = np.random.default_rng(9)
+    enc = rng.integers(0, 1 << nb, size=n, dtype=np.uint64)
+    buf = torch.zeros(n + 8, dtype=torch.int16, device="cuda")
+    buf[1:n + 1] = torch.from_numpy(enc.astype(np.uint16).view(np.int16)).cuda()
+    sub = buf[1:n + 1]  # 2-byte aligned only
+    v = bfp.pack(sub, spec)
+    assert np.array_equal(v.planes.cpu().numpy().view(np.uint32), oracle.pack_planes(enc, nb))
+    out = torch.zeros(n + 8, dtype=torch.int16, device="cuda")
+    L = _lib.lib()
+    rc = L.bfp_unpack_enc(spec.c, v.planes.data_ptr(), out[1:].data_ptr(), n,
+                          torch.cuda.current_stream().cuda_stream)
+    assert rc == 0
+    assert np.array_equal(out[1:n + 1].cpu().numpy().view(np.uint16).astype(np.uint64), enc)
+
+
+@pytest.mark.parametrize("fmt2", FORMATS)
+@pytest.mark.parametrize("mode", MODES)
+def test_pack_unpack_f32(oracle, fmt2, mode):
+    e, s = fmt2
+    nb = 1 + e + s
+    fmt = fmt2 + mode
+    spec = bfp.make_spec(e, s, mode[0], mode[1])
+    rng = np.random.default_rng(nb * 4 + mode[0] * 2 + mode[1])
+    n = (1 << 16) + 77
+    bits = rng.integers(0, 1 << 32, size=n, dtype=np.uint64).astype(np.uint32)
+    bits[: n // 2] = (bits[: n // 2] & 0x807FFFFF) | (
+        rng.integers(90, 165, size=n // 2, dtype=np.uint64).astype(np.uint32) << 23)
+    xs = bits.view(np.float32)
+    v = bfp.pack_f32(torch.from_numpy(xs).cuda(), spec)
+    want = oracle.encode_f32(fmt, xs)
+    assert np.array_equal(v.planes.cpu().numpy().view(np.uint32), oracle.pack_planes(want, nb))
+    back = bfp.unpack_f32(v).cpu().numpy().view(np.uint32)
+    assert np.array_equal(back, oracle.decode_f32(fmt, want).view(np.uint32))
+    if nb <= 16:  # every encoding through unpack_f32
+        encs = np.arange(1 << nb, dtype=np.uint64)
+        ve = bfp.pack(torch.from_numpy(encs.astype(np.int64)).cuda(), spec)
+        got = bfp.unpack_f32(ve).cpu().numpy().view(np.uint32)
+        assert np.array_equal(got, oracle.decode_f32(fmt, encs).view(np.uint32))
+
+
+def test_codec_golden_gpu():
+    g = np.load(GOLDEN / "codec.npz")
+    for (e, s) in FORMATS:
+        nb = 1 + e + s
+        for (rn, ftz) in MODES:
+            key = f"{e}_{s}_{rn}_{ftz}"
+            spec = bfp.make_spec(e, s, rn, ftz)
+            xs = g[f"f32in_{key}"].view(np.float32)
+            v = bfp.pack_f32(torch.from_numpy(xs.copy()).cuda(), spec)
+            got = bfp.to_u64(bfp.unpack(v), spec).cpu().numpy()
+            assert np.array_equal(got.astype(np.uint32), g[f"enc_{key}"]), key
+            ve = bfp.pack(torch.from_numpy(g[f"decin_{key}"].astype(np.int64)).cuda(), spec)
+            assert np.array_equal(bfp.unpack_f32(ve).cpu().numpy().view(np.uint32), g[f"dec_{key}"])
+
+
+# ------------------------------------------------------------ API / errors
+def test_python_api_roundtrip(oracle):
+    spec = bfp.make_spec(4, 3)
+    x = torch.linspace(-20, 20, 3000, device="cuda")
+    y = torch.linspace(7, -3, 3000, device="cuda")
+    vx, vy = bfp.pack_f32(x, spec), bfp.pack_f32(y, spec)
+    ex = oracle.encode_f32((4, 3, 1, 0), x.cpu().numpy())
+    ey = oracle.encode_f32((4, 3, 1, 0), y.cpu().numpy())
+    for fn, op in ((bfp.bfp_add, "add"), (bfp.bfp_sub, "sub"), (bfp.bfp_mul, "mul")):
+        z = bfp.to_u64(bfp.unpack(fn(vx, vy)), spec).cpu().numpy().astype(np.uint64)
+        assert np.array_equal(z, oracle.binop(op, (4, 3, 1, 0), ex, ey)), op
+    with pytest.raises(ValueError):
+        bfp.bfp_add(vx, bfp.pack_f32(y, bfp.make_spec(4, 3, name="other")))
+
+
+def test_unsupported_and_errors():
+    L = _lib.lib()
+    t = torch.zeros(4096, dtype=torch.int32, device="cuda")
+    f = _lib.BfpFormat(7, 20, 1, 0, b"")  # legal but not instantiated
+    assert L.bfp_add(C.byref(f), t.data_ptr(), t.data_ptr(), t.data_ptr(), 10, None) == _lib.BFP_EUNSUPPORTED
+    f = _lib.BfpFormat(1, 3, 1, 0, b"")
+    assert L.bfp_add(C.byref(f), t.data_ptr(), t.data_ptr(), t.data_ptr(), 10, None) == _lib.BFP_EFORMAT
+    f = _lib.BfpFormat(4, 3, 1, 0, b"")
+    assert L.bfp_add(C.byref(f), None, t.data_ptr(), t.data_ptr(), 10, None) == _lib.BFP_EARG
+    assert L.bfp_add(C.byref(f), t.data_ptr(), t.data_ptr(), t.data_ptr(), 0, None) == _lib.BFP_OK
+
+
+def test_host_pipeline_matches_device(oracle):
+    L = _lib.lib()
+    fmt = (5, 10, 1, 0)
+    nb = 16
+    n = 3 * (1 << 20) + 5000
+    rng = np.random.default_rng(4)
+    x, y = operands(5, 10, n, rng), operands(5, 10, n, rng)
+    px, py = oracle.pack_planes(x, nb), oracle.pack_planes(y, nb)
+    pz = np.zeros_like(px)
+    ctx = L.bfp_host_ctx_create(1 << 20)
+    try:
+        f = cfmt(fmt)
+        rc = L.bfp_arith_host(ctx, 2, C.byref(f), px.ctypes.data, py.ctypes.data, None, pz.ctypes.data, n)
+        assert rc == 0
+        assert np.array_equal(oracle.unpack_planes(pz, n, nb), oracle.binop("mul", fmt, x, y))
+        xs = (rng.standard_normal(n) * 100).astype(np.float32)
+        pp = np.zeros_like(px)
+        assert L.bfp_pack_f32_host(ctx, C.byref(f), xs.ctypes.data, pp.ctypes.data, n) == 0
+        assert np.array_equal(pp, oracle.pack_planes(oracle.encode_f32(fmt, xs), nb))
+        back = np.zeros(n, dtype=np.float32)
+        assert L.bfp_unpack_f32_host(ctx, C.byref(f), pp.ctypes.data, back.ctypes.data, n) == 0
+        assert np.array_equal(back.view(np.uint32),
+                              oracle.decode_f32(fmt, oracle.encode_f32(fmt, xs)).view(np.uint32))
+    finally:
+        L.bfp_host_ctx_destroy(ctx)
+
+
+# -------------------------------------------------------- BASELINE configs
+def _enc_np(t: torch.Tensor, spec) -> np.ndarray:
+    return bfp.to_u64(t, spec).cpu().numpy().astype(np.uint64)
+
+
+def test_config1_full(oracle):
+    """C1: 1/4/3 add, N=2^24, uniform [-16,16] -> encode_scalar -> planes."""
+    spec = bfp.make_spec(4, 3)
+    n = 1 << 24
+    a = W.c1_floats(0, n, W.SEED_A)
+    b = W.c1_floats(0, n, W.SEED_B)
+    va, vb = bfp.pack_f32(a, spec), bfp.pack_f32(b, spec)
+    z = bfp.bfp_add(va, vb)
+    ea = oracle.encode_f32((4, 3, 1, 0), a.cpu().numpy())
+    eb = oracle.encode_f32((4, 3, 1, 0), b.cpu().numpy())
+    assert np.array_equal(_enc_np(bfp.unpack(va), spec), ea)
+    assert np.array_equal(_enc_np(bfp.unpack(z), spec), oracle.binop("add", (4, 3, 1, 0), ea, eb))
+
+
+def test_config2_full(oracle):
+    """C2: 1/4/3 mul and sub, N=2^26 raw encodings incl. subnormals and 1% zeros."""
+    spec = bfp.make_spec(4, 3)
+    n = 1 << 26
+    a = W.c2_encodings(0, n, W.SEED_A)
+    b = W.c2_encodings(0, n, W.SEED_B)
+    va, vb = bfp.pack(a, spec), bfp.pack(b, spec)
+    ea, eb = a.cpu().numpy().astype(np.uint64), b.cpu().numpy().astype(np.uint64)
+    for fn, op in ((bfp.bfp_mul, "mul"), (bfp.bfp_sub, "sub")):
+        got = _enc_np(bfp.unpack(fn(va, vb)), spec)
+        assert np.array_equal(got, oracle.binop(op, (4, 3, 1, 0), ea, eb)), op
+
+
+def _sample_check(oracle, fmt, spec, ea_t, eb_t, z_t, op, k=1 << 20, ec_t=None):
+    n = ea_t.numel()
+    idx = torch.randint(0, n, (k,), device="cuda", generator=torch.Generator("cuda").manual_seed(5))
+    ea, eb = _enc_np(ea_t[idx], spec), _enc_np(eb_t[idx], spec)
+    ec = _enc_np(ec_t[idx], spec) if ec_t is not None else None
+    assert np.array_equal(_enc_np(z_t[idx], spec), oracle.binop(op, fmt, ea, eb, ec)), op
+
+
+@pytest.mark.slow
+def test_config3_properties(oracle):
+    """C3: 1/5/10, N=2^28: pack_f32 == IEEE binary16 RN (NaN-free input),
+    add/mul commutative, x - y == x + (-y), unpack_f32(pack_f32(x)) exact on
+    representable values; sampled oracle parity of every op."""
+    spec = bfp.make_spec(5, 10)
+    fmt = (5, 10, 1, 0)
+    n = 1 << 28
+    a = W.c3_floats(0, n, W.SEED_A)
+    b = W.c3_floats(0, n, W.SEED_B)
+    va, vb = bfp.pack_f32(a, spec), bfp.pack_f32(b, spec)
+    ea, eb = bfp.unpack(va), bfp.unpack(vb)
+    assert torch.equal(ea, a.to(torch.float16).view(torch.int16))
+    s = bfp.bfp_add(va, vb)
+    assert torch.equal(s.planes, bfp.bfp_add(vb, va).planes)
+    m = bfp.bfp_mul(va, vb)
+    assert torch.equal(m.planes, bfp.bfp_mul(vb, va).planes)
+    d = bfp.bfp_sub(va, vb)
+    nb = bfp.pack(eb ^ torch.tensor(-32768, dtype=torch.int16, device="cuda"), spec)
+    assert torch.equal(d.planes, bfp.bfp_add(va, nb).planes)
+    back = bfp.unpack_f32(va)
+    assert torch.equal(back, a.to(torch.float16).to(torch.float32))
+    _sample_check(oracle, fmt, spec, ea, eb, bfp.unpack(s), "add")
+    _sample_check(oracle, fmt, spec, ea, eb, bfp.unpack(m), "mul")
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("fmt2", [(3, 2), (5, 3), (5, 7), (8, 7), (8, 15)])
+def test_config4_sampled(oracle, fmt2):
+    e, s = fmt2
+    spec = bfp.make_spec(e, s)
+    n = 1 << 26  # a quarter of the bench size keeps the test fast; same kernels
+    a = W.c4_encodings(e, s, 0, n, W.SEED_A)
+    b = W.c4_encodings(e, s, 0, n, W.SEED_B)
+    va, vb = bfp.pack(a, spec), bfp.pack(b, spec)
+    for fn, op in ((bfp.bfp_add, "add"), (bfp.bfp_mul, "mul")):
+        z = fn(va, vb)
+        _sample_check(oracle, fmt2 + (1, 0), spec, bfp.unpack(va), bfp.unpack(vb), bfp.unpack(z), op)
+
+
+@pytest.mark.slow
+def test_config5_shards(oracle):
+    """C5: the fused 1/6/9 chain computed on 4 block-aligned shards
+    concatenates to the unsharded result (no exchange step), with sampled
+    oracle parity (the bench runs 2^32 / G per GPU)."""
+    spec = bfp.make_spec(6, 9)
+    n = (1 << 26) + 3 * 1024 + 17
+    ops = [bfp.pack_f32(W.c5_floats(0, n, sd), spec) for sd in (W.SEED_A, W.SEED_B, W.SEED_C)]
+    full = bfp.bfp_mul_add(*ops)
+    parts = []
+    for r in range(4):
+        lo, hi = W.shard(n, r, 4)
+        sh = [bfp.pack_f32(W.c5_floats(lo, hi, sd), spec) for sd in (W.SEED_A, W.SEED_B, W.SEED_C)]
+        parts.append(bfp.bfp_mul_add(*sh).planes)
+    assert torch.equal(torch.cat(parts), full.planes)
+    ea, eb, ec = (bfp.unpack(v) for v in ops)
+    _sample_check(oracle, (6, 9, 1, 0), spec, ea, eb, bfp.unpack(full), "mul_add", ec_t=ec)
+
+
+def test_launch_counter():
+    L = _lib.lib()
+    before = L.bfp_launch_count()
+    spec = bfp.make_spec(4, 3)
+    v = bfp.pack(torch.arange(2048, device="cuda") % 256, spec)
+    bfp.bfp_add(v, v)
+    assert L.bfp_launch_count() == before + 2

@@ -1,0 +1,95 @@
+"""Static SASS instruction mix per kernel of libbfpgpu.so (cuobjdump -sass).
+
+    python tools/sass_stats.py [--filter REGEX] [--json out.json]
+
+For the arithmetic kernels the loop body is one 32-element unit per thread,
+so (LOP3 count in the body) / 32 is the LOP3 work per element -- the logic
+leg of the roofline.  The body is everything between the
+first and the last global load/store of the kernel; the count reported is
+the whole function, which only adds the loop/address prologue.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import re
+import subprocess
+from collections import Counter
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent.parent
+LIB = ROOT / "paper_1602_04716_b200" / "libbfpgpu.so"
+
+ALU_PIPE = {"LOP3", "IADD3", "SHF", "PRMT", "ISETP", "SEL", "IMNMX", "FLO", "LEA", "LOP",
+            "VIADD", "IABS", "POPC", "BREV", "PLOP3", "VIMNMX", "SGXT", "BMSK", "FSEL", "FSETP", "P2R", "R2P"}
+FMA_PIPE = {"IMAD", "FFMA", "FMUL", "FADD", "HFMA2", "HADD2", "HMUL2", "IMUL", "IADD"}
+MEM = {"LDG", "STG", "LDS", "STS", "LDL", "STL", "LD", "ST"}
+
+
+def demangle(names: list[str]) -> dict[str, str]:
+    try:
+        out = subprocess.run(["c++filt"], input="\n".join(names), capture_output=True, text=True).stdout
+        return dict(zip(names, out.splitlines()))
+    except OSError:
+        return {n: n for n in names}
+
+
+def sass_functions(lib: Path) -> dict[str, list[str]]:
+    txt = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", str(lib)],
+                         capture_output=True, text=True, check=True).stdout
+    funcs: dict[str, list[str]] = {}
+    cur = None
+    for line in txt.splitlines():
+        m = re.match(r"\s*Function : (\S+)", line)
+        if m:
+            cur = m.group(1)
+            funcs[cur] = []
+            continue
+        if cur is None:
+            continue
+        m = re.match(r"\s*/\*[0-9a-f]+\*/\s+(@!?U?P\w+\s+)?([A-Z][A-Z0-9_.]*)", line)
+        if m:
+            funcs[cur].append(m.group(2))
+    return funcs
+
+
+def stats(lib: Path = LIB, pattern: str | None = None) -> dict[str, dict]:
+    funcs = sass_functions(lib)
+    dm = demangle(list(funcs))
+    res = {}
+    for name, ins in funcs.items():
+        pretty = dm.get(name, name)
+        if pattern and not re.search(pattern, pretty):
+            continue
+        base = Counter(i.split(".")[0] for i in ins)
+        alu = sum(v for k, v in base.items() if k in ALU_PIPE)
+        fma = sum(v for k, v in base.items() if k in FMA_PIPE)
+        res[pretty] = {
+            "mangled": name,
+            "total": len(ins),
+            "LOP3": base.get("LOP3", 0),
+            "alu_pipe": alu,
+            "fma_pipe": fma,
+            "mem": sum(v for k, v in base.items() if k in MEM),
+            "top": base.most_common(8),
+        }
+    return res
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--lib", default=str(LIB))
+    ap.add_argument("--filter", default=r"k_arith")
+    ap.add_argument("--json", default=None)
+    a = ap.parse_args()
+    res = stats(Path(a.lib), a.filter)
+    for name, r in sorted(res.items()):
+        short = re.sub(r"bfpg::|Format<|unsigned int|const", "", name)[:90]
+        print(f"{short:90s} tot={r['total']:5d} LOP3={r['LOP3']:5d} alu={r['alu_pipe']:5d} "
+              f"fma={r['fma_pipe']:4d} mem={r['mem']:3d}  LOP3/elem={r['LOP3'] / 32:.2f}")
+    if a.json:
+        Path(a.json).write_text(json.dumps(res, indent=1))
+
+
+if __name__ == "__main__":
+    main()
