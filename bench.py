@@ -26,6 +26,7 @@ from __future__ import annotations
 
 import argparse
 import ctypes as C
+import faulthandler
 import json
 import os
 import statistics
@@ -273,8 +274,12 @@ def run_e2e(cfg: str, steps: int, world: int, rank: int, local: int) -> dict:
 
     def host_copy(t):
         p = L.bfp_host_alloc(pb)
-        C.memmove(p, t.planes.cpu().numpy().ctypes.data, pb)
+        if not p:
+            raise RuntimeError("bfp_host_alloc failed")
         bufs.append(p)
+        src = t.planes.cpu().numpy()  # keep alive across the copy
+        C.memmove(p, src.ctypes.data, pb)
+        del src
         return p
 
     try:
@@ -432,10 +437,14 @@ def main_ours(args) -> None:
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg = args.config
+    log = (lambda m: print(f"[bench r{rank}] {m}", file=sys.stderr, flush=True))
+    log(f"device timing {cfg}")
     res = run_device(cfg, args.steps, args.warmup, world, rank, local)
     if clocks_rejected(res["clocks"]):  # re-measure once
         res = run_device(cfg, args.steps, args.warmup, world, rank, local)
+    log(f"device done: {res['ms_total'] / args.steps:.4f} ms/step; e2e")
     e2e = run_e2e(cfg, args.steps, world, rank, local)
+    log("lop3 probe")
     peak_lop3 = lop3_peak() if rank == 0 else None
 
     spec, n, nbits = res["spec"], res["n"], res["nbits"]
@@ -488,6 +497,7 @@ def main_ours(args) -> None:
         "gpu_launches": res["launches"],
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        log("cpu baseline")
         cb = ref_cpu_run(cfg, 1 << 22, seconds=args.cpu_seconds)
         line["cpu_baseline"] = {
             "value": round(cb["value"], 4), "unit": UNIT, "cores": cb["cores"], "kind": "reference",
@@ -501,6 +511,7 @@ def main_ours(args) -> None:
 
 
 def main() -> None:
+    faulthandler.enable()
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
