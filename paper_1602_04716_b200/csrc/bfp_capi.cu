@@ -122,7 +122,6 @@ bfp_status bfp_arith(int op, const bfp_format* f, const uint32_t* d_x, const uin
   const bfp_status s = resolve(f, &impl);
   if (s != BFP_OK) return s;
   if (op < 0 || op > 4) return fail(BFP_EARG, "bad op");
-  if (op == 3) return fail(BFP_EUNSUPPORTED, "div not compiled");
   if (count == 0) return BFP_OK;
   if (!d_x || !d_y || !d_z || (op == 4 && !d_c)) return fail(BFP_EARG, "null operand");
   ++g_launches;
@@ -314,7 +313,7 @@ bfp_status bfp_arith_host(bfp_host_ctx* c, int op, const bfp_format* f, const ui
   const Impl* impl = nullptr;
   bfp_status s = resolve(f, &impl);
   if (s != BFP_OK) return s;
-  if (op < 0 || op > 4 || op == 3) return fail(BFP_EUNSUPPORTED, "op");
+  if (op < 0 || op > 4) return fail(BFP_EARG, "bad op");
   if (!h_x || !h_y || !h_z || (op == 4 && !h_c)) return fail(BFP_EARG, "null operand");
   const size_t stride = nplanes(f) * 128;
   const void* ins[3] = {h_x, h_y, h_c};

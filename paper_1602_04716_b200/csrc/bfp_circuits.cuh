@@ -351,6 +351,104 @@ BFP_HD void add_w(const w32* X, const w32* Y, w32* Z) {
   Z[M] = sa & mux(as, ~use_nan, sb | nz);
 }
 
+// ====================================================== shared final stage
+// Rounds and packs a significand field R = [jam, guard, sig(S+1)] whose
+// biased exponent minus one is ez (EW = E+2 bit two's complement):
+//   ez >= 0: normal, exponent field ez + hidden (+ rounding carry);
+//   ez <  0: subnormal range, R shifts right by -ez first (jam collects);
+// then overflow (Inf under RN, max-finite under RZ), FTZ after rounding
+// (still below the smallest normal) and the special-value overrides:
+// zero_res / inf_res force a signed zero / Inf, use_nan the canonical NaN.
+template <class F>
+BFP_HD void finish_round(w32* R, const w32* ez, w32 sign, w32 zero_res, w32 inf_res, w32 use_nan,
+                         w32* Z) {
+  constexpr int E = F::E, S = F::S, M = E + S;
+  constexpr int EW = E + 2;
+  constexpr int WR = S + 3;
+  const w32 sub = ez[EW - 1];
+  {
+    // amt = -ez = ~ez + 1, live only on sub; saturate at 2^KR - 1 >= WR - 1.
+    constexpr int KR = clog2(WR);
+    constexpr int KRS = imin(KR, EW);
+    w32 ng[EW];
+    w32 c = ONES;
+    BFP_UNROLL for (int i = 0; i < EW; ++i) {
+      const w32 v = ~ez[i];
+      ng[i] = v ^ c;
+      c = v & c;
+    }
+    w32 big = 0;
+    BFP_UNROLL for (int k = KR; k < EW; ++k) big |= ng[k];
+    w32 amt[KRS];
+    BFP_UNROLL for (int k = 0; k < KRS; ++k) amt[k] = (ng[k] | big) & sub;
+    w32 (&Rr)[WR] = *reinterpret_cast<w32(*)[WR]>(R);
+    shr_jam<WR, KRS>(Rr, amt);
+  }
+  const w32* sig = R + 2;
+  w32 rnd = 0;
+  if constexpr (F::RN) rnd = R[1] & (R[0] | sig[0]);
+
+  // exponent field: ez masked to 0 in the subnormal range (E+1 bits kept for
+  // overflow detection), + hidden, + rounding carry.
+  w32 em[E + 1];
+  BFP_UNROLL for (int i = 0; i <= E; ++i) em[i] = ez[i] & ~sub;
+  w32 fr[S], ex[E + 2];
+  pack_round<E + 1, S, E + 1>(em, sig, rnd, fr, ex);
+  w32 eall = ONES;
+  BFP_UNROLL for (int i = 0; i < E; ++i) eall &= ex[i];
+  const w32 ovf = ex[E] | ex[E + 1] | eall;
+
+  w32 flush = 0;
+  if constexpr (F::FTZ) flush = sub & ~ex[0];  // still below the smallest normal
+  const w32 quiet = ~(zero_res | inf_res | use_nan);
+  const w32 force = inf_res | use_nan;  // exponent all ones
+  w32 keep, setf = 0;
+  if constexpr (F::RN) {
+    keep = quiet & ~ovf & ~flush;
+  } else {
+    keep = quiet & ~flush;
+    setf = quiet & ovf;
+  }
+  BFP_UNROLL for (int j = 0; j < S; ++j) Z[j] = (fr[j] & keep) | setf;
+  Z[S - 1] |= use_nan;
+  const w32 hset = force | (quiet & ovf);
+  BFP_UNROLL for (int j = 0; j < E; ++j) {
+    if constexpr (!F::RN) {
+      if (j == 0) {
+        Z[S] = (ex[0] & quiet & ~ovf) | force;
+        continue;
+      }
+    }
+    Z[S + j] = (ex[j] & quiet) | hset;
+  }
+  Z[M] = sign & ~use_nan;
+}
+
+// Operand classes shared by mul / div.
+struct Classes {
+  w32 h;   // hidden bit (exponent nonzero)
+  w32 s;   // exponent all ones (Inf / NaN)
+  w32 f;   // fraction nonzero
+  w32 z;   // zero
+  w32 inf;
+  w32 nan;
+};
+
+template <class F>
+BFP_HD Classes classify(const w32* X) {
+  constexpr int E = F::E, S = F::S;
+  Classes c{0, ONES, 0, 0, 0, 0};
+  BFP_UNROLL for (int i = 0; i < E; ++i) {
+    c.h |= X[S + i];
+    c.s &= X[S + i];
+  }
+  BFP_UNROLL for (int i = 0; i < S; ++i) c.f |= X[i];
+  c.z = ~c.h & ~c.f;
+  c.inf = c.s & ~c.f;
+  c.nan = c.s & c.f;
+  return c;
+}
+
 // ================================================================= MUL
 // Z = X * Y.  bfp_mul semantics, arith.hpp:330-373.
 template <class F>
@@ -358,18 +456,7 @@ BFP_HD void mul_w(const w32* X, const w32* Y, w32* Z) {
   constexpr int E = F::E, S = F::S, M = E + S;
   constexpr int EW = E + 2;  // signed working exponent
   const w32 sign = X[M] ^ Y[M];
-
-  w32 hx = 0, hy = 0, xs = ONES, ys = ONES, xf = 0, yf = 0;
-  BFP_UNROLL for (int i = 0; i < E; ++i) {
-    hx |= X[S + i];
-    hy |= Y[S + i];
-    xs &= X[S + i];
-    ys &= Y[S + i];
-  }
-  BFP_UNROLL for (int i = 0; i < S; ++i) {
-    xf |= X[i];
-    yf |= Y[i];
-  }
+  const Classes cx = classify<F>(X), cy = classify<F>(Y);
 
   // Exact product of the (S+1)-bit significands: shift-add rows.
   constexpr int WP = 2 * S + 2;
@@ -380,8 +467,8 @@ BFP_HD void mul_w(const w32* X, const w32* Y, w32* Z) {
       mx[i] = X[i];
       my[i] = Y[i];
     }
-    mx[S] = hx;
-    my[S] = hy;
+    mx[S] = cx.h;
+    my[S] = cy.h;
     BFP_UNROLL for (int j = 0; j <= S; ++j) P[j] = mx[j] & my[0];
     BFP_UNROLL for (int j = S + 1; j < WP; ++j) P[j] = 0;
     BFP_UNROLL for (int i = 1; i <= S; ++i) {
@@ -401,8 +488,7 @@ BFP_HD void mul_w(const w32* X, const w32* Y, w32* Z) {
   w32 lz[KP];
   normalize_stages<WP, KP, KP - 1>(P, lz);
 
-  // Ezm1 = ex_eff + ey_eff - bias - lz  (EW-bit two's complement); the
-  // biased result exponent is Ezm1 + 1 when positive.
+  // ez = ex_eff + ey_eff - bias - lz  (biased result exponent minus one).
   w32 ez[EW];
   {
     w32 a[EW], b[EW];
@@ -410,9 +496,8 @@ BFP_HD void mul_w(const w32* X, const w32* Y, w32* Z) {
       a[i] = (i < E) ? X[S + i] : 0u;
       b[i] = (i < E) ? Y[S + i] : 0u;
     }
-    a[0] |= ~hx;
-    b[0] |= ~hy;
-    // ex + ey + (-bias): add the constant two's complement of bias
+    a[0] |= ~cx.h;
+    b[0] |= ~cy.h;
     w32 t[EW];
     (void)add_k<EW>(a, b, 0, t);
     w32 nb[EW];
@@ -424,11 +509,9 @@ BFP_HD void mul_w(const w32* X, const w32* Y, w32* Z) {
     BFP_UNROLL for (int i = 0; i < EW; ++i) l[i] = (i < KP) ? lz[i] : 0u;
     (void)sub_k<EW>(u, l, ez);
   }
-  const w32 sub = ez[EW - 1];  // Ezm1 < 0: subnormal range
 
-  // Rounding field [jam, guard, sig(S+1)]; shift right by -Ezm1 when sub.
-  constexpr int WR = S + 3;
-  w32 R[WR];
+  // [jam, guard, sig(S+1)] from the normalised product.
+  w32 R[S + 3];
   {
     w32 st = 0;
     BFP_UNROLL for (int i = 0; i < S; ++i) st |= P[i];
@@ -436,66 +519,117 @@ BFP_HD void mul_w(const w32* X, const w32* Y, w32* Z) {
     R[1] = P[S];
     BFP_UNROLL for (int i = 0; i <= S; ++i) R[2 + i] = P[S + 1 + i];
   }
+  // Special-value rules of bfp_mul (arith.hpp:193-199).
+  const w32 use_nan = cx.nan | cy.nan | (cx.inf & cy.z) | (cx.z & cy.inf);
+  const w32 zero_res = (cx.z | cy.z) & ~use_nan;
+  const w32 inf_res = (cx.inf | cy.inf) & ~use_nan;
+  finish_round<F>(R, ez, sign, zero_res, inf_res, use_nan, Z);
+}
+
+// ================================================================= DIV
+// Z = X / Y.  bfp_div semantics, arith.hpp:375-444: both significands are
+// normalised (subnormal inputs slide up, their exponents absorb the count),
+// the dividend is doubled when its significand is the smaller so the
+// quotient lies in [1, 2), and a restoring divider produces S+1 quotient
+// bits (RZ) or S+2 (RN: one guard bit) plus a remainder-nonzero sticky.
+template <class F>
+BFP_HD void div_w(const w32* X, const w32* Y, w32* Z) {
+  constexpr int E = F::E, S = F::S, M = E + S;
+  constexpr int EW = E + 2;
+  constexpr int W1 = S + 1;
+  const w32 sign = X[M] ^ Y[M];
+  const Classes cx = classify<F>(X), cy = classify<F>(Y);
+
+  w32 nx[W1], ny[W1];
+  BFP_UNROLL for (int i = 0; i < S; ++i) {
+    nx[i] = X[i];
+    ny[i] = Y[i];
+  }
+  nx[S] = cx.h;
+  ny[S] = cy.h;
+  constexpr int KN = clog2(W1) > 0 ? clog2(W1) : 1;
+  w32 lzx[KN], lzy[KN];
+  normalize_stages<W1, KN, KN - 1>(nx, lzx);
+  normalize_stages<W1, KN, KN - 1>(ny, lzy);
+
+  // scale = nx < ny; num = nx << scale (S+2 bits, in [ny, 2ny)).
+  w32 bw = 0;
+  BFP_UNROLL for (int i = 0; i < W1; ++i) bw = maj(~nx[i], ny[i], bw);
+  const w32 scale = bw;
+  w32 num[W1 + 1];
+  num[0] = nx[0] & ~scale;
+  BFP_UNROLL for (int i = 1; i < W1; ++i) num[i] = mux(scale, nx[i - 1], nx[i]);
+  num[W1] = nx[W1 - 1] & scale;
+
+  // Restoring division.  The leading quotient bit is 1: R = num - ny < ny.
+  constexpr int QB = F::RN ? S + 2 : S + 1;
+  w32 q[QB];
+  q[QB - 1] = ONES;
+  w32 R[W1];
   {
-    // amt = -Ezm1 = ~Ezm1 + 1, live only on sub; saturate at 2^KR - 1 >= WR - 1.
-    constexpr int KR = clog2(WR);
-    constexpr int KRS = imin(KR, EW - 1);
-    w32 ng[EW];
-    w32 c = ONES;
-    BFP_UNROLL for (int i = 0; i < EW; ++i) {
-      const w32 v = ~ez[i];
-      ng[i] = v ^ c;
-      c = v & c;
-    }
-    w32 big = 0;
-    BFP_UNROLL for (int k = KR; k < EW - 1; ++k) big |= ng[k];
-    w32 amt[KRS];
-    BFP_UNROLL for (int k = 0; k < KRS; ++k) amt[k] = (ng[k] | big) & sub;
-    shr_jam<WR, KRS>(R, amt);
+    w32 d[W1 + 1], den[W1 + 1];
+    BFP_UNROLL for (int i = 0; i < W1; ++i) den[i] = ny[i];
+    den[W1] = 0;
+    (void)sub_k<W1 + 1>(num, den, d);
+    BFP_UNROLL for (int i = 0; i < W1; ++i) R[i] = d[i];
   }
-  const w32* sig = R + 2;
-  w32 rnd = 0;
-  if constexpr (F::RN) rnd = R[1] & (R[0] | sig[0]);
-
-  // exponent field: Ezm1 masked to 0 in the subnormal range (E+1 bits kept
-  // for overflow detection), + hidden, + rounding carry.
-  w32 em[E + 1];
-  BFP_UNROLL for (int i = 0; i <= E; ++i) em[i] = ez[i] & ~sub;
-  w32 fr[S], ex[E + 2];
-  pack_round<E + 1, S, E + 1>(em, sig, rnd, fr, ex);
-  w32 eall = ONES;
-  BFP_UNROLL for (int i = 0; i < E; ++i) eall &= ex[i];
-  const w32 ovf = ex[E] | ex[E + 1] | eall;
-
-  // Special-value classes (mul rules, arith.hpp:193-199).
-  const w32 xz = ~hx & ~xf, yz = ~hy & ~yf;
-  const w32 Zr = xz | yz;   // a zero operand
-  const w32 SP = xs | ys;   // an Inf/NaN operand
-  const w32 use_nan = (xs & xf) | (ys & yf) | (xs & yz) | (ys & xz);
-
-  w32 flush = 0;
-  if constexpr (F::FTZ) flush = sub & ~ex[0];  // still below the smallest normal
-  const w32 quiet = ~(Zr | SP);
-  w32 keep, setf = 0;
+  BFP_UNROLL for (int t = QB - 2; t >= 0; --t) {
+    // trial = 2R - ny over S+2 bits
+    w32 r2[W1 + 1], den[W1 + 1], tr[W1 + 1];
+    r2[0] = 0;
+    BFP_UNROLL for (int i = 0; i < W1; ++i) r2[i + 1] = R[i];
+    BFP_UNROLL for (int i = 0; i < W1; ++i) den[i] = ny[i];
+    den[W1] = 0;
+    const w32 borrow = sub_k<W1 + 1>(r2, den, tr);
+    const w32 qt = ~borrow;
+    q[t] = qt;
+    BFP_UNROLL for (int i = 0; i < W1; ++i) R[i] = mux(qt, tr[i], r2[i]);
+  }
+  w32 rem = 0;
   if constexpr (F::RN) {
-    keep = quiet & ~ovf & ~flush;
+    BFP_UNROLL for (int i = 0; i < W1; ++i) rem |= R[i];
+  }
+
+  // ez = (ex_eff - lzx) - (ey_eff - lzy) - scale + bias - 1
+  w32 ez[EW];
+  {
+    w32 a[EW], b[EW], la[EW], lb[EW], t1[EW], t2[EW], t3[EW];
+    BFP_UNROLL for (int i = 0; i < EW; ++i) {
+      a[i] = (i < E) ? X[S + i] : 0u;
+      b[i] = (i < E) ? Y[S + i] : 0u;
+      la[i] = (i < KN) ? lzx[i] : 0u;
+      lb[i] = (i < KN) ? lzy[i] : 0u;
+    }
+    a[0] |= ~cx.h;
+    b[0] |= ~cy.h;
+    (void)sub_k<EW>(a, la, t1);   // ex_eff - lzx
+    (void)add_k<EW>(t1, lb, 0, t2);  // + lzy
+    (void)sub_k<EW>(t2, b, t3);   // - ey_eff
+    w32 k[EW];
+    constexpr int KB = F::BIAS - 1;  // + bias - 1 (>= 0)
+    BFP_UNROLL for (int i = 0; i < EW; ++i) k[i] = ((KB >> i) & 1) ? ONES : 0u;
+    w32 t4[EW];
+    (void)add_k<EW>(t3, k, 0, t4);
+    w32 sc[EW];
+    BFP_UNROLL for (int i = 0; i < EW; ++i) sc[i] = i == 0 ? scale : 0u;
+    (void)sub_k<EW>(t4, sc, ez);
+  }
+
+  w32 Rf[S + 3];
+  if constexpr (F::RN) {
+    Rf[0] = rem;
+    Rf[1] = q[0];
+    BFP_UNROLL for (int i = 0; i <= S; ++i) Rf[2 + i] = q[1 + i];
   } else {
-    keep = quiet & ~flush;
-    setf = quiet & ovf;
+    Rf[0] = 0;
+    Rf[1] = 0;
+    BFP_UNROLL for (int i = 0; i <= S; ++i) Rf[2 + i] = q[i];
   }
-  BFP_UNROLL for (int j = 0; j < S; ++j) Z[j] = (fr[j] & keep) | setf;
-  Z[S - 1] |= use_nan;
-  const w32 hset = SP | (~Zr & ovf);
-  BFP_UNROLL for (int j = 0; j < E; ++j) {
-    w32 v = ex[j];
-    if constexpr (!F::RN)
-      if (j == 0) {
-        Z[S] = (v & ~Zr & ~ovf) | SP;
-        continue;
-      }
-    Z[S + j] = (v & ~Zr) | hset;
-  }
-  Z[M] = sign & ~use_nan;
+  // Special-value rules of bfp_div (arith.hpp:200-205).
+  const w32 use_nan = cx.nan | cy.nan | (cx.z & cy.z) | (cx.inf & cy.inf);
+  const w32 zero_res = (cx.z | cy.inf) & ~use_nan;
+  const w32 inf_res = (cx.inf | cy.z) & ~use_nan;
+  finish_round<F>(Rf, ez, sign, zero_res, inf_res, use_nan, Z);
 }
 
 // z = round(round(a * b) + c) -- the reference chain bfp_add(bfp_mul(a,b),c),

@@ -1,6 +1,6 @@
 // bfp_kernels.cuh -- sm_100a kernels over the slice-major plane layout.
 //
-// Arithmetic (add / sub / mul / mul_add): one thread per 32-element unit.
+// Arithmetic (add / sub / mul / div / mul_add): one thread per 32-element unit.
 // A warp owns one 1024-element block: for every plane the 32 threads read 32
 // consecutive words (one 128-B line), evaluate the format's unrolled LOP3
 // network in registers and write 32 consecutive words.  Loads use the
@@ -46,6 +46,8 @@ __global__ void __launch_bounds__(kThreads) k_arith(const w32* __restrict__ x,
       add_w<F, true>(X, Y, Z);
     } else if constexpr (OP == OP_MUL) {
       mul_w<F>(X, Y, Z);
+    } else if constexpr (OP == OP_DIV) {
+      div_w<F>(X, Y, Z);
     } else {
       w32 Cc[N];
       BFP_UNROLL for (int j = 0; j < N; ++j) Cc[j] = ld_stream(c + base + j * 32);
@@ -260,6 +262,7 @@ struct FormatImpl {
       case OP_ADD: return launch_arith<OP_ADD>(x, y, c, z, units, st);
       case OP_SUB: return launch_arith<OP_SUB>(x, y, c, z, units, st);
       case OP_MUL: return launch_arith<OP_MUL>(x, y, c, z, units, st);
+      case OP_DIV: return launch_arith<OP_DIV>(x, y, c, z, units, st);
       case OP_MUL_ADD: return launch_arith<OP_MUL_ADD>(x, y, c, z, units, st);
       default: return cudaErrorInvalidValue;
     }
@@ -269,6 +272,7 @@ struct FormatImpl {
       case OP_ADD: return reinterpret_cast<const void*>(k_arith<F, OP_ADD>);
       case OP_SUB: return reinterpret_cast<const void*>(k_arith<F, OP_SUB>);
       case OP_MUL: return reinterpret_cast<const void*>(k_arith<F, OP_MUL>);
+      case OP_DIV: return reinterpret_cast<const void*>(k_arith<F, OP_DIV>);
       case OP_MUL_ADD: return reinterpret_cast<const void*>(k_arith<F, OP_MUL_ADD>);
       case 10: return reinterpret_cast<const void*>(k_pack_enc<N, EB>);
       case 11: return reinterpret_cast<const void*>(k_unpack_enc<N, EB>);

@@ -76,7 +76,7 @@ class HostCircuits:
         self.L = L
 
     def binop(self, op: str, fmt, px, py, pc=None):
-        code = {"add": 0, "sub": 1, "mul": 2, "mul_add": 4}[op]
+        code = {"add": 0, "sub": 1, "mul": 2, "div": 3, "mul_add": 4}[op]
         nb = 1 + fmt[0] + fmt[1]
         z = np.zeros_like(px)
         rc = self.L.host_binop(code, fmt[0], fmt[1], fmt[2], fmt[3], px.ctypes.data, py.ctypes.data,

@@ -30,6 +30,7 @@ static void run(int op, const uint32_t* x, const uint32_t* y, const uint32_t* c,
         case 0: add_w<F, false>(X, Y, Z); break;
         case 1: add_w<F, true>(X, Y, Z); break;
         case 2: mul_w<F>(X, Y, Z); break;
+        case 3: div_w<F>(X, Y, Z); break;
         case 4: mul_add_w<F>(X, Y, C, Z); break;
         default: return;
       }

@@ -25,13 +25,13 @@ def _check(O, host, op, fmt, x, y, c=None):
 
 @pytest.mark.parametrize("fmt2", [(3, 2), (4, 3), (5, 3)])
 @pytest.mark.parametrize("mode", MODES)
-@pytest.mark.parametrize("op", ["add", "sub", "mul"])
+@pytest.mark.parametrize("op", ["add", "sub", "mul", "div"])
 def test_exhaustive_small(oracle, host, fmt2, mode, op):
     x, y = all_pairs(1 + fmt2[0] + fmt2[1])
     _check(oracle, host, op, fmt2 + mode, x, y)
 
 
-@pytest.mark.parametrize("op", ["add", "mul"])
+@pytest.mark.parametrize("op", ["add", "mul", "div"])
 def test_exhaustive_13bit(oracle, host, op):
     """1/5/7: all 2^26 pairs, RN + gradual."""
     x, y = all_pairs(13)
@@ -48,7 +48,7 @@ def test_random_wide(oracle, host, fmt2, mode):
     y = operands(e, s, n, rng)
     y[: n // 8] = related(x[: n // 8], e, s, rng)
     c = operands(e, s, n, rng)
-    for op in ("add", "sub", "mul", "mul_add"):
+    for op in ("add", "sub", "mul", "div", "mul_add"):
         _check(oracle, host, op, fmt2 + mode, x, y, c if op == "mul_add" else None)
 
 
@@ -70,7 +70,7 @@ def test_golden_host(oracle, host):
             key = f"{e}_{s}_{rn}_{ftz}"
             x, y, c = (g[f"{k}_{key}"].astype(np.uint64) for k in "xyc")
             px, py, pc = (oracle.pack_planes(v, nb) for v in (x, y, c))
-            for op in ("add", "sub", "mul", "mul_add"):
+            for op in ("add", "sub", "mul", "div", "mul_add"):
                 z = host.binop(op, (e, s, rn, ftz), px, py, pc if op == "mul_add" else None)
                 got = oracle.unpack_planes(z, len(x), nb)
                 assert np.array_equal(got, g[f"{op}_{key}"].astype(np.uint64)), (op, key)

@@ -72,14 +72,14 @@ def test_exhaustive_small(oracle, fmt2, mode):
     x, y = all_pairs(1 + e + s)
     rng = np.random.default_rng(e + s)
     c = rng.integers(0, 1 << (1 + e + s), size=len(x), dtype=np.uint64)
-    for op in ("add", "sub", "mul", "mul_add"):
+    for op in ("add", "sub", "mul", "div", "mul_add"):
         check(oracle, op, fmt2 + mode, x, y, c if op == "mul_add" else None)
 
 
 @pytest.mark.parametrize("mode", [(1, 0), (0, 1)])
 def test_exhaustive_13bit(oracle, mode):
     x, y = all_pairs(13)
-    for op in ("add", "mul"):
+    for op in ("add", "mul", "div"):
         check(oracle, op, (5, 7) + mode, x, y)
 
 
@@ -91,7 +91,7 @@ def test_16bit_every_x(oracle, fmt2):
     ys = operands(*fmt2, 48, rng)
     x = np.repeat(xs, len(ys))
     y = np.tile(ys, len(xs))
-    for op in ("add", "sub", "mul"):
+    for op in ("add", "sub", "mul", "div"):
         check(oracle, op, fmt2 + (1, 0), x, y)
 
 
@@ -105,7 +105,7 @@ def test_random_wide(oracle, fmt2, mode):
     y = operands(e, s, n, rng)
     y[: n // 8] = related(x[: n // 8], e, s, rng)
     c = operands(e, s, n, rng)
-    for op in ("add", "sub", "mul", "mul_add"):
+    for op in ("add", "sub", "mul", "div", "mul_add"):
         check(oracle, op, fmt2 + mode, x, y, c if op == "mul_add" else None)
 
 
@@ -117,7 +117,7 @@ def test_golden_gpu(oracle):
             key = f"{e}_{s}_{rn}_{ftz}"
             x, y, c = (g[f"{k}_{key}"].astype(np.uint64) for k in "xyc")
             px, py, pc = (oracle.pack_planes(v, nb) for v in (x, y, c))
-            for op in ("add", "sub", "mul", "mul_add"):
+            for op in ("add", "sub", "mul", "div", "mul_add"):
                 z = gpu_arith(op, (e, s, rn, ftz), px, py, pc if op == "mul_add" else None)
                 got = oracle.unpack_planes(z, len(x), nb)
                 assert np.array_equal(got, g[f"{op}_{key}"].astype(np.uint64)), (op, key)
