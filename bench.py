@@ -146,48 +146,131 @@ def sass_lop3(fmt, rn, ftz, op: int) -> int | None:
 
 
 # ------------------------------------------------------------ the workloads
-def make_inputs(cfg: str, rank: int, world: int, device):
-    """Per-rank operands of config `cfg` as resident planes."""
+class Job:
+    """One timed kernel of a step: `launch(i)` issues it on the current
+    stream (i = step index, for rotating outputs)."""
+
+    def __init__(self, label, op, spec, n, launch, algo_bytes, host=None):
+        self.label, self.op, self.spec, self.n = label, op, spec, n
+        self.launch, self.algo_bytes, self.host = launch, algo_bytes, host
+
+
+def _chunked_pack_f32(gen, n, spec, device, chunk=1 << 27):
+    """pack_f32 of gen(lo, hi) in block-aligned chunks (bounded temporaries)."""
+    import torch
+    import paper_1602_04716_b200 as bfp
+    v = bfp.empty(spec, n, device)
+    nb = spec.total_bits()
+    for lo in range(0, n, chunk):
+        hi = min(n, lo + chunk)
+        x = gen(lo, hi)
+        w0 = (lo // 1024) * nb * 32
+        sub = v.planes[w0:w0 + ((hi - lo + 1023) // 1024) * nb * 32]
+        rc = bfp.lib().bfp_pack_f32(spec.c, x.data_ptr(), sub.data_ptr(), hi - lo,
+                                    torch.cuda.current_stream().cuda_stream)
+        if rc != 0:
+            raise RuntimeError(bfp.lib().bfp_last_error())
+        del x
+    return v
+
+
+def _arith_job(label, op, spec, n, a, b, c, device):
+    import torch
+    import paper_1602_04716_b200 as bfp
+    L = bfp.lib()
+    outs = [bfp.empty(spec, n, device) for _ in range(2)]  # rotating outputs
+
+    def launch(i, st):
+        rc = L.bfp_arith(OPNAMES[op], spec.c, a.planes.data_ptr(), b.planes.data_ptr(),
+                         c.planes.data_ptr() if c is not None else None,
+                         outs[i & 1].planes.data_ptr(), n, st)
+        if rc != 0:
+            raise RuntimeError(L.bfp_last_error())
+
+    nbits = spec.total_bits()
+    nin = 3 if c is not None else 2
+    return Job(label, op, spec, n, launch, (nin + 1) * nbits / 8 * n,
+               host={"kind": "arith", "op": op, "inputs": [a, b] + ([c] if c is not None else [])})
+
+
+def make_jobs(cfg: str, rank: int, world: int, device) -> list:
+    """Per-rank resident operands and the timed kernels of config `cfg`."""
     import torch
     import paper_1602_04716_b200 as bfp
     from paper_1602_04716_b200 import workloads as W
 
+    L = bfp.lib()
     if cfg == "C1":
         n = 1 << 24
         spec = bfp.make_spec(4, 3)
         lo = rank * n
         a = bfp.pack_f32(W.c1_floats(lo, lo + n, W.SEED_A, device), spec)
         b = bfp.pack_f32(W.c1_floats(lo, lo + n, W.SEED_B, device), spec)
-        return spec, n, [("add", a, b, None)]
+        return [_arith_job("add", "add", spec, n, a, b, None, device)]
     if cfg == "C2":
         n = 1 << 26
         spec = bfp.make_spec(4, 3)
         lo = rank * n
         a = bfp.pack(W.c2_encodings(lo, lo + n, W.SEED_A, device), spec)
         b = bfp.pack(W.c2_encodings(lo, lo + n, W.SEED_B, device), spec)
-        return spec, n, [("mul", a, b, None), ("sub", a, b, None)]
+        return [_arith_job("mul", "mul", spec, n, a, b, None, device),
+                _arith_job("sub", "sub", spec, n, a, b, None, device)]
+    if cfg == "C3":
+        n = 1 << 28
+        spec = bfp.make_spec(5, 10)
+        lo = rank * n
+        xa = W.c3_floats(lo, lo + n, W.SEED_A, device)
+        xb = W.c3_floats(lo, lo + n, W.SEED_B, device)
+        a, b = bfp.pack_f32(xa, spec), bfp.pack_f32(xb, spec)
+        del xb
+        torch.cuda.empty_cache()
+        pk_out = [bfp.empty(spec, n, device) for _ in range(2)]
+        up_out = [torch.empty(n, dtype=torch.float32, device=device) for _ in range(2)]
+
+        def pack_launch(i, st):
+            rc = L.bfp_pack_f32(spec.c, xa.data_ptr(), pk_out[i & 1].planes.data_ptr(), n, st)
+            if rc != 0:
+                raise RuntimeError(L.bfp_last_error())
+
+        def unpack_launch(i, st):
+            rc = L.bfp_unpack_f32(spec.c, a.planes.data_ptr(), up_out[i & 1].data_ptr(), n, st)
+            if rc != 0:
+                raise RuntimeError(L.bfp_last_error())
+
+        nb = spec.total_bits()
+        return [Job("pack_f32", "pack_f32", spec, n, pack_launch, (4 + nb / 8) * n,
+                    host={"kind": "pack_f32", "x": xa}),
+                _arith_job("add", "add", spec, n, a, b, None, device),
+                _arith_job("mul", "mul", spec, n, a, b, None, device),
+                Job("unpack_f32", "unpack_f32", spec, n, unpack_launch, (nb / 8 + 4) * n,
+                    host={"kind": "unpack_f32", "v": a})]
+    if cfg == "C4":
+        n = 1 << 28
+        lo = rank * n
+        jobs = []
+        for (e, s) in W.CONFIGS["C4"]["fmts"]:
+            spec = bfp.make_spec(e, s)
+            a = bfp.pack(W.c4_encodings(e, s, lo, lo + n, W.SEED_A, device), spec)
+            b = bfp.pack(W.c4_encodings(e, s, lo, lo + n, W.SEED_B, device), spec)
+            torch.cuda.empty_cache()
+            jobs.append(_arith_job(f"add_1/{e}/{s}", "add", spec, n, a, b, None, device))
+            jobs.append(_arith_job(f"mul_1/{e}/{s}", "mul", spec, n, a, b, None, device))
+        return jobs
     if cfg == "C5":
         total = 1 << 32
         lo, hi = W.shard(total, rank, world)
+        n = hi - lo
         spec = bfp.make_spec(6, 9)
-        ops = [bfp.pack_f32(W.c5_floats(lo, hi, sd, device), spec)
+        ops = [_chunked_pack_f32(lambda a_, b_, sd=sd: W.c5_floats(lo + a_, lo + b_, sd, device), n,
+                                 spec, device)
                for sd in (W.SEED_A, W.SEED_B, W.SEED_C)]
         torch.cuda.empty_cache()
-        return spec, hi - lo, [("mul_add", ops[0], ops[1], ops[2])]
+        return [_arith_job("mul_add", "mul_add", spec, n, ops[0], ops[1], ops[2], device)]
     raise ValueError(cfg)
 
 
-def algorithmic_bytes(op: str, nbits: int, n: int) -> float:
-    if op == "mul_add":
-        return 4 * nbits / 8 * n
-    if op == "pack_f32":
-        return (4 + nbits / 8) * n
-    if op == "unpack_f32":
-        return (nbits / 8 + 4) * n
-    return 3 * nbits / 8 * n
-
-
-def run_device(cfg: str, steps: int, warmup: int, world: int, rank: int, local: int) -> dict:
+def run_device(cfg: str, steps: int, warmup: int, world: int, rank: int, local: int,
+               jobs=None) -> dict:
     import torch
     import torch.distributed as dist
     import paper_1602_04716_b200 as bfp
@@ -195,22 +278,16 @@ def run_device(cfg: str, steps: int, warmup: int, world: int, rank: int, local: 
     device = torch.device("cuda", local)
     torch.cuda.set_device(device)
     L = bfp.lib()
-    spec, n, ops = make_inputs(cfg, rank, world, device)
-    nbits = spec.total_bits()
-    # two rotating output sets; inputs (2 x n*nbits/8 B) + outputs exceed L2
-    outs = [[bfp.empty(spec, n, device) for _ in ops] for _ in range(2)]
+    if jobs is None:
+        jobs = make_jobs(cfg, rank, world, device)
     stream = torch.cuda.current_stream(device)
+    st = stream.cuda_stream
 
     def step(i, evs=None):
-        for k, (op, a, b, c) in enumerate(ops):
+        for k, j in enumerate(jobs):
             if evs is not None:
                 evs[k][0].record(stream)
-            z = outs[i & 1][k]
-            rc = L.bfp_arith(OPNAMES[op], spec.c, a.planes.data_ptr(), b.planes.data_ptr(),
-                             c.planes.data_ptr() if c is not None else None, z.planes.data_ptr(),
-                             n, stream.cuda_stream)
-            if rc != 0:
-                raise RuntimeError(L.bfp_last_error())
+            j.launch(i, st)
             if evs is not None:
                 evs[k][1].record(stream)
 
@@ -230,9 +307,8 @@ def run_device(cfg: str, steps: int, warmup: int, world: int, rank: int, local: 
         torch.cuda.synchronize()
     clocks = cs.summary()
 
-    # timed region
     per_kernel = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-                   for _ in range(steps)] for _ in ops]
+                   for _ in range(steps)] for _ in jobs]
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if world > 1:
         dist.barrier()
@@ -240,7 +316,7 @@ def run_device(cfg: str, steps: int, warmup: int, world: int, rank: int, local: 
     launches0 = L.bfp_launch_count()
     t0.record(stream)
     for i in range(steps):
-        step(i, [[per_kernel[k][i][0], per_kernel[k][i][1]] for k in range(len(ops))])
+        step(i, [[per_kernel[k][i][0], per_kernel[k][i][1]] for k in range(len(jobs))])
     t1.record(stream)
     torch.cuda.synchronize()
     if world > 1:
@@ -248,60 +324,77 @@ def run_device(cfg: str, steps: int, warmup: int, world: int, rank: int, local: 
     launches = L.bfp_launch_count() - launches0
     ms_total = t0.elapsed_time(t1)
     kern_ms = [sum(per_kernel[k][i][0].elapsed_time(per_kernel[k][i][1]) for i in range(steps)) / steps
-               for k in range(len(ops))]
+               for k in range(len(jobs))]
     if world > 1:
         t = torch.tensor([ms_total], device=device)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_total = float(t.item())
-    return {"spec": spec, "n": n, "ops": [o[0] for o in ops], "ms_total": ms_total,
-            "kern_ms": kern_ms, "clocks": clocks, "launches": int(launches), "nbits": nbits}
+    return {"jobs": jobs, "ms_total": ms_total, "kern_ms": kern_ms, "clocks": clocks,
+            "launches": int(launches)}
 
 
-def run_e2e(cfg: str, steps: int, world: int, rank: int, local: int) -> dict:
-    """The same step through the C ABI with HOST planes (pinned): every step
+def run_e2e(cfg: str, jobs, steps: int, world: int, rank: int, local: int) -> dict:
+    """The same step through the C ABI with HOST buffers (pinned): every step
     copies its inputs H2D and its results D2H inside the timed region."""
-    import numpy as np
     import torch
     import torch.distributed as dist
     import paper_1602_04716_b200 as bfp
 
     device = torch.device("cuda", local)
     L = bfp.lib()
-    spec, n, ops = make_inputs(cfg, rank, world, device)
-    pb = spec.plane_bytes(n)
     ctx = L.bfp_host_ctx_create(1 << 22)
     bufs = []
 
-    def host_copy(t):
-        p = L.bfp_host_alloc(pb)
+    def pinned(nbytes):
+        p = L.bfp_host_alloc(nbytes)
         if not p:
             raise RuntimeError("bfp_host_alloc failed")
         bufs.append(p)
-        src = t.planes.cpu().numpy()  # keep alive across the copy
-        C.memmove(p, src.ctypes.data, pb)
+        return p
+
+    def host_copy(t: torch.Tensor):
+        nbytes = t.numel() * t.element_size()
+        p = pinned(nbytes)
+        src = t.cpu().numpy()  # keep alive across the copy
+        C.memmove(p, src.ctypes.data, nbytes)
         del src
         return p
 
     try:
-        hops = []
-        for op, a, b, c in ops:
-            hops.append((op, host_copy(a), host_copy(b), host_copy(c) if c is not None else None,
-                         L.bfp_host_alloc(pb)))
-            bufs.append(hops[-1][4])
-        del ops
+        calls = []  # (fn, h2d bytes, d2h bytes, elements)
+        for j in jobs:
+            spec, n = j.spec, j.n
+            pb = spec.plane_bytes(n)
+            if j.host["kind"] == "arith":
+                hin = [host_copy(v.planes) for v in j.host["inputs"]]
+                hz = pinned(pb)
+                hc = hin[2] if len(hin) > 2 else None
+                calls.append((lambda op=j.op, spec=spec, hin=hin, hc=hc, hz=hz, n=n:
+                              L.bfp_arith_host(ctx, OPNAMES[op], spec.c, hin[0], hin[1], hc, hz, n),
+                              len(hin) * pb, pb, n))
+            elif j.host["kind"] == "pack_f32":
+                hx = host_copy(j.host["x"])
+                hz = pinned(pb)
+                calls.append((lambda spec=spec, hx=hx, hz=hz, n=n:
+                              L.bfp_pack_f32_host(ctx, spec.c, hx, hz, n), 4 * n, pb, n))
+            elif j.host["kind"] == "unpack_f32":
+                hp = host_copy(j.host["v"].planes)
+                hz = pinned(4 * n)
+                calls.append((lambda spec=spec, hp=hp, hz=hz, n=n:
+                              L.bfp_unpack_f32_host(ctx, spec.c, hp, hz, n), pb, 4 * n, n))
         torch.cuda.empty_cache()
 
         def step():
-            for op, ha, hb, hc, hz in hops:
-                rc = L.bfp_arith_host(ctx, OPNAMES[op], spec.c, ha, hb, hc, hz, n)
+            for fn, _, _, _ in calls:
+                rc = fn()
                 if rc != 0:
                     raise RuntimeError(L.bfp_last_error())
 
         step()
         if world > 1:
             dist.barrier()
+        k = max(2, min(steps // 4, 10))
         t = time.perf_counter()
-        k = max(2, steps // 4)
         for _ in range(k):
             step()
         dt = (time.perf_counter() - t) / k
@@ -309,8 +402,8 @@ def run_e2e(cfg: str, steps: int, world: int, rank: int, local: int) -> dict:
             tt = torch.tensor([dt], device=device)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             dt = float(tt.item())
-        n_in = sum(3 if o[3] is not None else 2 for o in hops)
-        return {"s_per_step": dt, "h2d": n_in * pb, "d2h": len(hops) * pb, "elems": len(hops) * n}
+        return {"s_per_step": dt, "h2d": sum(c[1] for c in calls),
+                "d2h": sum(c[2] for c in calls), "elems": sum(c[3] for c in calls), "steps": k}
     finally:
         for p in bufs:
             L.bfp_host_free(p)
@@ -326,51 +419,96 @@ def lop3_peak() -> float | None:
 
 
 # --------------------------------------------------------- reference (CPU)
-def ref_cpu_run(cfg: str, sample: int, reps: int | None = None, seconds: float = 10.0,
-                threads: int | None = None) -> dict:
-    """The reference templates (oracle/_ref: unmodified headers + shim) over
-    `sample` elements of the config's operands, lane<1024>, all host cores."""
+def ref_cpu_jobs(cfg: str, sample: int, threads: int):
+    """The reference's CPU path for `cfg` on `sample` elements: a list of
+    (label, callable) over operands prepared outside the timing.  Arithmetic
+    runs the unmodified templates (oracle/_ref) on lane<1024> plane images;
+    C3's pack / unpack time encode_scalar + the shipped pack and the shipped
+    unpack + decode_scalar (the reference's own conversion path; its
+    transpose output is wrong -- SURVEY.md §0.4 -- but its cost is what a
+    reference user pays)."""
     import numpy as np
-    import torch
     sys.path.insert(0, str(ROOT / "oracle"))
     import oracle as O
     from paper_1602_04716_b200 import workloads as W
 
-    threads = threads or os.cpu_count() or 1
-    if cfg == "C2":
-        fmt, opl = (4, 3, 1, 0), ["mul", "sub"]
-        a = W.c2_encodings(0, sample, W.SEED_A, "cpu").numpy().astype(np.uint64)
-        b = W.c2_encodings(0, sample, W.SEED_B, "cpu").numpy().astype(np.uint64)
-        c = None
-    elif cfg == "C1":
-        fmt, opl = (4, 3, 1, 0), ["add"]
-        a = O.encode_f32(fmt, W.c1_floats(0, sample, W.SEED_A, "cpu").numpy())
-        b = O.encode_f32(fmt, W.c1_floats(0, sample, W.SEED_B, "cpu").numpy())
-        c = None
+    R = O.ref()
+    jobs = []
+
+    def arith(label, op, fmt, encs):
+        nb = 1 + fmt[0] + fmt[1]
+        planes = [O.pack_planes(v, nb) for v in encs]
+        c = planes[2] if len(planes) > 2 else None
+        jobs.append((label, lambda: O.ref_binop_planes(op, fmt, planes[0], planes[1], c,
+                                                        threads=threads)))
+
+    if cfg == "C1":
+        fmt = (4, 3, 1, 0)
+        encs = [O.encode_f32(fmt, W.c1_floats(0, sample, sd, "cpu").numpy()) for sd in (1, 2)]
+        arith("add", "add", fmt, encs)
+    elif cfg == "C2":
+        fmt = (4, 3, 1, 0)
+        encs = [W.c2_encodings(0, sample, sd, "cpu").numpy().astype(np.uint64) for sd in (1, 2)]
+        arith("mul", "mul", fmt, encs)
+        arith("sub", "sub", fmt, encs)
+    elif cfg == "C3":
+        fmt = (5, 10, 1, 0)
+        xs = [W.c3_floats(0, sample, sd, "cpu").numpy() for sd in (1, 2)]
+        encs = [O.encode_f32(fmt, x) for x in xs]
+        planes_out = np.zeros(O.nblocks(sample) * 16 * 32, dtype=np.uint32)
+        fl_out = np.zeros(sample, dtype=np.float32)
+        pa = O.pack_planes(encs[0], 16)
+        x0 = np.ascontiguousarray(xs[0])
+        jobs.append(("pack_f32", lambda: R.ref_pack_f32_path(
+            x0.ctypes.data_as(O._f32p), sample, planes_out.ctypes.data_as(O._u32p), 5, 10, 1, 0,
+            threads)))
+        arith("add", "add", fmt, encs)
+        arith("mul", "mul", fmt, encs)
+        jobs.append(("unpack_f32", lambda: R.ref_unpack_f32_path(
+            pa.ctypes.data_as(O._u32p), sample, fl_out.ctypes.data_as(O._f32p), 5, 10, threads)))
+    elif cfg == "C4":
+        for (e, s) in W.CONFIGS["C4"]["fmts"]:
+            fmt = (e, s, 1, 0)
+            encs = [W.c4_encodings(e, s, 0, sample, sd, "cpu").numpy().astype(np.uint64)
+                    for sd in (1, 2)]
+            arith(f"add_1/{e}/{s}", "add", fmt, encs)
+            arith(f"mul_1/{e}/{s}", "mul", fmt, encs)
     elif cfg == "C5":
-        fmt, opl = (6, 9, 1, 0), ["mul_add"]
-        a, b, c = (O.encode_f32(fmt, W.c5_floats(0, sample, sd, "cpu").numpy())
-                   for sd in (W.SEED_A, W.SEED_B, W.SEED_C))
+        fmt = (6, 9, 1, 0)
+        encs = [O.encode_f32(fmt, W.c5_floats(0, sample, sd, "cpu").numpy()) for sd in (1, 2, 3)]
+        arith("mul_add", "mul_add", fmt, encs)
     else:
         raise ValueError(cfg)
-    nb = 1 + fmt[0] + fmt[1]
-    pa, pb = O.pack_planes(a, nb), O.pack_planes(b, nb)
-    pc = O.pack_planes(c, nb) if c is not None else None
-    times = []
+    return jobs, O.ref_lib_path().name
+
+
+REF_SAMPLE = {"C1": 1 << 22, "C2": 1 << 22, "C3": 1 << 20, "C4": 1 << 20, "C5": 1 << 20}
+
+
+def ref_cpu_run(cfg: str, sample: int, reps: int | None = None, seconds: float = 10.0,
+                threads: int | None = None) -> dict:
+    """Time the reference's CPU path: whole steps (every job once) repeated
+    `reps` times or for ~`seconds`; rate from the best step."""
+    threads = threads or os.cpu_count() or 1
+    jobs, libname = ref_cpu_jobs(cfg, sample, threads)
+    times, per_job = [], {lbl: [] for lbl, _ in jobs}
     t_start = time.perf_counter()
     while True:
         t = time.perf_counter()
-        for op in opl:
-            O.ref_binop_planes(op, fmt, pa, pb, pc, threads=threads)
+        for lbl, fn in jobs:
+            tj = time.perf_counter()
+            fn()
+            per_job[lbl].append(time.perf_counter() - tj)
         times.append(time.perf_counter() - t)
         if reps is not None and len(times) >= reps:
             break
         if reps is None and time.perf_counter() - t_start >= seconds:
             break
     best = min(times)
-    return {"value": len(opl) * sample / best / 1e9, "cores": threads, "reps": len(times),
-            "best_s": best, "median_s": statistics.median(times), "lib": O.ref_lib_path().name,
-            "ops": opl, "sample": sample}
+    return {"value": len(jobs) * sample / best / 1e9, "cores": threads, "reps": len(times),
+            "best_s": best, "median_s": statistics.median(times), "lib": libname,
+            "ops": [lbl for lbl, _ in jobs], "sample": sample,
+            "per_op_gelems": {lbl: round(sample / min(v) / 1e9, 5) for lbl, v in per_job.items()}}
 
 
 def cpu_model() -> str:
@@ -383,22 +521,33 @@ def cpu_model() -> str:
     return "unknown"
 
 
-def config_block(cfg: str, world: int) -> dict:
-    base = {"l2": "inputs + outputs > L2 (126 MB); two rotating output sets",
-            "parallelism": f"dp{world} (independent shards, no collective)",
-            "rounding": "rn", "subnormals": "gradual"}
-    if cfg == "C2":
-        return {"workload": "C2: fp8 1/4/3 elementwise mul + sub, N=2^26 per GPU, raw encodings "
-                            "(random sign, all 16 exponent codes, 1% zeros)",
-                "format": "1/4/3", "n_per_gpu": 1 << 26, "ops_per_step": ["mul", "sub"], **base}
-    if cfg == "C1":
-        return {"workload": "C1: fp8 1/4/3 elementwise add, N=2^24 per GPU, float32 U[-16,16] "
-                            "-> encode_scalar", "format": "1/4/3", "n_per_gpu": 1 << 24,
-                "ops_per_step": ["add"], **base}
-    if cfg == "C5":
-        return {"workload": "C5: 1/6/9 z=round(round(a*b)+c), N=2^32 total split over GPUs",
-                "format": "1/6/9", "n_total": 1 << 32, "ops_per_step": ["mul_add"], **base}
-    return {"workload": cfg, **base}
+CONFIG_TEXT = {
+    "C1": ("C1: fp8 1/4/3 elementwise add, N=2^24 per GPU; float32 U[-16,16] -> encode_scalar "
+           "-> planes", "1/4/3", 1 << 24),
+    "C2": ("C2: fp8 1/4/3 elementwise mul + sub, N=2^26 per GPU; raw encodings (random sign, all "
+           "16 exponent codes incl. subnormal/Inf/NaN, 1% zeros)", "1/4/3", 1 << 26),
+    "C3": ("C3: 1/5/10 float32->bitslice pack, add, mul, bitslice->float32 unpack, N=2^28 per GPU, "
+           "each timed separately; float32 normal(0,100) clamped to +-65504", "1/5/10", 1 << 28),
+    "C4": ("C4: add + mul sweep over 1/3/2, 1/5/3, 1/5/7, 1/8/7, 1/8/15, N=2^28 per GPU per "
+           "format; uniform finite bit patterns", "sweep", 1 << 28),
+    "C5": ("C5: 1/6/9 z=round(round(a*b)+c) fused, N=2^32 total split evenly over the GPUs; "
+           "float32 sign x 2^U[-10,9] x U[1,2) -> encode_scalar", "1/6/9", None),
+}
+
+
+def config_block(cfg: str, world: int, jobs=None) -> dict:
+    text, fmt, n = CONFIG_TEXT[cfg]
+    d = {"workload": text, "format": fmt, "rounding": "rn", "subnormals": "gradual",
+         "parallelism": f"dp{world} (independent block-aligned shards, no collective)",
+         "l2": "every input > L2 (126 MB) except C1 (48 MB working set); outputs rotate over "
+               "two buffers"}
+    if n:
+        d["n_per_gpu"] = n
+    else:
+        d["n_total"] = 1 << 32
+    if jobs is not None:
+        d["ops_per_step"] = [j.label for j in jobs]
+    return d
 
 
 # ------------------------------------------------------------------- arms
@@ -406,27 +555,28 @@ def main_reference(args) -> None:
     world, rank, local = env_dist()
     if rank != 0:
         return
-    cfg = args.config
-    sample = {"C2": 1 << 24, "C1": 1 << 24, "C5": 1 << 22}[cfg]
-    for _ in range(args.warmup):
-        ref_cpu_run(cfg, sample, reps=1)
-    r = ref_cpu_run(cfg, sample, reps=args.steps)
-    ms = r["median_s"] * 1e3
-    value = r["value"]
-    line = {
-        "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": UNIT,
-        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32 (bitslice)",
-        "data": "synthetic (seeded SplitMix64 operands; BASELINE.json configs)",
-        "config": config_block(cfg, world),
-        "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": r["cores"],
-                         "kind": "reference",
-                         "sample": f"{r['sample']} elements x {r['ops']} per step, lane<1024>, "
-                                   f"{r['cores']} threads, {cpu_model()}, {r['lib']}"},
-        "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
-                "d2h_bytes_per_step": 0},
-    }
-    print(json.dumps(line), flush=True)
+    for cfg in args.configs:
+        sample = REF_SAMPLE[cfg]
+        r = ref_cpu_run(cfg, sample, reps=args.warmup)  # warm-up steps
+        r = ref_cpu_run(cfg, sample, reps=args.steps)
+        value = r["value"]
+        line = {
+            "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": UNIT,
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(r["median_s"] * 1e3, 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u64 lanes (lane<1024> bitslice)",
+            "data": "synthetic (seeded SplitMix64 operands; BASELINE.json configs)",
+            "config": config_block(cfg, world),
+            "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": r["cores"],
+                             "kind": "reference",
+                             "sample": f"{r['sample']} elements x {r['ops']} per step, "
+                                       f"lane<1024>, {r['cores']} threads, {cpu_model()}, "
+                                       f"{r['lib']}",
+                             "per_op": r["per_op_gelems"]},
+            "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
+        }
+        print(json.dumps(line), flush=True)
 
 
 def main_ours(args) -> None:
@@ -436,76 +586,94 @@ def main_ours(args) -> None:
     world, rank, local = env_dist()
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    cfg = args.config
     log = (lambda m: print(f"[bench r{rank}] {m}", file=sys.stderr, flush=True))
-    log(f"device timing {cfg}")
-    res = run_device(cfg, args.steps, args.warmup, world, rank, local)
-    if clocks_rejected(res["clocks"]):  # re-measure once
+    peak_lop3 = None
+    for cfg in args.configs:
+        log(f"device timing {cfg}")
         res = run_device(cfg, args.steps, args.warmup, world, rank, local)
-    log(f"device done: {res['ms_total'] / args.steps:.4f} ms/step; e2e")
-    e2e = run_e2e(cfg, args.steps, world, rank, local)
-    log("lop3 probe")
-    peak_lop3 = lop3_peak() if rank == 0 else None
+        if clocks_rejected(res["clocks"]):  # re-measure once
+            log("clocks rejected; re-measuring")
+            res = run_device(cfg, args.steps, args.warmup, world, rank, local, jobs=res["jobs"])
+        jobs = res["jobs"]
+        log(f"device done: {res['ms_total'] / args.steps:.4f} ms/step; e2e")
+        e2e = run_e2e(cfg, jobs, args.steps, world, rank, local) if not args.no_e2e else None
+        if peak_lop3 is None and rank == 0:
+            log("lop3 probe")
+            peak_lop3 = lop3_peak()
 
-    spec, n, nbits = res["spec"], res["n"], res["nbits"]
-    total_elems = n * len(res["ops"]) * world
-    ms_step = res["ms_total"] / args.steps
-    value = total_elems / (ms_step * 1e-3) / 1e9
-    k_dom = max(range(len(res["ops"])), key=lambda k: res["kern_ms"][k])
-    op_dom = res["ops"][k_dom]
-    dur = res["kern_ms"][k_dom] * 1e-3
-    algo = algorithmic_bytes(op_dom, nbits, n)
-    peaks = measured_peaks()
-    achieved = algo / dur / 1e9
-    e, s = spec.exp_bits, spec.sig_bits
-    lop3 = sass_lop3((e, s), int(spec.rounding), int(spec.subnormals), OPNAMES[op_dom])
-    traffic = None
-    tfile = ROOT / "profiles" / "ncu_traffic.json"
-    if tfile.exists():
-        tj = json.loads(tfile.read_text())
-        traffic = tj.get(f"{cfg}:{op_dom}")
-    roof = {
-        "bound": "hbm", "kernel": f"k_arith<{e},{s},rn>:{op_dom}",
-        "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
-        "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": traffic,
-        "peak_source": peaks["source"], "algorithmic_bytes_per_launch": int(algo),
-        "launch_ms": round(dur * 1e3, 4),
-        "per_op_ms": {o: round(t, 4) for o, t in zip(res["ops"], res["kern_ms"])},
-    }
-    if lop3 is not None and peak_lop3:
-        per_elem = lop3 / 32.0
-        ach = per_elem * n / dur
-        roof["logic"] = {"lop3_per_elem_sass": round(per_elem, 3), "achieved_lop3_per_s": ach,
-                         "peak_lop3_per_s_measured": peak_lop3, "frac": round(ach / peak_lop3, 4)}
-        hbm_t = algo / (peaks["hbm_gbs"] * 1e9)
-        logic_t = per_elem * n / peak_lop3
-        roof["binding_leg"] = "logic" if logic_t > hbm_t else "hbm"
-        roof["frac_of_binding"] = round(max(hbm_t, logic_t) / dur, 4)
-
-    line = {
-        "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 5),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "u32 (bitslice words; 1/4/3 custom FP)",
-        "data": "synthetic (seeded SplitMix64 operands; BASELINE.json configs)",
-        "config": config_block(cfg, world),
-        "roofline": roof,
-        "e2e": {"value": round(e2e["elems"] * world / e2e["s_per_step"] / 1e9, 3), "unit": UNIT,
-                "h2d_bytes_per_step": int(e2e["h2d"]), "d2h_bytes_per_step": int(e2e["d2h"]),
-                "path": "bfp_arith_host (C ABI, pinned host planes, chunked H2D/kernel/D2H)"},
-        "clocks": res["clocks"],
-        "gpu_launches": res["launches"],
-    }
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        log("cpu baseline")
-        cb = ref_cpu_run(cfg, 1 << 22, seconds=args.cpu_seconds)
-        line["cpu_baseline"] = {
-            "value": round(cb["value"], 4), "unit": UNIT, "cores": cb["cores"], "kind": "reference",
-            "sample": f"{cb['sample']} elements x {cb['ops']}, best of {cb['reps']} reps "
-                      f"(~{args.cpu_seconds:.0f} s), lane<1024>, {cb['cores']} threads, "
-                      f"{cpu_model()}, {cb['lib']}"}
-    if rank == 0:
-        print(json.dumps(line), flush=True)
+        total_elems = sum(j.n for j in jobs) * world
+        ms_step = res["ms_total"] / args.steps
+        value = total_elems / (ms_step * 1e-3) / 1e9
+        peaks = measured_peaks()
+        per_op = {}
+        roofs = []
+        for j, ms in zip(jobs, res["kern_ms"]):
+            dur = ms * 1e-3
+            ach = j.algo_bytes / dur / 1e9
+            e, s = j.spec.exp_bits, j.spec.sig_bits
+            ent = {"ms": round(ms, 4), "gelem_s": round(j.n / dur / 1e9, 2),
+                   "hbm_gbs": round(ach, 1), "hbm_frac": round(ach / peaks["hbm_gbs"], 4)}
+            if j.op in OPNAMES:
+                lop3 = sass_lop3((e, s), int(j.spec.rounding), int(j.spec.subnormals), OPNAMES[j.op])
+                if lop3 is not None and peak_lop3:
+                    pe = lop3 / 32.0
+                    hbm_t = j.algo_bytes / (peaks["hbm_gbs"] * 1e9)
+                    logic_t = pe * j.n / peak_lop3
+                    ent.update({"lop3_per_elem": round(pe, 3),
+                                "logic_frac": round(logic_t / dur, 4),
+                                "binding": "logic" if logic_t > hbm_t else "hbm",
+                                "frac_of_binding": round(max(hbm_t, logic_t) / dur, 4)})
+            per_op[j.label] = ent
+            roofs.append((ms, j, ach))
+        ms_dom, jd, ach = max(roofs, key=lambda r: r[0])
+        traffic = None
+        tfile = ROOT / "profiles" / "ncu_traffic.json"
+        if tfile.exists():
+            traffic = json.loads(tfile.read_text()).get(f"{cfg}:{jd.label}")
+        roof = {"bound": "hbm", "kernel": f"{jd.label} (1/{jd.spec.exp_bits}/{jd.spec.sig_bits} rn)",
+                "achieved": round(ach, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": round(ach / peaks["hbm_gbs"], 4), "traffic": traffic,
+                "peak_source": peaks["source"],
+                "algorithmic_bytes_per_launch": int(jd.algo_bytes),
+                "launch_ms": round(ms_dom, 4), "per_op": per_op}
+        if peak_lop3:
+            roof["peak_lop3_per_s_measured"] = peak_lop3
+        dd = per_op[jd.label]
+        if "binding" in dd:
+            roof["binding_leg"] = dd["binding"]
+            roof["frac_of_binding"] = dd["frac_of_binding"]
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 5),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "u32 (bitslice words)",
+            "data": "synthetic (seeded SplitMix64 operands; BASELINE.json configs)",
+            "config": config_block(cfg, world, jobs),
+            "roofline": roof,
+            "clocks": res["clocks"],
+            "gpu_launches": res["launches"],
+        }
+        if e2e is not None:
+            line["e2e"] = {"value": round(e2e["elems"] * world / e2e["s_per_step"] / 1e9, 3),
+                           "unit": UNIT, "h2d_bytes_per_step": int(e2e["h2d"]),
+                           "d2h_bytes_per_step": int(e2e["d2h"]),
+                           "path": "C ABI host entry points (bfp_*_host: pinned host buffers, "
+                                   "chunked H2D / kernel / D2H on 3 streams)",
+                           "steps": e2e["steps"]}
+        if rank == 0 and world == 1 and not args.no_cpu_baseline:
+            log("cpu baseline")
+            cb = ref_cpu_run(cfg, REF_SAMPLE[cfg], seconds=args.cpu_seconds)
+            line["cpu_baseline"] = {
+                "value": round(cb["value"], 4), "unit": UNIT, "cores": cb["cores"],
+                "kind": "reference",
+                "sample": f"{cb['sample']} elements x {cb['ops']} per step, best of {cb['reps']} "
+                          f"steps (~{args.cpu_seconds:.0f} s), lane<1024>, {cb['cores']} threads, "
+                          f"{cpu_model()}, {cb['lib']}",
+                "per_op": cb["per_op_gelems"]}
+        del jobs, res
+        torch.cuda.empty_cache()
+        if rank == 0:
+            print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
 
@@ -517,10 +685,13 @@ def main() -> None:
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", default="C2", choices=["C1", "C2", "C5"])
+    ap.add_argument("--config", default="C2", help="C1..C5, comma list, or 'all'")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     args = ap.parse_args()
+    args.configs = (["C1", "C2", "C3", "C4", "C5"] if args.config == "all"
+                    else args.config.split(","))
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
