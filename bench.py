@@ -174,13 +174,25 @@ def _chunked_pack_f32(gen, n, spec, device, chunk=1 << 27):
     return v
 
 
-def _arith_job(label, op, spec, n, a, b, c, device):
+L2_BYTES = 126 * 1024 * 1024
+
+
+def input_sets(spec, n, n_inputs: int) -> int:
+    """Rotating input sets so that consecutive uses of one set are separated
+    by >= 2x L2 of other traffic (inputs always come from HBM)."""
+    set_bytes = n_inputs * spec.plane_bytes(n)
+    return max(1, -(-2 * L2_BYTES // set_bytes))
+
+
+def _arith_job(label, op, spec, n, sets, device):
+    """sets: list of (a, b, c) operand tuples rotated step by step."""
     import torch
     import paper_1602_04716_b200 as bfp
     L = bfp.lib()
     outs = [bfp.empty(spec, n, device) for _ in range(2)]  # rotating outputs
 
     def launch(i, st):
+        a, b, c = sets[i % len(sets)]
         rc = L.bfp_arith(OPNAMES[op], spec.c, a.planes.data_ptr(), b.planes.data_ptr(),
                          c.planes.data_ptr() if c is not None else None,
                          outs[i & 1].planes.data_ptr(), n, st)
@@ -188,9 +200,11 @@ def _arith_job(label, op, spec, n, a, b, c, device):
             raise RuntimeError(L.bfp_last_error())
 
     nbits = spec.total_bits()
+    a, b, c = sets[0]
     nin = 3 if c is not None else 2
     return Job(label, op, spec, n, launch, (nin + 1) * nbits / 8 * n,
-               host={"kind": "arith", "op": op, "inputs": [a, b] + ([c] if c is not None else [])})
+               host={"kind": "arith", "op": op, "inputs": [a, b] + ([c] if c is not None else []),
+                     "sets": len(sets)})
 
 
 def make_jobs(cfg: str, rank: int, world: int, device) -> list:
@@ -204,17 +218,23 @@ def make_jobs(cfg: str, rank: int, world: int, device) -> list:
         n = 1 << 24
         spec = bfp.make_spec(4, 3)
         lo = rank * n
-        a = bfp.pack_f32(W.c1_floats(lo, lo + n, W.SEED_A, device), spec)
-        b = bfp.pack_f32(W.c1_floats(lo, lo + n, W.SEED_B, device), spec)
-        return [_arith_job("add", "add", spec, n, a, b, None, device)]
+        sets = []
+        for r in range(input_sets(spec, n, 2)):  # same data, distinct buffers
+            if r == 0:
+                a = bfp.pack_f32(W.c1_floats(lo, lo + n, W.SEED_A, device), spec)
+                b = bfp.pack_f32(W.c1_floats(lo, lo + n, W.SEED_B, device), spec)
+            sets.append((a, b, None) if r == 0 else (a.clone(), b.clone(), None))
+        return [_arith_job("add", "add", spec, n, sets, device)]
     if cfg == "C2":
         n = 1 << 26
         spec = bfp.make_spec(4, 3)
         lo = rank * n
         a = bfp.pack(W.c2_encodings(lo, lo + n, W.SEED_A, device), spec)
         b = bfp.pack(W.c2_encodings(lo, lo + n, W.SEED_B, device), spec)
-        return [_arith_job("mul", "mul", spec, n, a, b, None, device),
-                _arith_job("sub", "sub", spec, n, a, b, None, device)]
+        sets = [(a, b, None)] + [(a.clone(), b.clone(), None)
+                                 for _ in range(input_sets(spec, n, 2) - 1)]
+        return [_arith_job("mul", "mul", spec, n, sets, device),
+                _arith_job("sub", "sub", spec, n, sets, device)]
     if cfg == "C3":
         n = 1 << 28
         spec = bfp.make_spec(5, 10)
@@ -240,8 +260,8 @@ def make_jobs(cfg: str, rank: int, world: int, device) -> list:
         nb = spec.total_bits()
         return [Job("pack_f32", "pack_f32", spec, n, pack_launch, (4 + nb / 8) * n,
                     host={"kind": "pack_f32", "x": xa}),
-                _arith_job("add", "add", spec, n, a, b, None, device),
-                _arith_job("mul", "mul", spec, n, a, b, None, device),
+                _arith_job("add", "add", spec, n, [(a, b, None)], device),
+                _arith_job("mul", "mul", spec, n, [(a, b, None)], device),
                 Job("unpack_f32", "unpack_f32", spec, n, unpack_launch, (nb / 8 + 4) * n,
                     host={"kind": "unpack_f32", "v": a})]
     if cfg == "C4":
@@ -253,8 +273,8 @@ def make_jobs(cfg: str, rank: int, world: int, device) -> list:
             a = bfp.pack(W.c4_encodings(e, s, lo, lo + n, W.SEED_A, device), spec)
             b = bfp.pack(W.c4_encodings(e, s, lo, lo + n, W.SEED_B, device), spec)
             torch.cuda.empty_cache()
-            jobs.append(_arith_job(f"add_1/{e}/{s}", "add", spec, n, a, b, None, device))
-            jobs.append(_arith_job(f"mul_1/{e}/{s}", "mul", spec, n, a, b, None, device))
+            jobs.append(_arith_job(f"add_1/{e}/{s}", "add", spec, n, [(a, b, None)], device))
+            jobs.append(_arith_job(f"mul_1/{e}/{s}", "mul", spec, n, [(a, b, None)], device))
         return jobs
     if cfg == "C5":
         total = 1 << 32
@@ -265,7 +285,7 @@ def make_jobs(cfg: str, rank: int, world: int, device) -> list:
                                  spec, device)
                for sd in (W.SEED_A, W.SEED_B, W.SEED_C)]
         torch.cuda.empty_cache()
-        return [_arith_job("mul_add", "mul_add", spec, n, ops[0], ops[1], ops[2], device)]
+        return [_arith_job("mul_add", "mul_add", spec, n, [tuple(ops)], device)]
     raise ValueError(cfg)
 
 
@@ -539,8 +559,8 @@ def config_block(cfg: str, world: int, jobs=None) -> dict:
     text, fmt, n = CONFIG_TEXT[cfg]
     d = {"workload": text, "format": fmt, "rounding": "rn", "subnormals": "gradual",
          "parallelism": f"dp{world} (independent block-aligned shards, no collective)",
-         "l2": "every input > L2 (126 MB) except C1 (48 MB working set); outputs rotate over "
-               "two buffers"}
+         "l2": "inputs larger than L2: operand sets rotate step by step so each set is reused "
+               "only after >= 2x L2 (126 MB) of other traffic; outputs rotate over two buffers"}
     if n:
         d["n_per_gpu"] = n
     else:

@@ -151,31 +151,42 @@ __global__ void __launch_bounds__(kThreads) k_unpack_enc(const w32* __restrict__
   }
 }
 
-// float32 -> encode_scalar -> planes.
+// float32 -> encode_scalar -> planes.  Hardware cvt (binary16 / bfloat16)
+// where it coincides with the reference converter, else the branch-free
+// per-element encoder; then the register transpose.
 template <class F>
 __global__ void __launch_bounds__(kThreads) k_pack_f32(const float* __restrict__ in,
                                                        w32* __restrict__ planes, size_t n,
                                                        size_t units, bool aligned) {
   constexpr int N = F::N;
+  constexpr int HW = HwCodec<F>::kind;
   const size_t stride = size_t(gridDim.x) * kThreads;
   const uint8_t* inb = reinterpret_cast<const uint8_t*>(in);
   for (size_t u = size_t(blockIdx.x) * kThreads + threadIdx.x; u < units; u += stride) {
     w32 V[32];
-    load_unit<4>(inb, u, n, aligned, V);
-    BFP_UNROLL for (int k = 0; k < 32; ++k) V[k] = encode_f32<F>(V[k]);  // +0 -> 0 on the tail
+    load_unit<4>(inb, u, n, aligned, V);  // zero past n -> +0 encodes to 0
     w32 P[32];
-    if constexpr (N <= 8) {
-      w32 L[8];
-      BFP_UNROLL for (int q = 0; q < 8; ++q)
-        L[q] = V[4 * q] | (V[4 * q + 1] << 8) | (V[4 * q + 2] << 16) | (V[4 * q + 3] << 24);
-      enc8_to_planes(L, P);
-    } else if constexpr (N <= 16) {
+    if constexpr (HW != 0) {
       w32 L[16];
-      BFP_UNROLL for (int q = 0; q < 16; ++q) L[q] = V[2 * q] | (V[2 * q + 1] << 16);
+      BFP_UNROLL for (int q = 0; q < 16; ++q)
+        L[q] = hw_cvt2<HW, F::RN>(__uint_as_float(V[2 * q]), __uint_as_float(V[2 * q + 1]));
       enc16_to_planes(L, P);
+      canon_nan_planes<F>(P);
     } else {
-      BFP_UNROLL for (int i = 0; i < 32; ++i) P[i] = V[i];
-      enc32_to_planes(P);
+      BFP_UNROLL for (int k = 0; k < 32; ++k) V[k] = encode_f32_fast<F>(V[k]);
+      if constexpr (N <= 8) {
+        w32 L[8];
+        BFP_UNROLL for (int q = 0; q < 8; ++q)
+          L[q] = V[4 * q] | (V[4 * q + 1] << 8) | (V[4 * q + 2] << 16) | (V[4 * q + 3] << 24);
+        enc8_to_planes(L, P);
+      } else if constexpr (N <= 16) {
+        w32 L[16];
+        BFP_UNROLL for (int q = 0; q < 16; ++q) L[q] = V[2 * q] | (V[2 * q + 1] << 16);
+        enc16_to_planes(L, P);
+      } else {
+        BFP_UNROLL for (int i = 0; i < 32; ++i) P[i] = V[i];
+        enc32_to_planes(P);
+      }
     }
     const size_t base = (u >> 5) * (size_t(N) * 32) + (u & 31);
     BFP_UNROLL for (int j = 0; j < N; ++j) st_stream(planes + base + j * 32, P[j]);
@@ -188,6 +199,7 @@ __global__ void __launch_bounds__(kThreads) k_unpack_f32(const w32* __restrict__
                                                          float* __restrict__ out, size_t n,
                                                          size_t units, bool aligned) {
   constexpr int N = F::N;
+  constexpr int HW = HwCodec<F>::kind;
   const size_t stride = size_t(gridDim.x) * kThreads;
   uint8_t* outb = reinterpret_cast<uint8_t*>(out);
   for (size_t u = size_t(blockIdx.x) * kThreads + threadIdx.x; u < units; u += stride) {
@@ -195,19 +207,29 @@ __global__ void __launch_bounds__(kThreads) k_unpack_f32(const w32* __restrict__
     w32 P[32];
     BFP_UNROLL for (int j = 0; j < 32; ++j) P[j] = (j < N) ? ld_stream(planes + base + j * 32) : 0u;
     w32 V[32];
-    if constexpr (N <= 8) {
-      w32 L[8];
-      planes_to_enc8(P, L);
-      BFP_UNROLL for (int k = 0; k < 32; ++k) V[k] = (L[k >> 2] >> (8 * (k & 3))) & 0xffu;
-    } else if constexpr (N <= 16) {
+    if constexpr (HW != 0) {
+      canon_nan_planes<F>(P);  // 0x7e00 / 0x7fc0 widen to 0x7fc00000
       w32 L[16];
       planes_to_enc16(P, L);
-      BFP_UNROLL for (int k = 0; k < 32; ++k) V[k] = (L[k >> 1] >> (16 * (k & 1))) & 0xffffu;
+      BFP_UNROLL for (int q = 0; q < 16; ++q) {
+        V[2 * q] = hw_widen<HW>(L[q] & 0xffffu);
+        V[2 * q + 1] = hw_widen<HW>(L[q] >> 16);
+      }
     } else {
-      planes_to_enc32(P);
-      BFP_UNROLL for (int k = 0; k < 32; ++k) V[k] = P[k];
+      if constexpr (N <= 8) {
+        w32 L[8];
+        planes_to_enc8(P, L);
+        BFP_UNROLL for (int k = 0; k < 32; ++k) V[k] = (L[k >> 2] >> (8 * (k & 3))) & 0xffu;
+      } else if constexpr (N <= 16) {
+        w32 L[16];
+        planes_to_enc16(P, L);
+        BFP_UNROLL for (int k = 0; k < 32; ++k) V[k] = (L[k >> 1] >> (16 * (k & 1))) & 0xffffu;
+      } else {
+        planes_to_enc32(P);
+        BFP_UNROLL for (int k = 0; k < 32; ++k) V[k] = P[k];
+      }
+      BFP_UNROLL for (int k = 0; k < 32; ++k) V[k] = decode_f32_fast<F>(V[k]);
     }
-    BFP_UNROLL for (int k = 0; k < 32; ++k) V[k] = decode_f32<F>(V[k]);
     store_unit<4>(outb, u, n, aligned, V);
   }
 }

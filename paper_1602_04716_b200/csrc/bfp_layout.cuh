@@ -19,6 +19,8 @@
 // The codec follows encode_scalar / decode_scalar (format.hpp:101-188) for
 // binary32 inputs / outputs.
 #pragma once
+#include <string.h>
+
 #include "bfp_circuits.cuh"
 
 namespace bfpg {
@@ -219,5 +221,137 @@ BFP_HD w32 decode_f32(w32 enc) {
   }
   return sign | (w32(int(be) - F::BIAS + 127) << 23) | (fr << (23 - S));
 }
+
+// ------------------------------------------------ branch-free codec
+// The kernels use these; encode_f32 / decode_f32 above are the direct
+// restatements they are checked against (tests/test_circuits_host.py).
+
+// Subnormal-range rounding: frac = round(|x| / 2^(emin - S)) for |x| < 2^emin.
+template <class F>
+BFP_HD w32 sub_round(w32 a) {
+  constexpr int EMIN = 1 - F::BIAS, S = F::S;
+#if defined(__CUDA_ARCH__)
+  // one FADD at the subnormal ulp: |x| + 2^(emin - S + 23) rounds |x| to a
+  // multiple of 2^(emin - S) (RN-even or RZ in hardware, exactly like the
+  // reference's guard/sticky rounding); the sum's low bits are the fraction.
+  const float M = __uint_as_float(w32(127 + EMIN - S + 23) << 23);
+  const float x = __uint_as_float(a);
+  const float sum = F::RN ? __fadd_rn(x, M) : __fadd_rz(x, M);
+  return __float_as_uint(sum) - __float_as_uint(M);
+#else
+  const int ef = int(a >> 23);
+  const uint64_t sig = ef ? ((a & 0x7fffffu) | 0x800000u) : a;
+  const int e = (ef ? ef : 1) - 150;
+  const int shift = (EMIN - S) - e;  // >= 1 in the subnormal range
+  if (shift >= 40) return 0;
+  uint64_t kept = sig >> shift;
+  const uint64_t g = (sig >> (shift - 1)) & 1u;
+  const uint64_t st = (sig & ((uint64_t(1) << (shift - 1)) - 1)) != 0;
+  if (F::RN && g && (st || (kept & 1u))) ++kept;
+  return w32(kept);
+#endif
+}
+
+template <class F>
+BFP_HD w32 encode_f32_fast(w32 u) {
+  constexpr int E = F::E, S = F::S, SH = 23 - S;
+  constexpr int EMIN = 1 - F::BIAS, EMAX = F::BIAS;
+  constexpr w32 EMASK = (1u << E) - 1;
+  constexpr w32 FMASK = (1u << S) - 1;
+  const w32 a = u & 0x7fffffffu;
+  w32 t = a;
+  if constexpr (SH > 0 && F::RN) t = a + ((1u << (SH - 1)) - 1u) + ((a >> SH) & 1u);
+  const w32 enc_n = (t >> SH) - (w32(127 - F::BIAS) << S);
+  constexpr w32 MINN = w32(127 + EMIN) << 23;     // 2^emin
+  constexpr w32 OVF = w32(127 + EMAX + 1) << 23;  // 2^(emax+1)
+  w32 r = (a < MINN) ? sub_round<F>(a) : enc_n;
+  if constexpr (OVF < 0x7f800000u || F::RN) {
+    if (t >= OVF) r = F::RN ? (EMASK << S) : (((EMASK - 1) << S) | FMASK);
+  }
+  if constexpr (F::FTZ) r = (r <= FMASK) ? 0u : r;
+  r = (a == 0x7f800000u) ? (EMASK << S) : r;
+  r |= (u >> 31) << (E + S);
+  return (a > 0x7f800000u) ? ((EMASK << S) | (1u << (S - 1))) : r;
+}
+
+template <class F>
+BFP_HD w32 decode_f32_fast(w32 enc) {
+  constexpr int E = F::E, S = F::S, SH = 23 - S;
+  constexpr int EMIN = 1 - F::BIAS;
+  constexpr w32 EMASK = (1u << E) - 1;
+  const w32 mag = enc & ((1u << (E + S)) - 1u);
+  const w32 be = mag >> S;
+  const w32 r_n = (mag << SH) + (w32(127 - F::BIAS) << 23);
+  // subnormal: as_float(bits(M) + frac) - M == frac * 2^(emin - S), exact
+  constexpr w32 MB = w32(127 + EMIN - S + 23) << 23;
+#if defined(__CUDA_ARCH__)
+  const w32 r_s = __float_as_uint(__uint_as_float(MB + mag) - __uint_as_float(MB));
+#else
+  float fa, fm;
+  const w32 ta = MB + mag, tm = MB;
+  memcpy(&fa, &ta, 4);
+  memcpy(&fm, &tm, 4);
+  const float d = fa - fm;
+  w32 r_s;
+  memcpy(&r_s, &d, 4);
+#endif
+  w32 r = (be == 0) ? r_s : r_n;
+  r = (be == EMASK) ? 0x7f800000u : r;
+  r |= ((enc >> (E + S)) & 1u) << 31;
+  return (be == EMASK && (mag & ((1u << S) - 1u))) ? 0x7fc00000u : r;
+}
+
+// Canonical NaN in the bitslice domain: every element whose exponent planes
+// are all ones and whose fraction is nonzero becomes the canonical NaN
+// (positive, fraction MSB only -- format.hpp:49-52).  ~(E+S)/2 + N LOP3s
+// per 32 elements.
+template <class F>
+BFP_HD void canon_nan_planes(w32* P) {
+  constexpr int E = F::E, S = F::S;
+  w32 ea = ONES, fo = 0;
+  BFP_UNROLL for (int i = 0; i < E; ++i) ea &= P[S + i];
+  BFP_UNROLL for (int i = 0; i < S; ++i) fo |= P[i];
+  const w32 nan = ea & fo;
+  BFP_UNROLL for (int j = 0; j < S - 1; ++j) P[j] &= ~nan;
+  P[S - 1] |= nan;
+  P[S + E] &= ~nan;
+}
+
+// Hardware conversion applies when IEEE binary16 / bfloat16 conversion
+// equals encode_scalar / decode_scalar for the format (RN-even or RZ,
+// gradual underflow, overflow to Inf / max-finite) -- NaN aside, which the
+// planes fix above canonicalises.  0 = generic, 1 = binary16, 2 = bfloat16.
+template <class F>
+struct HwCodec {
+  static constexpr int kind = F::FTZ ? 0 : (F::E == 5 && F::S == 10) ? 1 : (F::E == 8 && F::S == 7) ? 2 : 0;
+};
+
+#if defined(__CUDACC__)
+// two floats -> two encodings packed lo | hi << 16 (cvt.*.x2: first source
+// to the upper half)
+template <int KIND, bool RN>
+__device__ __forceinline__ w32 hw_cvt2(float lo, float hi) {
+  w32 r;
+  if constexpr (KIND == 1) {
+    if constexpr (RN) asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+    else asm("cvt.rz.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  } else {
+    if constexpr (RN) asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+    else asm("cvt.rz.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  }
+  return r;
+}
+
+template <int KIND>
+__device__ __forceinline__ w32 hw_widen(w32 h16) {
+  if constexpr (KIND == 1) {
+    float f;
+    asm("{.reg .b16 h; cvt.u16.u32 h, %1; cvt.f32.f16 %0, h;}" : "=f"(f) : "r"(h16));
+    return __float_as_uint(f);
+  } else {
+    return h16 << 16;
+  }
+}
+#endif
 
 }  // namespace bfpg

@@ -40,7 +40,14 @@ static void run(int op, const uint32_t* x, const uint32_t* y, const uint32_t* c,
 
 template <class F>
 static void codec(int dir, const uint32_t* in, uint32_t* out, size_t n) {
-  for (size_t i = 0; i < n; ++i) out[i] = dir == 0 ? encode_f32<F>(in[i]) : decode_f32<F>(in[i]);
+  for (size_t i = 0; i < n; ++i) {
+    switch (dir) {
+      case 0: out[i] = encode_f32<F>(in[i]); break;
+      case 1: out[i] = decode_f32<F>(in[i]); break;
+      case 2: out[i] = encode_f32_fast<F>(in[i]); break;
+      default: out[i] = decode_f32_fast<F>(in[i]); break;
+    }
+  }
 }
 
 template <int E_, int S_, class Fn>

@@ -86,15 +86,17 @@ def test_codec_host(oracle, host, fmt2):
         rng.integers(90, 165, size=1 << 14, dtype=np.uint64).astype(np.uint32) << 23)
     for mode in MODES:
         fmt = fmt2 + mode
-        got = host.codec(0, fmt, bits).astype(np.uint64)
         want = oracle.encode_f32(fmt, bits.view(np.float32))
-        assert np.array_equal(got, want), (fmt, int((got != want).sum()))
+        for direction in (0, 2):  # restatement and branch-free kernel codec
+            got = host.codec(direction, fmt, bits).astype(np.uint64)
+            assert np.array_equal(got, want), (fmt, direction, int((got != want).sum()))
     nb = 1 + e + s
     encs = (np.arange(1 << nb, dtype=np.uint64) if nb <= 16
             else rng.integers(0, 1 << nb, size=1 << 16, dtype=np.uint64))
-    got = host.codec(1, (e, s, 1, 0), encs.astype(np.uint32))
     want = oracle.decode_f32((e, s, 1, 0), encs).view(np.uint32)
-    assert np.array_equal(got, want)
+    for direction in (1, 3):
+        got = host.codec(direction, (e, s, 1, 0), encs.astype(np.uint32))
+        assert np.array_equal(got, want), direction
 
 
 # ---------------------------------------------------------------------- layout

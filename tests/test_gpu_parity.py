@@ -362,3 +362,39 @@ def test_launch_counter():
     v = bfp.pack(torch.arange(2048, device="cuda") % 256, spec)
     bfp.bfp_add(v, v)
     assert L.bfp_launch_count() == before + 2
+
+
+@pytest.mark.slow
+def test_pack_f32_all_binary32_1_5_10():
+    """encode_scalar for 1/5/10 RN + gradual on ALL 2^32 float32 inputs (the
+    hardware-cvt path) equals IEEE binary16 RN conversion (torch's own
+    float -> half kernel); NaNs must be the canonical 0x7e00."""
+    spec = bfp.make_spec(5, 10)
+    chunk = 1 << 28
+    nan_canon = torch.tensor(0x7E00, dtype=torch.int16, device="cuda")
+    for lo in range(0, 1 << 32, chunk):
+        bits = torch.arange(lo, lo + chunk, dtype=torch.int64, device="cuda").to(torch.int32)
+        x = bits.view(torch.float32)
+        got = bfp.unpack(bfp.pack_f32(x, spec))
+        want = x.to(torch.float16).view(torch.int16)
+        want = torch.where(torch.isnan(x), nan_canon, want)
+        assert torch.equal(got, want), hex(lo)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("fmt2", FORMATS)
+@pytest.mark.parametrize("mode", MODES)
+def test_pack_f32_strided_sweep(oracle, fmt2, mode):
+    """every 4099th binary32 bit pattern (~1M inputs spanning all exponents,
+    both signs, subnormals, Inf, NaN) through pack_f32 / unpack_f32."""
+    e, s = fmt2
+    spec = bfp.make_spec(e, s, mode[0], mode[1])
+    fmt = fmt2 + mode
+    bits = (np.arange(0, 1 << 32, 4099, dtype=np.uint64)).astype(np.uint32)
+    xs = bits.view(np.float32)
+    v = bfp.pack_f32(torch.from_numpy(xs).cuda(), spec)
+    want = oracle.encode_f32(fmt, xs)
+    got = bfp.to_u64(bfp.unpack(v), spec).cpu().numpy().astype(np.uint64)
+    assert np.array_equal(got, want), int((got != want).sum())
+    back = bfp.unpack_f32(v).cpu().numpy().view(np.uint32)
+    assert np.array_equal(back, oracle.decode_f32(fmt, want).view(np.uint32))

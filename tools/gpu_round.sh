@@ -1,9 +1,5 @@
 set -x
-P="python tools/profile_kernels.py --config C2 --iters 4"
-$P > gpurun_out/plain.log 2>&1 && \
-ncu --metrics gpu__time_duration.sum --clock-control none -k regex:k_arith --csv --log-file gpurun_out/launches_c2.csv $P > gpurun_out/ncu1.log 2>&1
-echo rc1=$?
-$P > gpurun_out/plain2.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:k_arith -s 2 -c 2 -o gpurun_out/prof_c2 $P > gpurun_out/ncu2.log 2>&1
-echo rc2=$?
-ls -la gpurun_out
+timeout 1200 python -m pytest tests -x -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; echo pytest_rc=$?
+tail -5 gpurun_out/pytest_gpu.log
+timeout 1500 python bench.py --config all --steps 20 --warmup 3 > gpurun_out/bench_all.log 2> gpurun_out/bench_all.err; echo bench_rc=$?
+tail -5 gpurun_out/bench_all.err
