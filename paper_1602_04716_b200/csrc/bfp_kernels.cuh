@@ -105,16 +105,99 @@ __device__ __forceinline__ void store_unit(uint8_t* __restrict__ enc, size_t u, 
   }
 }
 
+// Warp-cooperative tile through shared memory: lane t owns row t (its
+// unit's 32 elements = CH 16-byte chunks); global memory sees the tile
+// row-major, so each warp instruction moves 512 contiguous bytes.  Chunks
+// are XOR-swizzled by row so the row-wise and the flat accesses are both
+// (nearly) bank-conflict free.  Requires the whole warp active.
+template <int CH>
+__device__ __forceinline__ int tile_off(int row, int chunk) {
+  return row * (CH * 4) + ((chunk ^ (row & (CH - 1))) << 2);
+}
+
+template <int CH>
+__device__ __forceinline__ void tile_store_rows(w32* tile, const w32* V, int lane) {
+  BFP_UNROLL for (int c = 0; c < CH; ++c)
+    *reinterpret_cast<uint4*>(tile + tile_off<CH>(lane, c)) =
+        make_uint4(V[4 * c], V[4 * c + 1], V[4 * c + 2], V[4 * c + 3]);
+}
+
+template <int CH>
+__device__ __forceinline__ void tile_load_rows(const w32* tile, w32* V, int lane) {
+  BFP_UNROLL for (int c = 0; c < CH; ++c) {
+    const uint4 q = *reinterpret_cast<const uint4*>(tile + tile_off<CH>(lane, c));
+    V[4 * c] = q.x;
+    V[4 * c + 1] = q.y;
+    V[4 * c + 2] = q.z;
+    V[4 * c + 3] = q.w;
+  }
+}
+
+// global (32 * CH * 4 contiguous words at g) <-> tile, flat order
+template <int CH>
+__device__ __forceinline__ void tile_from_global(w32* tile, const w32* __restrict__ g, int lane) {
+  BFP_UNROLL for (int i = 0; i < CH; ++i) {
+    const int flat = i * 128 + lane * 4;  // word index in the tile
+    const uint4 q = __ldcs(reinterpret_cast<const uint4*>(g + flat));
+    *reinterpret_cast<uint4*>(tile + tile_off<CH>(flat / (CH * 4), (flat % (CH * 4)) >> 2)) = q;
+  }
+}
+
+template <int CH>
+__device__ __forceinline__ void tile_to_global(const w32* tile, w32* __restrict__ g, int lane) {
+  BFP_UNROLL for (int i = 0; i < CH; ++i) {
+    const int flat = i * 128 + lane * 4;
+    const uint4 q =
+        *reinterpret_cast<const uint4*>(tile + tile_off<CH>(flat / (CH * 4), (flat % (CH * 4)) >> 2));
+    __stcs(reinterpret_cast<uint4*>(g + flat), q);
+  }
+}
+
+// Element side of one warp's 1024 elements (EB bytes each): coalesced via the
+// tile when the warp's range is complete and 16-B aligned, else per element.
+template <int EB>
+__device__ __forceinline__ void warp_load_elems(const uint8_t* __restrict__ src, size_t u, size_t n,
+                                                bool aligned, w32* tile, int lane, w32* L) {
+  constexpr int CH = 2 * EB;
+  const size_t e0w = (u - lane) * 32;
+  if (aligned && e0w + 1024 <= n) {
+    tile_from_global<CH>(tile, reinterpret_cast<const w32*>(src + e0w * EB), lane);
+    __syncwarp();
+    tile_load_rows<CH>(tile, L, lane);
+    __syncwarp();
+  } else {
+    load_unit<EB>(src, u, n, aligned, L);
+  }
+}
+
+template <int EB>
+__device__ __forceinline__ void warp_store_elems(uint8_t* __restrict__ dst, size_t u, size_t n,
+                                                 bool aligned, w32* tile, int lane, const w32* L) {
+  constexpr int CH = 2 * EB;
+  const size_t e0w = (u - lane) * 32;
+  if (aligned && e0w + 1024 <= n) {
+    tile_store_rows<CH>(tile, L, lane);
+    __syncwarp();
+    tile_to_global<CH>(tile, reinterpret_cast<w32*>(dst + e0w * EB), lane);
+    __syncwarp();
+  } else {
+    store_unit<EB>(dst, u, n, aligned, L);
+  }
+}
+
 // Raw encodings (EB = 1/2/4 bytes each) -> planes.  Every unit of every
 // block is written; elements >= n are zero (pack.hpp:50).
 template <int N, int EB>
 __global__ void __launch_bounds__(kThreads) k_pack_enc(const uint8_t* __restrict__ enc,
                                                        w32* __restrict__ planes, size_t n,
                                                        size_t units, bool aligned) {
+  __shared__ __align__(16) w32 tiles[kThreads / 32][256 * EB];
+  const int lane = threadIdx.x & 31;
+  w32* tile = tiles[threadIdx.x >> 5];
   const size_t stride = size_t(gridDim.x) * kThreads;
   for (size_t u = size_t(blockIdx.x) * kThreads + threadIdx.x; u < units; u += stride) {
     w32 L[32 * EB / 4];
-    load_unit<EB>(enc, u, n, aligned, L);
+    warp_load_elems<EB>(enc, u, n, aligned, tile, lane, L);
     w32 P[32];
     if constexpr (EB == 1) {
       enc8_to_planes(L, P);
@@ -133,8 +216,12 @@ template <int N, int EB>
 __global__ void __launch_bounds__(kThreads) k_unpack_enc(const w32* __restrict__ planes,
                                                          uint8_t* __restrict__ enc, size_t n,
                                                          size_t units, bool aligned) {
+  __shared__ __align__(16) w32 tiles[kThreads / 32][256 * EB];
+  const int lane = threadIdx.x & 31;
+  w32* tile = tiles[threadIdx.x >> 5];
   const size_t stride = size_t(gridDim.x) * kThreads;
-  for (size_t u = size_t(blockIdx.x) * kThreads + threadIdx.x; u < units; u += stride) {
+  const size_t wunits = (units + 31) & ~size_t(31);  // whole warps (planes exist)
+  for (size_t u = size_t(blockIdx.x) * kThreads + threadIdx.x; u < wunits; u += stride) {
     const size_t base = (u >> 5) * (size_t(N) * 32) + (u & 31);
     w32 P[32];
     BFP_UNROLL for (int j = 0; j < 32; ++j) P[j] = (j < N) ? ld_stream(planes + base + j * 32) : 0u;
@@ -147,7 +234,7 @@ __global__ void __launch_bounds__(kThreads) k_unpack_enc(const w32* __restrict__
       planes_to_enc32(P);
       BFP_UNROLL for (int i = 0; i < 32; ++i) L[i] = P[i];
     }
-    store_unit<EB>(enc, u, n, aligned, L);
+    warp_store_elems<EB>(enc, u, n, aligned, tile, lane, L);
   }
 }
 
@@ -160,11 +247,15 @@ __global__ void __launch_bounds__(kThreads) k_pack_f32(const float* __restrict__
                                                        size_t units, bool aligned) {
   constexpr int N = F::N;
   constexpr int HW = HwCodec<F>::kind;
+  __shared__ __align__(16) w32 tiles[kThreads / 32][1024];
+  const int lane = threadIdx.x & 31;
+  w32* tile = tiles[threadIdx.x >> 5];
   const size_t stride = size_t(gridDim.x) * kThreads;
   const uint8_t* inb = reinterpret_cast<const uint8_t*>(in);
+  // units is a multiple of 32 (whole blocks), so warps stay converged
   for (size_t u = size_t(blockIdx.x) * kThreads + threadIdx.x; u < units; u += stride) {
     w32 V[32];
-    load_unit<4>(inb, u, n, aligned, V);  // zero past n -> +0 encodes to 0
+    warp_load_elems<4>(inb, u, n, aligned, tile, lane, V);  // zero past n -> +0 -> 0
     w32 P[32];
     if constexpr (HW != 0) {
       w32 L[16];
@@ -200,9 +291,13 @@ __global__ void __launch_bounds__(kThreads) k_unpack_f32(const w32* __restrict__
                                                          size_t units, bool aligned) {
   constexpr int N = F::N;
   constexpr int HW = HwCodec<F>::kind;
+  __shared__ __align__(16) w32 tiles[kThreads / 32][1024];
+  const int lane = threadIdx.x & 31;
+  w32* tile = tiles[threadIdx.x >> 5];
   const size_t stride = size_t(gridDim.x) * kThreads;
   uint8_t* outb = reinterpret_cast<uint8_t*>(out);
-  for (size_t u = size_t(blockIdx.x) * kThreads + threadIdx.x; u < units; u += stride) {
+  const size_t wunits = (units + 31) & ~size_t(31);  // whole warps (planes exist)
+  for (size_t u = size_t(blockIdx.x) * kThreads + threadIdx.x; u < wunits; u += stride) {
     const size_t base = (u >> 5) * (size_t(N) * 32) + (u & 31);
     w32 P[32];
     BFP_UNROLL for (int j = 0; j < 32; ++j) P[j] = (j < N) ? ld_stream(planes + base + j * 32) : 0u;
@@ -230,7 +325,7 @@ __global__ void __launch_bounds__(kThreads) k_unpack_f32(const w32* __restrict__
       }
       BFP_UNROLL for (int k = 0; k < 32; ++k) V[k] = decode_f32_fast<F>(V[k]);
     }
-    store_unit<4>(outb, u, n, aligned, V);
+    warp_store_elems<4>(outb, u, n, aligned, tile, lane, V);
   }
 }
 

@@ -347,7 +347,11 @@ __device__ __forceinline__ w32 hw_widen(w32 h16) {
   if constexpr (KIND == 1) {
     float f;
     asm("{.reg .b16 h; cvt.u16.u32 h, %1; cvt.f32.f16 %0, h;}" : "=f"(f) : "r"(h16));
-    return __float_as_uint(f);
+    // NaN inputs are canonical and positive here (canon_nan_planes); the
+    // widening may return its own canonical NaN (0x7fffffff): a signed min
+    // maps every positive NaN pattern above 0x7fc00000 to quiet_NaN() and
+    // leaves finite values, +Inf and all negative values unchanged.
+    return w32(min(int(__float_as_uint(f)), 0x7fc00000));
   } else {
     return h16 << 16;
   }
