@@ -4,6 +4,7 @@
 
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -18,6 +19,16 @@ BFP_FORMAT_LIST(DECLARE_IMPL)
 }  // namespace bfpg
 
 using bfpg::Impl;
+
+namespace bfpg {
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* v = std::getenv("BFP_PDL");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
+}  // namespace bfpg
 
 namespace {
 

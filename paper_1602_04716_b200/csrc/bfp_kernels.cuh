@@ -24,35 +24,65 @@ enum Op { OP_ADD = 0, OP_SUB = 1, OP_MUL = 2, OP_DIV = 3, OP_MUL_ADD = 4 };
 constexpr int kThreads = 128;
 
 __device__ __forceinline__ w32 ld_stream(const w32* p) { return __ldcs(p); }
+
+// Programmatic dependent launch: every kernel lets the next kernel in the
+// stream be scheduled at once (its CTAs fill SMs as ours retire) and waits for
+// the previous grid to complete -- memory included -- before its first
+// global access, so stream-ordered dependent calls remain correct.  Both are
+// no-ops when the launch did not enable PDL.
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
 __device__ __forceinline__ void st_stream(w32* p, w32 v) { __stcs(p, v); }
 
+// Operands of one unit: NIN inputs x N planes, loaded with the streaming path.
+template <int N, int NIN>
+struct Operands {
+  w32 v[NIN][N];
+  __device__ __forceinline__ void load(const w32* __restrict__ x, const w32* __restrict__ y,
+                                       const w32* __restrict__ c, size_t base) {
+    BFP_UNROLL for (int j = 0; j < N; ++j) {
+      v[0][j] = ld_stream(x + base + j * 32);
+      v[1][j] = ld_stream(y + base + j * 32);
+      if constexpr (NIN == 3) v[2][j] = ld_stream(c + base + j * 32);
+    }
+  }
+};
+
+template <class F, int OP>
+__device__ __forceinline__ void eval_unit(const w32* X, const w32* Y, const w32* Cc, w32* Z) {
+  if constexpr (OP == OP_ADD) {
+    add_w<F, false>(X, Y, Z);
+  } else if constexpr (OP == OP_SUB) {
+    add_w<F, true>(X, Y, Z);
+  } else if constexpr (OP == OP_MUL) {
+    mul_w<F>(X, Y, Z);
+  } else if constexpr (OP == OP_DIV) {
+    div_w<F>(X, Y, Z);
+  } else {
+    mul_add_w<F>(X, Y, Cc, Z);
+  }
+}
+
+// One thread per unit, grid-stride.  (A register double-buffered variant --
+// next unit's loads issued before the current network -- measured slower on
+// the B200: the extra registers cost more occupancy than the overlap gained.)
 template <class F, int OP>
 __global__ void __launch_bounds__(kThreads) k_arith(const w32* __restrict__ x,
                                                     const w32* __restrict__ y,
                                                     const w32* __restrict__ c,
                                                     w32* __restrict__ z, size_t units) {
+  pdl_enter();
   constexpr int N = F::N;
+  constexpr int NIN = OP == OP_MUL_ADD ? 3 : 2;
   const size_t stride = size_t(gridDim.x) * kThreads;
   for (size_t u = size_t(blockIdx.x) * kThreads + threadIdx.x; u < units; u += stride) {
     const size_t base = (u >> 5) * (size_t(N) * 32) + (u & 31);
-    w32 X[N], Y[N], Z[N];
-    BFP_UNROLL for (int j = 0; j < N; ++j) {
-      X[j] = ld_stream(x + base + j * 32);
-      Y[j] = ld_stream(y + base + j * 32);
-    }
-    if constexpr (OP == OP_ADD) {
-      add_w<F, false>(X, Y, Z);
-    } else if constexpr (OP == OP_SUB) {
-      add_w<F, true>(X, Y, Z);
-    } else if constexpr (OP == OP_MUL) {
-      mul_w<F>(X, Y, Z);
-    } else if constexpr (OP == OP_DIV) {
-      div_w<F>(X, Y, Z);
-    } else {
-      w32 Cc[N];
-      BFP_UNROLL for (int j = 0; j < N; ++j) Cc[j] = ld_stream(c + base + j * 32);
-      mul_add_w<F>(X, Y, Cc, Z);
-    }
+    Operands<N, NIN> cur;
+    cur.load(x, y, c, base);
+    w32 Z[N];
+    eval_unit<F, OP>(cur.v[0], cur.v[1], cur.v[NIN - 1], Z);
     BFP_UNROLL for (int j = 0; j < N; ++j) st_stream(z + base + j * 32, Z[j]);
   }
 }
@@ -191,6 +221,7 @@ template <int N, int EB>
 __global__ void __launch_bounds__(kThreads) k_pack_enc(const uint8_t* __restrict__ enc,
                                                        w32* __restrict__ planes, size_t n,
                                                        size_t units, bool aligned) {
+  pdl_enter();
   __shared__ __align__(16) w32 tiles[kThreads / 32][256 * EB];
   const int lane = threadIdx.x & 31;
   w32* tile = tiles[threadIdx.x >> 5];
@@ -216,6 +247,7 @@ template <int N, int EB>
 __global__ void __launch_bounds__(kThreads) k_unpack_enc(const w32* __restrict__ planes,
                                                          uint8_t* __restrict__ enc, size_t n,
                                                          size_t units, bool aligned) {
+  pdl_enter();
   __shared__ __align__(16) w32 tiles[kThreads / 32][256 * EB];
   const int lane = threadIdx.x & 31;
   w32* tile = tiles[threadIdx.x >> 5];
@@ -245,6 +277,7 @@ template <class F>
 __global__ void __launch_bounds__(kThreads) k_pack_f32(const float* __restrict__ in,
                                                        w32* __restrict__ planes, size_t n,
                                                        size_t units, bool aligned) {
+  pdl_enter();
   constexpr int N = F::N;
   constexpr int HW = HwCodec<F>::kind;
   __shared__ __align__(16) w32 tiles[kThreads / 32][1024];
@@ -289,6 +322,7 @@ template <class F>
 __global__ void __launch_bounds__(kThreads) k_unpack_f32(const w32* __restrict__ planes,
                                                          float* __restrict__ out, size_t n,
                                                          size_t units, bool aligned) {
+  pdl_enter();
   constexpr int N = F::N;
   constexpr int HW = HwCodec<F>::kind;
   __shared__ __align__(16) w32 tiles[kThreads / 32][1024];
@@ -330,6 +364,22 @@ __global__ void __launch_bounds__(kThreads) k_unpack_f32(const w32* __restrict__
 }
 
 // ------------------------------------------------------- launch + table
+bool pdl_enabled();  // bfp_capi.cu: BFP_PDL environment switch (default on)
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch(void (*k)(KArgs...), int grid, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
+
 // Resident CTAs for a full wave of `kernel`: #SM x occupancy.
 template <typename K>
 inline int wave_ctas(K kernel) {
@@ -368,8 +418,7 @@ struct FormatImpl {
                                   cudaStream_t st) {
     auto k = k_arith<F, OP>;
     static const int wave = wave_ctas(k);
-    k<<<grid_for(wave, units), kThreads, 0, st>>>(x, y, c, z, units);
-    return cudaGetLastError();
+    return launch(k, grid_for(wave, units), st, x, y, c, z, units);
   }
   static cudaError_t arith(int op, const w32* x, const w32* y, const w32* c, w32* z,
                            size_t nblocks, cudaStream_t st) {
@@ -405,9 +454,8 @@ struct FormatImpl {
     const bool al = (reinterpret_cast<uintptr_t>(enc) & 15) == 0;
     auto k = k_pack_enc<N, EB>;
     static const int wave = wave_ctas(k);
-    k<<<grid_for(wave, units), kThreads, 0, st>>>(static_cast<const uint8_t*>(enc), planes, n,
+    return launch(k, grid_for(wave, units), st, static_cast<const uint8_t*>(enc), planes, n,
                                                       units, al);
-    return cudaGetLastError();
   }
   static cudaError_t unpack_enc(const w32* planes, void* enc, size_t n, cudaStream_t st) {
     const size_t units = (n + 31) / 32;
@@ -415,9 +463,8 @@ struct FormatImpl {
     const bool al = (reinterpret_cast<uintptr_t>(enc) & 15) == 0;
     auto k = k_unpack_enc<N, EB>;
     static const int wave = wave_ctas(k);
-    k<<<grid_for(wave, units), kThreads, 0, st>>>(planes, static_cast<uint8_t*>(enc), n, units,
+    return launch(k, grid_for(wave, units), st, planes, static_cast<uint8_t*>(enc), n, units,
                                                       al);
-    return cudaGetLastError();
   }
   static cudaError_t pack_f32(const float* in, w32* planes, size_t n, cudaStream_t st) {
     if constexpr (F::E > 8 || F::S > 23) {
@@ -428,8 +475,7 @@ struct FormatImpl {
       const bool al = (reinterpret_cast<uintptr_t>(in) & 15) == 0;
       auto k = k_pack_f32<F>;
       static const int wave = wave_ctas(k);
-      k<<<grid_for(wave, units), kThreads, 0, st>>>(in, planes, n, units, al);
-      return cudaGetLastError();
+      return launch(k, grid_for(wave, units), st, in, planes, n, units, al);
     }
   }
   static cudaError_t unpack_f32(const w32* planes, float* out, size_t n, cudaStream_t st) {
@@ -441,8 +487,7 @@ struct FormatImpl {
       const bool al = (reinterpret_cast<uintptr_t>(out) & 15) == 0;
       auto k = k_unpack_f32<F>;
       static const int wave = wave_ctas(k);
-      k<<<grid_for(wave, units), kThreads, 0, st>>>(planes, out, n, units, al);
-      return cudaGetLastError();
+      return launch(k, grid_for(wave, units), st, planes, out, n, units, al);
     }
   }
   static const Impl* get() {
