@@ -68,6 +68,42 @@ constexpr int imin(int a, int b) { return a < b ? a : b; }
 BFP_HD w32 mux(w32 s, w32 a, w32 b) { return (s & a) | (~s & b); }  // s ? a : b
 BFP_HD w32 maj(w32 a, w32 b, w32 c) { return (a & b) | (c & (a | b)); }
 
+// Pinned 3-input LUTs.  ptxas maps plain C expressions greedily and fuses a
+// shared sub-term (e.g. a partial product) into every consumer, duplicating
+// it; where the optimal cover is known, the network is written directly in
+// lop3.b32 so ptxas keeps exactly one LOP3 per node.
+#if defined(__CUDA_ARCH__)
+template <int LUT>
+__device__ __forceinline__ w32 lop3(w32 a, w32 b, w32 c) {
+  w32 r;
+  asm("lop3.b32 %0, %1, %2, %3, %4;" : "=r"(r) : "r"(a), "r"(b), "r"(c), "n"(LUT));
+  return r;
+}
+#else
+template <int LUT>
+inline w32 lop3(w32 a, w32 b, w32 c) {
+  w32 r = 0;
+  for (int k = 0; k < 8; ++k) {
+    const w32 ta = (k & 4) ? a : ~a, tb = (k & 2) ? b : ~b, tc = (k & 1) ? c : ~c;
+    if ((LUT >> k) & 1) r |= ta & tb & tc;
+  }
+  return r;
+}
+#endif
+// LUT encodings over (a, b, c) = (0xF0, 0xCC, 0xAA)
+constexpr int L_AND2 = 0xC0;       // a & b
+constexpr int L_XOR3 = 0x96;       // a ^ b ^ c
+constexpr int L_MAJ = 0xE8;        // maj(a, b, c)
+constexpr int L_XOR_AND = 0x6A;    // c ^ (a & b)
+constexpr int L_AND3 = 0x80;       // a & b & c
+constexpr int L_MUX = 0xCA;        // a ? b : c
+constexpr int L_ANDN = 0x30;       // a & ~b
+constexpr int L_OR3 = 0xFE;        // a | b | c
+
+// Pinned mux / masked copy (one LOP3 each, never duplicated into consumers).
+BFP_HD w32 pmux(w32 s, w32 a, w32 b) { return lop3<L_MUX>(s, a, b); }
+BFP_HD w32 pandn(w32 a, w32 s) { return lop3<L_ANDN>(a, s, 0u); }
+
 // a >= v for an unsigned K-bit field a (LSB first) and a constant v.
 template <int K>
 BFP_HD w32 ge_const(const w32* a, int v) {
@@ -88,7 +124,8 @@ BFP_HD void shr_jam_stage(w32 (&f)[W], w32 sel) {
     BFP_UNROLL for (int i = 1; i <= DIST && i < W; ++i) t |= f[i];
     w32 nf[W];
     nf[0] = f[0] | (sel & t);
-    BFP_UNROLL for (int i = 1; i < W; ++i) nf[i] = mux(sel, (i + DIST < W) ? f[i + DIST] : 0u, f[i]);
+    BFP_UNROLL for (int i = 1; i < W; ++i)
+      nf[i] = (i + DIST < W) ? pmux(sel, f[i + DIST], f[i]) : pandn(f[i], sel);
     BFP_UNROLL for (int i = 0; i < W; ++i) f[i] = nf[i];
   } else {
     w32 t = 0;
@@ -110,7 +147,8 @@ BFP_HD void shr_jam(w32 (&f)[W], const w32* amt) {
 template <int W, int DIST>
 BFP_HD void shl_stage(w32 (&f)[W], w32 sel) {
   w32 nf[W];
-  BFP_UNROLL for (int i = 0; i < W; ++i) nf[i] = mux(sel, (i >= DIST) ? f[i - DIST] : 0u, f[i]);
+  BFP_UNROLL for (int i = 0; i < W; ++i)
+    nf[i] = (i >= DIST) ? pmux(sel, f[i - DIST], f[i]) : pandn(f[i], sel);
   BFP_UNROLL for (int i = 0; i < W; ++i) f[i] = nf[i];
 }
 
@@ -199,8 +237,8 @@ BFP_HD void add_w(const w32* X, const w32* Y, w32* Z) {
   const w32 swap = bw;
   w32 A[M], B[M];
   BFP_UNROLL for (int i = 0; i < M; ++i) {
-    A[i] = mux(swap, Y[i], X[i]);
-    B[i] = mux(swap, X[i], Y[i]);
+    A[i] = pmux(swap, Y[i], X[i]);
+    B[i] = pmux(swap, X[i], Y[i]);
   }
   const w32 sa = mux(swap, sy, sx);
   const w32 sb = mux(swap, sx, sy);
@@ -282,7 +320,8 @@ BFP_HD void add_w(const w32* X, const w32* Y, w32* Z) {
     const w32 c = ok & ~any;
     sh[k] = c;
     w32 nx[WN];
-    BFP_UNROLL for (int i = 0; i < WN; ++i) nx[i] = mux(c, (i >= D) ? x[i - D] : 0u, x[i]);
+    BFP_UNROLL for (int i = 0; i < WN; ++i)
+      nx[i] = (i >= D) ? pmux(c, x[i - D], x[i]) : pandn(x[i], c);
     BFP_UNROLL for (int i = 0; i < WN; ++i) x[i] = nx[i];
     if (k > 0) {
       // r -= c << k (r >= 2^k whenever c is set)
@@ -458,7 +497,8 @@ BFP_HD void mul_w(const w32* X, const w32* Y, w32* Z) {
   const w32 sign = X[M] ^ Y[M];
   const Classes cx = classify<F>(X), cy = classify<F>(Y);
 
-  // Exact product of the (S+1)-bit significands: shift-add rows.
+  // Exact product of the (S+1)-bit significands: shift-add rows, one carry
+  // chain per row; each cell = AND (partial product) + XOR3 + MAJ, pinned.
   constexpr int WP = 2 * S + 2;
   w32 P[WP];
   {
@@ -469,15 +509,22 @@ BFP_HD void mul_w(const w32* X, const w32* Y, w32* Z) {
     }
     mx[S] = cx.h;
     my[S] = cy.h;
-    BFP_UNROLL for (int j = 0; j <= S; ++j) P[j] = mx[j] & my[0];
-    BFP_UNROLL for (int j = S + 1; j < WP; ++j) P[j] = 0;
+    BFP_UNROLL for (int j = 0; j <= S; ++j) P[j] = lop3<L_AND2>(mx[j], my[0], 0u);
     BFP_UNROLL for (int i = 1; i <= S; ++i) {
-      w32 c = 0;
-      BFP_UNROLL for (int j = 0; j <= S; ++j) {
-        const w32 pp = mx[j] & my[i];
+      // j = 0: carry-in 0 -> sum = a ^ pp, carry = a & pp (AND fused)
+      w32 c = lop3<L_AND3>(mx[0], my[i], P[i]);
+      P[i] = lop3<L_XOR_AND>(mx[0], my[i], P[i]);
+      BFP_UNROLL for (int j = 1; j <= S; ++j) {
+        if (i == 1 && j == S) {  // nothing accumulated above row 0 yet
+          const w32 s0 = lop3<L_XOR_AND>(mx[j], my[i], c);
+          c = lop3<L_AND3>(mx[j], my[i], c);
+          P[i + j] = s0;
+          continue;
+        }
+        const w32 pp = lop3<L_AND2>(mx[j], my[i], 0u);
         const w32 a = P[i + j];
-        P[i + j] = a ^ pp ^ c;
-        c = maj(a, pp, c);
+        P[i + j] = lop3<L_XOR3>(a, pp, c);
+        c = lop3<L_MAJ>(a, pp, c);
       }
       P[i + S + 1] = c;
     }
@@ -583,7 +630,7 @@ BFP_HD void div_w(const w32* X, const w32* Y, w32* Z) {
     const w32 borrow = sub_k<W1 + 1>(r2, den, tr);
     const w32 qt = ~borrow;
     q[t] = qt;
-    BFP_UNROLL for (int i = 0; i < W1; ++i) R[i] = mux(qt, tr[i], r2[i]);
+    BFP_UNROLL for (int i = 0; i < W1; ++i) R[i] = (i == 0) ? (tr[0] & qt) : pmux(qt, tr[i], r2[i]);
   }
   w32 rem = 0;
   if constexpr (F::RN) {
