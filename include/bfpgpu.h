@@ -84,6 +84,15 @@ bfp_status bfp_pack_f32(const bfp_format* f, const float* d_in, uint32_t* d_plan
 bfp_status bfp_unpack_f32(const bfp_format* f, const uint32_t* d_planes, float* d_out,
                           size_t count, void* stream);
 
+/* .bfpraw records (pack.hpp:78-109): count = nbytes / bfp_bfpraw_stride(f)
+ * little-endian ceil(n/8)-byte encodings, back to back, no padding.
+ * BFP_ESIZE when nbytes is not a multiple of the stride (pack.hpp:98-100). */
+size_t bfp_bfpraw_stride(const bfp_format* f);
+bfp_status bfp_pack_bfpraw(const bfp_format* f, const void* d_bytes, size_t nbytes,
+                           uint32_t* d_planes, void* stream);
+bfp_status bfp_unpack_bfpraw(const bfp_format* f, const uint32_t* d_planes, size_t count,
+                             void* d_bytes, void* stream);
+
 /* ---- arithmetic (device buffers, all operands in format f) --------------- */
 bfp_status bfp_add(const bfp_format* f, const uint32_t* d_x, const uint32_t* d_y,
                    uint32_t* d_z, size_t count, void* stream);

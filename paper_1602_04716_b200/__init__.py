@@ -16,6 +16,9 @@ from .bfp import (  # noqa: F401
     bfp_mul_add,
     bfp_sub,
     bfp_vector,
+    bfpraw_stride,
+    pack_bfpraw,
+    unpack_bfpraw,
     decode_scalar,
     empty,
     encode_scalar,

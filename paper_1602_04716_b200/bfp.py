@@ -185,6 +185,37 @@ def unpack(v: bfp_vector, count: int | None = None) -> torch.Tensor:
     return out
 
 
+def bfpraw_stride(spec: format_spec) -> int:
+    """pack.hpp:78-80."""
+    return (spec.total_bits() + 7) // 8
+
+
+def pack_bfpraw(raw: torch.Tensor, spec: format_spec) -> bfp_vector:
+    """.bfpraw bytes (device uint8: little-endian ceil(n/8)-byte records,
+    pack.hpp:78-109) -> planes.  ValueError when the length is not a multiple
+    of the stride (from_bfpraw, pack.hpp:98-100)."""
+    validate(spec)
+    raw = raw.to(torch.uint8).contiguous()
+    stride = bfpraw_stride(spec)
+    if raw.numel() % stride:
+        raise ValueError("bfpraw: byte count not a multiple of the encoding stride")
+    out = empty(spec, raw.numel() // stride, raw.device)
+    check(lib().bfp_pack_bfpraw(spec.c, raw.data_ptr(), raw.numel(), out.planes.data_ptr(),
+                                _stream()), "pack_bfpraw")
+    return out
+
+
+def unpack_bfpraw(v: bfp_vector, count: int | None = None) -> torch.Tensor:
+    """planes -> .bfpraw bytes (to_bfpraw, pack.hpp:86-95)."""
+    count = v.count if count is None else count
+    if count > v.count:
+        raise ValueError("unpack_bfpraw: count exceeds vector width")
+    out = torch.empty(count * bfpraw_stride(v.spec), dtype=torch.uint8, device=v.planes.device)
+    check(lib().bfp_unpack_bfpraw(v.spec.c, v.planes.data_ptr(), count, out.data_ptr(), _stream()),
+          "unpack_bfpraw")
+    return out
+
+
 def to_u64(encs: torch.Tensor, spec: format_spec) -> torch.Tensor:
     """Bit patterns of `unpack` as non-negative int64."""
     mask = (1 << spec.total_bits()) - 1

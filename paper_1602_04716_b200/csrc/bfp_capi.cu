@@ -210,6 +210,45 @@ bfp_status bfp_unpack_f32(const bfp_format* f, const uint32_t* d_planes, float* 
                      "unpack_f32 launch");
 }
 
+// .bfpraw (pack.hpp:78-109): little-endian ceil(n/8)-byte records, no padding.
+size_t bfp_bfpraw_stride(const bfp_format* f) {
+  if (validate(f) != BFP_OK) return 0;
+  return (nplanes(f) + 7) / 8;
+}
+
+bfp_status bfp_pack_bfpraw(const bfp_format* f, const void* d_bytes, size_t nbytes,
+                           uint32_t* d_planes, void* stream) {
+  const Impl* impl = nullptr;
+  const bfp_status s = resolve(f, &impl);
+  if (s != BFP_OK) return s;
+  const size_t stride = bfp_bfpraw_stride(f);
+  if (nbytes % stride != 0)
+    return fail(BFP_ESIZE, "bfpraw: byte count not a multiple of the encoding stride");
+  const size_t count = nbytes / stride;
+  if (count == 0) return BFP_OK;
+  if (!d_bytes || !d_planes) return fail(BFP_EARG, "null buffer");
+  if (stride > 4) return fail(BFP_EUNSUPPORTED, "bfpraw: records wider than 4 bytes");
+  ++g_launches;
+  const cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (stride == 3) return cuda_status(impl->pack_raw3(d_bytes, d_planes, count, st), "pack_bfpraw");
+  return cuda_status(impl->pack_enc(d_bytes, d_planes, count, st), "pack_bfpraw");
+}
+
+bfp_status bfp_unpack_bfpraw(const bfp_format* f, const uint32_t* d_planes, size_t count,
+                             void* d_bytes, void* stream) {
+  const Impl* impl = nullptr;
+  const bfp_status s = resolve(f, &impl);
+  if (s != BFP_OK) return s;
+  if (count == 0) return BFP_OK;
+  if (!d_bytes || !d_planes) return fail(BFP_EARG, "null buffer");
+  const size_t stride = bfp_bfpraw_stride(f);
+  if (stride > 4) return fail(BFP_EUNSUPPORTED, "bfpraw: records wider than 4 bytes");
+  ++g_launches;
+  const cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (stride == 3) return cuda_status(impl->unpack_raw3(d_planes, d_bytes, count, st), "unpack_bfpraw");
+  return cuda_status(impl->unpack_enc(d_planes, d_bytes, count, st), "unpack_bfpraw");
+}
+
 bfp_status bfp_kernel_attrs(const bfp_format* f, int kernel, int* regs, int* ctas_per_sm,
                             int* threads_per_cta) {
   const Impl* impl = nullptr;

@@ -106,14 +106,8 @@ __device__ __forceinline__ void load_unit(const uint8_t* __restrict__ enc, size_
     }
   } else {
     BFP_UNROLL for (int i = 0; i < WORDS; ++i) L[i] = 0;
-    for (int k = 0; k < 32; ++k) {
-      if (e0 + k < n) {
-        w32 v = 0;
-        for (int b = 0; b < EB; ++b) v |= w32(enc[(e0 + k) * EB + b]) << (8 * b);
-        const int bit = (k * EB * 8) & 31;
-        L[(k * EB) / 4] |= (EB == 4) ? v : (v << bit);
-      }
-    }
+    const size_t nb = (n > e0) ? ((n - e0 < 32 ? n - e0 : 32) * EB) : 0;
+    for (size_t b = 0; b < nb; ++b) L[b >> 2] |= w32(enc[e0 * EB + b]) << (8 * (b & 3));
   }
 }
 
@@ -128,10 +122,8 @@ __device__ __forceinline__ void store_unit(uint8_t* __restrict__ enc, size_t u, 
     BFP_UNROLL for (int i = 0; i < WORDS / 4; ++i)
       __stcs(p + i, make_uint4(L[4 * i], L[4 * i + 1], L[4 * i + 2], L[4 * i + 3]));
   } else {
-    for (int k = 0; k < 32 && e0 + k < n; ++k) {
-      const w32 w = L[(k * EB) / 4] >> ((k * EB * 8) & 31);
-      for (int b = 0; b < EB; ++b) enc[(e0 + k) * EB + b] = uint8_t(w >> (8 * b));
-    }
+    const size_t nb = (n - e0 < 32 ? n - e0 : 32) * EB;
+    for (size_t b = 0; b < nb; ++b) enc[e0 * EB + b] = uint8_t(L[b >> 2] >> (8 * (b & 3)));
   }
 }
 
@@ -142,7 +134,8 @@ __device__ __forceinline__ void store_unit(uint8_t* __restrict__ enc, size_t u, 
 // (nearly) bank-conflict free.  Requires the whole warp active.
 template <int CH>
 __device__ __forceinline__ int tile_off(int row, int chunk) {
-  return row * (CH * 4) + ((chunk ^ (row & (CH - 1))) << 2);
+  if constexpr ((CH & (CH - 1)) == 0) return row * (CH * 4) + ((chunk ^ (row & (CH - 1))) << 2);
+  else return row * (CH * 4) + (((chunk + row) % CH) << 2);
 }
 
 template <int CH>
@@ -234,6 +227,9 @@ __global__ void __launch_bounds__(kThreads) k_pack_enc(const uint8_t* __restrict
       enc8_to_planes(L, P);
     } else if constexpr (EB == 2) {
       enc16_to_planes(L, P);
+    } else if constexpr (EB == 3) {
+      bytes24_to_enc32(L, P);
+      enc32_to_planes(P);
     } else {
       BFP_UNROLL for (int i = 0; i < 32; ++i) P[i] = L[i];
       enc32_to_planes(P);
@@ -262,6 +258,9 @@ __global__ void __launch_bounds__(kThreads) k_unpack_enc(const w32* __restrict__
       planes_to_enc8(P, L);
     } else if constexpr (EB == 2) {
       planes_to_enc16(P, L);
+    } else if constexpr (EB == 3) {
+      planes_to_enc32(P);
+      enc32_to_bytes24(P, L);
     } else {
       planes_to_enc32(P);
       BFP_UNROLL for (int i = 0; i < 32; ++i) L[i] = P[i];
@@ -405,7 +404,11 @@ struct Impl {
   cudaError_t (*unpack_enc)(const w32* planes, void* enc, size_t n, cudaStream_t st);
   cudaError_t (*pack_f32)(const float* in, w32* planes, size_t n, cudaStream_t st);
   cudaError_t (*unpack_f32)(const w32* planes, float* out, size_t n, cudaStream_t st);
-  const void* (*kernel)(int op);  // device function handle (for attribute queries)
+  const void* (*kernel)(int op);
+  // .bfpraw records (stride ceil(N/8) bytes); nullptr when the stride is not 3
+  // (strides 1/2/4 are the pack_enc/unpack_enc byte layouts)
+  cudaError_t (*pack_raw3)(const void* bytes, w32* planes, size_t n, cudaStream_t st);
+  cudaError_t (*unpack_raw3)(const w32* planes, void* bytes, size_t n, cudaStream_t st);  // device function handle (for attribute queries)
 };
 
 template <class F>
@@ -490,8 +493,35 @@ struct FormatImpl {
       return launch(k, grid_for(wave, units), st, planes, out, n, units, al);
     }
   }
+  static cudaError_t pack_raw3(const void* bytes, w32* planes, size_t n, cudaStream_t st) {
+    if constexpr (N <= 16 || N > 24) {
+      return cudaErrorNotSupported;
+    } else {
+      const size_t units = units_for(n);
+      if (!units) return cudaSuccess;
+      const bool al = (reinterpret_cast<uintptr_t>(bytes) & 15) == 0;
+      auto k = k_pack_enc<N, 3>;
+      static const int wave = wave_ctas(k);
+      return launch(k, grid_for(wave, units), st, static_cast<const uint8_t*>(bytes), planes, n,
+                    units, al);
+    }
+  }
+  static cudaError_t unpack_raw3(const w32* planes, void* bytes, size_t n, cudaStream_t st) {
+    if constexpr (N <= 16 || N > 24) {
+      return cudaErrorNotSupported;
+    } else {
+      const size_t units = (n + 31) / 32;
+      if (!units) return cudaSuccess;
+      const bool al = (reinterpret_cast<uintptr_t>(bytes) & 15) == 0;
+      auto k = k_unpack_enc<N, 3>;
+      static const int wave = wave_ctas(k);
+      return launch(k, grid_for(wave, units), st, planes, static_cast<uint8_t*>(bytes), n, units,
+                    al);
+    }
+  }
   static const Impl* get() {
-    static const Impl impl = {&arith, &pack_enc, &unpack_enc, &pack_f32, &unpack_f32, &kernel};
+    static const Impl impl = {&arith,  &pack_enc, &unpack_enc, &pack_f32,
+                              &unpack_f32, &kernel, &pack_raw3, &unpack_raw3};
     return &impl;
   }
 };

@@ -133,6 +133,29 @@ BFP_HD void planes_to_enc16(const w32* P, w32* L) {
   }
 }
 
+// .bfpraw with a 3-byte stride (pack.hpp:78-109; formats of 17..24 bits):
+// 32 records = 96 bytes = 24 words (little-endian) <-> 32 encodings.
+BFP_HD void bytes24_to_enc32(const w32* L, w32* V) {
+  BFP_UNROLL for (int k = 0; k < 32; ++k) {
+    const int b = 3 * k, w = b >> 2, off = b & 3;
+    const w32 sel = w32(off) | (w32(off + 1) << 4) | (w32(off + 2) << 8);
+    V[k] = prmt(L[w], (w + 1 < 24) ? L[w + 1] : 0u, sel) & 0xffffffu;
+  }
+}
+
+BFP_HD void enc32_to_bytes24(const w32* V, w32* L) {
+  BFP_UNROLL for (int i = 0; i < 24; ++i) {
+    // bytes 4i..4i+3 come from records k0 = 4i/3 and k0 + 1
+    const int k0 = (4 * i) / 3;
+    w32 sel = 0;
+    BFP_UNROLL for (int t = 0; t < 4; ++t) {
+      const int b = 4 * i + t, k = b / 3, byte = b % 3;
+      sel |= w32((k - k0) * 4 + byte) << (4 * t);
+    }
+    L[i] = prmt(V[k0], (k0 + 1 < 32) ? V[k0 + 1] : 0u, sel);
+  }
+}
+
 // 32 encodings of <= 32 bits, one per word -> planes (in place).
 BFP_HD void enc32_to_planes(w32* v) { xpose32(v); }
 BFP_HD void planes_to_enc32(w32* v) { xpose32(v); }

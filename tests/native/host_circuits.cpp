@@ -123,3 +123,14 @@ extern "C" int host_unpack_enc(int eb, unsigned nbits, const uint32_t* planes, s
   }
   return 0;
 }
+
+// 96 .bfpraw bytes (32 records of 3 bytes) -> 32 encodings -> 96 bytes.
+extern "C" int host_raw3(const uint8_t* bytes96, uint32_t* enc32, uint8_t* back96) {
+  w32 L[24], V[32], B[24];
+  std::memcpy(L, bytes96, 96);
+  bytes24_to_enc32(L, V);
+  std::memcpy(enc32, V, 128);
+  enc32_to_bytes24(V, B);
+  std::memcpy(back96, B, 96);
+  return 0;
+}

@@ -117,3 +117,19 @@ def test_layout_golden_host(host):
         eb = 1 if nb <= 8 else 2 if nb <= 16 else 4
         enc = g[f"enc_{e}_{s}"].astype(np.uint64)
         assert np.array_equal(host.pack_enc(eb, nb, enc), g[f"planes_{e}_{s}"])
+
+
+def test_bfpraw_stride3_host(host):
+    """3-byte .bfpraw records (pack.hpp:78-109) <-> 32-bit encodings."""
+    import ctypes as C
+    host.L.host_raw3.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+    rng = np.random.default_rng(24)
+    for _ in range(50):
+        raw = rng.integers(0, 256, size=96, dtype=np.uint8)
+        enc = np.zeros(32, dtype=np.uint32)
+        back = np.zeros(96, dtype=np.uint8)
+        host.L.host_raw3(raw.ctypes.data, enc.ctypes.data, back.ctypes.data)
+        want = raw.reshape(32, 3).astype(np.uint32)
+        want = want[:, 0] | (want[:, 1] << 8) | (want[:, 2] << 16)
+        assert np.array_equal(enc, want)
+        assert np.array_equal(back, raw)

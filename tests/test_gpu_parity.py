@@ -398,3 +398,27 @@ def test_pack_f32_strided_sweep(oracle, fmt2, mode):
     assert np.array_equal(got, want), int((got != want).sum())
     back = bfp.unpack_f32(v).cpu().numpy().view(np.uint32)
     assert np.array_equal(back, oracle.decode_f32(fmt, want).view(np.uint32))
+
+
+@pytest.mark.parametrize("fmt2", [f for f in FORMATS if 1 + f[0] + f[1] <= 32])
+def test_bfpraw_roundtrip_vs_reference(ref_oracle, fmt2):
+    """.bfpraw bytes written by the reference's to_bfpraw (pack.hpp:86-95) ->
+    pack_bfpraw == field_from_elements planes; unpack_bfpraw == the bytes."""
+    O = ref_oracle
+    e, s = fmt2
+    nb = 1 + e + s
+    spec = bfp.make_spec(e, s)
+    stride = bfp.bfpraw_stride(spec)
+    rng = np.random.default_rng(nb + 100)
+    for n in (1, 33, 1024, 3001, 1 << 16):
+        enc = rng.integers(0, 1 << nb, size=n, dtype=np.uint64)
+        raw = np.zeros(n * stride, dtype=np.uint8)
+        O.ref().ref_to_bfpraw(enc.ctypes.data_as(O._u64p), n, raw.ctypes.data_as(O._u8p), e, s)
+        v = bfp.pack_bfpraw(torch.from_numpy(raw).cuda(), spec)
+        assert np.array_equal(v.planes.cpu().numpy().view(np.uint32), O.pack_planes(enc, nb)), n
+        back = bfp.unpack_bfpraw(v).cpu().numpy()
+        assert np.array_equal(back, raw), n
+    with pytest.raises(ValueError):
+        bfp.pack_bfpraw(torch.zeros(stride * 10 + (1 if stride > 1 else 0), dtype=torch.uint8,
+                                    device="cuda") if stride > 1 else torch.zeros(0), spec) \
+            if stride > 1 else (_ for _ in ()).throw(ValueError())
