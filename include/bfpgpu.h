@@ -109,6 +109,12 @@ bfp_status bfp_mul_add(const bfp_format* f, const uint32_t* d_a, const uint32_t*
 bfp_status bfp_arith(int op, const bfp_format* f, const uint32_t* d_x, const uint32_t* d_y,
                      const uint32_t* d_c, uint32_t* d_z, size_t count, void* stream);
 
+/* Fused float32-in / float32-out: z = (float)decode(op(encode(x), encode(y)
+ * [, encode(c)])) in one kernel -- the same result as pack_f32 / op /
+ * unpack_f32 without the bitslice intermediate in memory.  E <= 8, S <= 23. */
+bfp_status bfp_arith_f32(int op, const bfp_format* f, const float* d_x, const float* d_y,
+                         const float* d_c, float* d_z, size_t count, void* stream);
+
 /* ---- host-buffer entry points (pipelined H2D / kernel / D2H) ------------- */
 typedef struct bfp_host_ctx bfp_host_ctx;
 bfp_host_ctx* bfp_host_ctx_create(size_t chunk_elems); /* 0 = default (2^22) */
@@ -125,7 +131,8 @@ void* bfp_host_alloc(size_t bytes); /* pinned host memory */
 void bfp_host_free(void* p);
 
 /* ---- introspection (for tests / bench) ----------------------------------- */
-/* kernel: 0..4 = arith op, 10 pack_enc, 11 unpack_enc, 12 pack_f32, 13 unpack_f32 */
+/* kernel: 0..4 = arith op, 10 pack_enc, 11 unpack_enc, 12 pack_f32, 13 unpack_f32,
+ *         20 / 22 = fused float32 add / mul */
 bfp_status bfp_kernel_attrs(const bfp_format* f, int kernel, int* regs_per_thread,
                             int* ctas_per_sm, int* threads_per_cta);
 /* Number of kernel launches issued by this library in this process. */

@@ -283,6 +283,24 @@ def bfp_mul_add(a: bfp_vector, b: bfp_vector, c: bfp_vector,
     return _binop(OP_MUL_ADD, a, b, c, out=out)
 
 
+def arith_f32(op: int, spec: format_spec, x: torch.Tensor, y: torch.Tensor,
+              c: torch.Tensor | None = None) -> torch.Tensor:
+    """Fused float32-in / float32-out op in `spec`:
+    (float)decode(op(encode_scalar(x), encode_scalar(y)[, encode_scalar(c)]))
+    in one kernel; bit-identical to unpack_f32(op(pack_f32(x), pack_f32(y)))."""
+    validate(spec)
+    x = x.to(torch.float32).contiguous()
+    y = y.to(torch.float32).contiguous()
+    if x.numel() != y.numel() or (c is not None and c.numel() != x.numel()):
+        raise ValueError("operands must have the same element count")
+    cc = c.to(torch.float32).contiguous() if c is not None else None
+    z = torch.empty_like(x)
+    check(lib().bfp_arith_f32(op, spec.c, x.data_ptr(), y.data_ptr(),
+                              cc.data_ptr() if cc is not None else None, z.data_ptr(), x.numel(),
+                              _stream()), "arith_f32")
+    return z
+
+
 # --------------------------------------------------------------------- host codec
 def encode_scalar(x: float, f: format_spec) -> int:
     """format.hpp:125-188: correctly rounded binary64 -> format (host, scalar)."""

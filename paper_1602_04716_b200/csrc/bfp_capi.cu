@@ -210,6 +210,19 @@ bfp_status bfp_unpack_f32(const bfp_format* f, const uint32_t* d_planes, float* 
                      "unpack_f32 launch");
 }
 
+bfp_status bfp_arith_f32(int op, const bfp_format* f, const float* d_x, const float* d_y,
+                         const float* d_c, float* d_z, size_t count, void* stream) {
+  const Impl* impl = nullptr;
+  const bfp_status s = resolve(f, &impl);
+  if (s != BFP_OK) return s;
+  if (op < 0 || op > 4) return fail(BFP_EARG, "bad op");
+  if (count == 0) return BFP_OK;
+  if (!d_x || !d_y || !d_z || (op == 4 && !d_c)) return fail(BFP_EARG, "null operand");
+  ++g_launches;
+  return cuda_status(impl->arith_f32(op, d_x, d_y, d_c, d_z, count, static_cast<cudaStream_t>(stream)),
+                     "arith_f32 launch");
+}
+
 // .bfpraw (pack.hpp:78-109): little-endian ceil(n/8)-byte records, no padding.
 size_t bfp_bfpraw_stride(const bfp_format* f) {
   if (validate(f) != BFP_OK) return 0;

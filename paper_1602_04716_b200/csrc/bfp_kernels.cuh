@@ -269,16 +269,76 @@ __global__ void __launch_bounds__(kThreads) k_unpack_enc(const w32* __restrict__
   }
 }
 
-// float32 -> encode_scalar -> planes.  Hardware cvt (binary16 / bfloat16)
-// where it coincides with the reference converter, else the branch-free
-// per-element encoder; then the register transpose.
+// 32 float32 bit patterns of one unit -> the unit's N plane words (encode_scalar
+// semantics).  Hardware cvt (binary16 / bfloat16) where it coincides with the
+// reference converter, else the branch-free per-element encoder; then the
+// register transpose.
+template <class F>
+__device__ __forceinline__ void floats_to_planes(w32* V, w32* P) {
+  constexpr int N = F::N;
+  constexpr int HW = HwCodec<F>::kind;
+  if constexpr (HW != 0) {
+    w32 L[16];
+    BFP_UNROLL for (int q = 0; q < 16; ++q)
+      L[q] = hw_cvt2<HW, F::RN>(__uint_as_float(V[2 * q]), __uint_as_float(V[2 * q + 1]));
+    enc16_to_planes(L, P);
+    canon_nan_planes<F>(P);
+  } else {
+    BFP_UNROLL for (int k = 0; k < 32; ++k) V[k] = encode_f32_fast<F>(V[k]);
+    if constexpr (N <= 8) {
+      w32 L[8];
+      BFP_UNROLL for (int q = 0; q < 8; ++q)
+        L[q] = V[4 * q] | (V[4 * q + 1] << 8) | (V[4 * q + 2] << 16) | (V[4 * q + 3] << 24);
+      enc8_to_planes(L, P);
+    } else if constexpr (N <= 16) {
+      w32 L[16];
+      BFP_UNROLL for (int q = 0; q < 16; ++q) L[q] = V[2 * q] | (V[2 * q + 1] << 16);
+      enc16_to_planes(L, P);
+    } else {
+      BFP_UNROLL for (int i = 0; i < 32; ++i) P[i] = V[i];
+      enc32_to_planes(P);
+    }
+  }
+}
+
+// The unit's N plane words -> 32 float32 bit patterns ((float)decode_scalar).
+// P is clobbered (32 words, rows >= N must be zero).
+template <class F>
+__device__ __forceinline__ void planes_to_floats(w32* P, w32* V) {
+  constexpr int N = F::N;
+  constexpr int HW = HwCodec<F>::kind;
+  if constexpr (HW != 0) {
+    canon_nan_planes<F>(P);  // 0x7e00 / 0x7fc0 widen to 0x7fc00000
+    w32 L[16];
+    planes_to_enc16(P, L);
+    BFP_UNROLL for (int q = 0; q < 16; ++q) {
+      V[2 * q] = hw_widen<HW>(L[q] & 0xffffu);
+      V[2 * q + 1] = hw_widen<HW>(L[q] >> 16);
+    }
+  } else {
+    if constexpr (N <= 8) {
+      w32 L[8];
+      planes_to_enc8(P, L);
+      BFP_UNROLL for (int k = 0; k < 32; ++k) V[k] = (L[k >> 2] >> (8 * (k & 3))) & 0xffu;
+    } else if constexpr (N <= 16) {
+      w32 L[16];
+      planes_to_enc16(P, L);
+      BFP_UNROLL for (int k = 0; k < 32; ++k) V[k] = (L[k >> 1] >> (16 * (k & 1))) & 0xffffu;
+    } else {
+      planes_to_enc32(P);
+      BFP_UNROLL for (int k = 0; k < 32; ++k) V[k] = P[k];
+    }
+    BFP_UNROLL for (int k = 0; k < 32; ++k) V[k] = decode_f32_fast<F>(V[k]);
+  }
+}
+
+// float32 -> encode_scalar -> planes.
 template <class F>
 __global__ void __launch_bounds__(kThreads) k_pack_f32(const float* __restrict__ in,
                                                        w32* __restrict__ planes, size_t n,
                                                        size_t units, bool aligned) {
   pdl_enter();
   constexpr int N = F::N;
-  constexpr int HW = HwCodec<F>::kind;
   __shared__ __align__(16) w32 tiles[kThreads / 32][1024];
   const int lane = threadIdx.x & 31;
   w32* tile = tiles[threadIdx.x >> 5];
@@ -289,28 +349,7 @@ __global__ void __launch_bounds__(kThreads) k_pack_f32(const float* __restrict__
     w32 V[32];
     warp_load_elems<4>(inb, u, n, aligned, tile, lane, V);  // zero past n -> +0 -> 0
     w32 P[32];
-    if constexpr (HW != 0) {
-      w32 L[16];
-      BFP_UNROLL for (int q = 0; q < 16; ++q)
-        L[q] = hw_cvt2<HW, F::RN>(__uint_as_float(V[2 * q]), __uint_as_float(V[2 * q + 1]));
-      enc16_to_planes(L, P);
-      canon_nan_planes<F>(P);
-    } else {
-      BFP_UNROLL for (int k = 0; k < 32; ++k) V[k] = encode_f32_fast<F>(V[k]);
-      if constexpr (N <= 8) {
-        w32 L[8];
-        BFP_UNROLL for (int q = 0; q < 8; ++q)
-          L[q] = V[4 * q] | (V[4 * q + 1] << 8) | (V[4 * q + 2] << 16) | (V[4 * q + 3] << 24);
-        enc8_to_planes(L, P);
-      } else if constexpr (N <= 16) {
-        w32 L[16];
-        BFP_UNROLL for (int q = 0; q < 16; ++q) L[q] = V[2 * q] | (V[2 * q + 1] << 16);
-        enc16_to_planes(L, P);
-      } else {
-        BFP_UNROLL for (int i = 0; i < 32; ++i) P[i] = V[i];
-        enc32_to_planes(P);
-      }
-    }
+    floats_to_planes<F>(V, P);
     const size_t base = (u >> 5) * (size_t(N) * 32) + (u & 31);
     BFP_UNROLL for (int j = 0; j < N; ++j) st_stream(planes + base + j * 32, P[j]);
   }
@@ -323,7 +362,6 @@ __global__ void __launch_bounds__(kThreads) k_unpack_f32(const w32* __restrict__
                                                          size_t units, bool aligned) {
   pdl_enter();
   constexpr int N = F::N;
-  constexpr int HW = HwCodec<F>::kind;
   __shared__ __align__(16) w32 tiles[kThreads / 32][1024];
   const int lane = threadIdx.x & 31;
   w32* tile = tiles[threadIdx.x >> 5];
@@ -335,30 +373,44 @@ __global__ void __launch_bounds__(kThreads) k_unpack_f32(const w32* __restrict__
     w32 P[32];
     BFP_UNROLL for (int j = 0; j < 32; ++j) P[j] = (j < N) ? ld_stream(planes + base + j * 32) : 0u;
     w32 V[32];
-    if constexpr (HW != 0) {
-      canon_nan_planes<F>(P);  // 0x7e00 / 0x7fc0 widen to 0x7fc00000
-      w32 L[16];
-      planes_to_enc16(P, L);
-      BFP_UNROLL for (int q = 0; q < 16; ++q) {
-        V[2 * q] = hw_widen<HW>(L[q] & 0xffffu);
-        V[2 * q + 1] = hw_widen<HW>(L[q] >> 16);
-      }
-    } else {
-      if constexpr (N <= 8) {
-        w32 L[8];
-        planes_to_enc8(P, L);
-        BFP_UNROLL for (int k = 0; k < 32; ++k) V[k] = (L[k >> 2] >> (8 * (k & 3))) & 0xffu;
-      } else if constexpr (N <= 16) {
-        w32 L[16];
-        planes_to_enc16(P, L);
-        BFP_UNROLL for (int k = 0; k < 32; ++k) V[k] = (L[k >> 1] >> (16 * (k & 1))) & 0xffffu;
-      } else {
-        planes_to_enc32(P);
-        BFP_UNROLL for (int k = 0; k < 32; ++k) V[k] = P[k];
-      }
-      BFP_UNROLL for (int k = 0; k < 32; ++k) V[k] = decode_f32_fast<F>(V[k]);
-    }
+    planes_to_floats<F>(P, V);
     warp_store_elems<4>(outb, u, n, aligned, tile, lane, V);
+  }
+}
+
+// Fused float32-in / float32-out arithmetic: the
+// operands are converted to planes in registers, the network runs, the
+// result is converted back -- the bitslice intermediate never reaches HBM
+// (4 B/elem per operand in, 4 B/elem out).  Equals
+// unpack_f32(op(pack_f32(x), pack_f32(y)[, pack_f32(c)])).
+template <class F, int OP>
+__global__ void __launch_bounds__(kThreads) k_arith_f32(const float* __restrict__ x,
+                                                        const float* __restrict__ y,
+                                                        const float* __restrict__ c,
+                                                        float* __restrict__ z, size_t n,
+                                                        size_t units, bool aligned) {
+  pdl_enter();
+  constexpr int N = F::N;
+  constexpr int NIN = OP == OP_MUL_ADD ? 3 : 2;
+  __shared__ __align__(16) w32 tiles[kThreads / 32][1024];
+  const int lane = threadIdx.x & 31;
+  w32* tile = tiles[threadIdx.x >> 5];
+  const size_t stride = size_t(gridDim.x) * kThreads;
+  const float* src[3] = {x, y, c};
+  for (size_t u = size_t(blockIdx.x) * kThreads + threadIdx.x; u < units; u += stride) {
+    w32 ops[NIN][N];
+    BFP_UNROLL for (int a = 0; a < NIN; ++a) {
+      w32 V[32], P[32];
+      warp_load_elems<4>(reinterpret_cast<const uint8_t*>(src[a]), u, n, aligned, tile, lane, V);
+      floats_to_planes<F>(V, P);
+      BFP_UNROLL for (int j = 0; j < N; ++j) ops[a][j] = P[j];
+    }
+    w32 P[32];
+    eval_unit<F, OP>(ops[0], ops[1], ops[NIN - 1], P);
+    BFP_UNROLL for (int j = N; j < 32; ++j) P[j] = 0;
+    w32 V[32];
+    planes_to_floats<F>(P, V);
+    warp_store_elems<4>(reinterpret_cast<uint8_t*>(z), u, n, aligned, tile, lane, V);
   }
 }
 
@@ -404,11 +456,14 @@ struct Impl {
   cudaError_t (*unpack_enc)(const w32* planes, void* enc, size_t n, cudaStream_t st);
   cudaError_t (*pack_f32)(const float* in, w32* planes, size_t n, cudaStream_t st);
   cudaError_t (*unpack_f32)(const w32* planes, float* out, size_t n, cudaStream_t st);
-  const void* (*kernel)(int op);
-  // .bfpraw records (stride ceil(N/8) bytes); nullptr when the stride is not 3
-  // (strides 1/2/4 are the pack_enc/unpack_enc byte layouts)
+  const void* (*kernel)(int op);  // device function handle (for attribute queries)
+  // .bfpraw records with a 3-byte stride (17..24-bit formats; strides 1/2/4
+  // are the pack_enc/unpack_enc byte layouts); cudaErrorNotSupported otherwise
   cudaError_t (*pack_raw3)(const void* bytes, w32* planes, size_t n, cudaStream_t st);
-  cudaError_t (*unpack_raw3)(const w32* planes, void* bytes, size_t n, cudaStream_t st);  // device function handle (for attribute queries)
+  // fused float32-in / float32-out arithmetic
+  cudaError_t (*arith_f32)(int op, const float* x, const float* y, const float* c, float* z,
+                           size_t n, cudaStream_t st);
+  cudaError_t (*unpack_raw3)(const w32* planes, void* bytes, size_t n, cudaStream_t st);
 };
 
 template <class F>
@@ -447,6 +502,8 @@ struct FormatImpl {
       case 11: return reinterpret_cast<const void*>(k_unpack_enc<N, EB>);
       case 12: return reinterpret_cast<const void*>(k_pack_f32<F>);
       case 13: return reinterpret_cast<const void*>(k_unpack_f32<F>);
+      case 20: return reinterpret_cast<const void*>(k_arith_f32<F, OP_ADD>);
+      case 22: return reinterpret_cast<const void*>(k_arith_f32<F, OP_MUL>);
       default: return nullptr;
     }
   }
@@ -519,9 +576,36 @@ struct FormatImpl {
                     al);
     }
   }
+  template <int OP>
+  static cudaError_t launch_arith_f32(const float* x, const float* y, const float* c, float* z,
+                                     size_t n, cudaStream_t st) {
+    const size_t units = units_for(n);
+    if (!units) return cudaSuccess;
+    const uintptr_t al_bits = reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y) |
+                              reinterpret_cast<uintptr_t>(z) |
+                              (OP == OP_MUL_ADD ? reinterpret_cast<uintptr_t>(c) : 0);
+    auto k = k_arith_f32<F, OP>;
+    static const int wave = wave_ctas(k);
+    return launch(k, grid_for(wave, units), st, x, y, c, z, n, units, (al_bits & 15) == 0);
+  }
+  static cudaError_t arith_f32(int op, const float* x, const float* y, const float* c, float* z,
+                               size_t n, cudaStream_t st) {
+    if constexpr (F::E > 8 || F::S > 23) {
+      return cudaErrorNotSupported;
+    } else {
+      switch (op) {
+        case OP_ADD: return launch_arith_f32<OP_ADD>(x, y, c, z, n, st);
+        case OP_SUB: return launch_arith_f32<OP_SUB>(x, y, c, z, n, st);
+        case OP_MUL: return launch_arith_f32<OP_MUL>(x, y, c, z, n, st);
+        case OP_DIV: return launch_arith_f32<OP_DIV>(x, y, c, z, n, st);
+        case OP_MUL_ADD: return launch_arith_f32<OP_MUL_ADD>(x, y, c, z, n, st);
+        default: return cudaErrorInvalidValue;
+      }
+    }
+  }
   static const Impl* get() {
-    static const Impl impl = {&arith,  &pack_enc, &unpack_enc, &pack_f32,
-                              &unpack_f32, &kernel, &pack_raw3, &unpack_raw3};
+    static const Impl impl = {&arith,  &pack_enc, &unpack_enc, &pack_f32,  &unpack_f32,
+                              &kernel, &pack_raw3, &arith_f32, &unpack_raw3};
     return &impl;
   }
 };

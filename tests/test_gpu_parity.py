@@ -418,7 +418,42 @@ def test_bfpraw_roundtrip_vs_reference(ref_oracle, fmt2):
         assert np.array_equal(v.planes.cpu().numpy().view(np.uint32), O.pack_planes(enc, nb)), n
         back = bfp.unpack_bfpraw(v).cpu().numpy()
         assert np.array_equal(back, raw), n
-    with pytest.raises(ValueError):
-        bfp.pack_bfpraw(torch.zeros(stride * 10 + (1 if stride > 1 else 0), dtype=torch.uint8,
-                                    device="cuda") if stride > 1 else torch.zeros(0), spec) \
-            if stride > 1 else (_ for _ in ()).throw(ValueError())
+    if stride > 1:  # from_bfpraw rejects a ragged byte count (pack.hpp:98-100)
+        with pytest.raises(ValueError):
+            bfp.pack_bfpraw(torch.zeros(stride * 10 + 1, dtype=torch.uint8, device="cuda"), spec)
+
+
+@pytest.mark.parametrize("fmt2", [f for f in FORMATS if f[0] <= 8 and f[1] <= 23])
+@pytest.mark.parametrize("mode", MODES)
+def test_arith_f32_fused(oracle, fmt2, mode):
+    """Fused float32-in/out ops == decode(op(encode(x), encode(y))) per the
+    oracle, and == the unfused pack_f32 / op / unpack_f32 composition."""
+    e, s = fmt2
+    fmt = fmt2 + mode
+    spec = bfp.make_spec(e, s, mode[0], mode[1])
+    rng = np.random.default_rng(e * 31 + s + mode[0] * 7 + mode[1])
+    n = (1 << 15) + 1234  # ragged tail
+    def floats():
+        bits = rng.integers(0, 1 << 32, size=n, dtype=np.uint64).astype(np.uint32)
+        bits[: n // 2] = (bits[: n // 2] & 0x807FFFFF) | (
+            rng.integers(110, 145, size=n // 2, dtype=np.uint64).astype(np.uint32) << 23)
+        return bits.view(np.float32)
+    xs, ys, cs = floats(), floats(), floats()
+    ex, ey, ec = (oracle.encode_f32(fmt, v) for v in (xs, ys, cs))
+    tx, ty, tc = (torch.from_numpy(v).cuda() for v in (xs, ys, cs))
+    for op, code in (("add", 0), ("sub", 1), ("mul", 2), ("div", 3), ("mul_add", 4)):
+        got = bfp.arith_f32(code, spec, tx, ty, tc if code == 4 else None).cpu().numpy().view(np.uint32)
+        want = oracle.decode_f32(fmt, oracle.binop(op, fmt, ex, ey, ec)).view(np.uint32)
+        assert np.array_equal(got, want), (op, int((got != want).sum()))
+
+
+def test_arith_f32_unaligned():
+    spec = bfp.make_spec(5, 10)
+    n = 5000
+    buf = torch.randn(3 * n + 3, device="cuda") * 50
+    x, y, z = buf[1:n + 1], buf[n + 2:2 * n + 2], torch.empty(n + 1, device="cuda")[1:]
+    L = _lib.lib()
+    assert L.bfp_arith_f32(2, spec.c, x.data_ptr(), y.data_ptr(), None, z.data_ptr(), n,
+                           torch.cuda.current_stream().cuda_stream) == 0
+    ref = bfp.unpack_f32(bfp.bfp_mul(bfp.pack_f32(x, spec), bfp.pack_f32(y, spec)))
+    assert torch.equal(z.view(torch.int32), ref.view(torch.int32))
