@@ -67,7 +67,13 @@ const char* bfp_status_string(bfp_status s);
 const char* bfp_last_error(void); /* thread-local text of the last failure */
 bfp_status bfp_validate(const bfp_format* f);
 bfp_status bfp_same_shape(const bfp_format* a, const bfp_format* b);
-int bfp_is_supported(const bfp_format* f); /* 1 when a compiled network exists */
+/* 1 when the format can run: a compiled network (1/3/2, 1/4/3, 1/5/3, 1/5/7,
+ * 1/5/10, 1/6/9, 1/8/7, 1/8/15, 1/8/23 x RN/RZ x gradual/FTZ) or, for every
+ * other legal format, the NVRTC runtime backend (compiled on first use;
+ * disable with BFP_JIT=0).  Layout kernels need n <= 32 bits, float32
+ * conversions e <= 8 and s <= 23 (BFP_EUNSUPPORTED otherwise). */
+int bfp_is_supported(const bfp_format* f);
+int bfp_is_compiled(const bfp_format* f); /* 1 when an ahead-of-time network exists */
 size_t bfp_plane_bytes(const bfp_format* f, size_t count);
 size_t bfp_enc_bytes(const bfp_format* f); /* device encoding width: 1, 2 or 4 */
 

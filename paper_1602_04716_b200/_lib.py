@@ -35,6 +35,7 @@ SIGNATURES = {
     "bfp_validate": (C.c_int, [_F]),
     "bfp_same_shape": (C.c_int, [_F, _F]),
     "bfp_is_supported": (C.c_int, [_F]),
+    "bfp_is_compiled": (C.c_int, [_F]),
     "bfp_plane_bytes": (C.c_size_t, [_F, C.c_size_t]),
     "bfp_enc_bytes": (C.c_size_t, [_F]),
     "bfp_pack_enc": (C.c_int, [_F, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),

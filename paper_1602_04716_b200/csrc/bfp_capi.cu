@@ -16,6 +16,8 @@ namespace bfpg {
 #define DECLARE_IMPL(E_, S_) const Impl* impl_##E_##_##S_(int rn, int ftz);
 BFP_FORMAT_LIST(DECLARE_IMPL)
 #undef DECLARE_IMPL
+const Impl* jit_impl(unsigned e, unsigned s, int rn, int ftz);  // bfp_jit.cu
+bool jit_available();
 }  // namespace bfpg
 
 using bfpg::Impl;
@@ -58,7 +60,7 @@ bfp_status validate(const bfp_format* f) {
   return BFP_OK;
 }
 
-const Impl* lookup(const bfp_format* f) {
+const Impl* lookup_compiled(const bfp_format* f) {
   const int rn = f->rounding == 1, ftz = f->subnormals == 1;
 #define LOOKUP(E_, S_) \
   if (f->exp_bits == E_ && f->sig_bits == S_) return bfpg::impl_##E_##_##S_(rn, ftz);
@@ -67,11 +69,18 @@ const Impl* lookup(const bfp_format* f) {
   return nullptr;
 }
 
+// Compiled network when the format is instantiated, else the NVRTC
+// runtime-format backend (same templates, compiled on first use).
+const Impl* lookup(const bfp_format* f) {
+  if (const Impl* c = lookup_compiled(f)) return c;
+  return bfpg::jit_impl(f->exp_bits, f->sig_bits, f->rounding == 1, f->subnormals == 1);
+}
+
 bfp_status resolve(const bfp_format* f, const Impl** out) {
   const bfp_status s = validate(f);
   if (s != BFP_OK) return s;
   const Impl* impl = lookup(f);
-  if (!impl) return fail(BFP_EUNSUPPORTED, "format has no compiled network");
+  if (!impl) return fail(BFP_EUNSUPPORTED, "format has no compiled network and NVRTC is unavailable");
   *out = impl;
   return BFP_OK;
 }
@@ -113,7 +122,11 @@ bfp_status bfp_same_shape(const bfp_format* a, const bfp_format* b) {
 }
 
 int bfp_is_supported(const bfp_format* f) {
-  return validate(f) == BFP_OK && lookup(f) != nullptr;
+  return validate(f) == BFP_OK && (lookup_compiled(f) != nullptr || bfpg::jit_available());
+}
+
+int bfp_is_compiled(const bfp_format* f) {
+  return validate(f) == BFP_OK && lookup_compiled(f) != nullptr;
 }
 
 size_t bfp_plane_bytes(const bfp_format* f, size_t count) {

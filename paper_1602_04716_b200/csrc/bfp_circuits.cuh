@@ -31,7 +31,14 @@
 // The same header compiles for the host (g++) so the networks can be checked
 // exhaustively without a GPU.
 #pragma once
+#if defined(__CUDACC_RTC__)
+typedef unsigned int uint32_t;
+typedef unsigned long long uint64_t;
+typedef unsigned char uint8_t;
+typedef unsigned long long uintptr_t;
+#else
 #include <stdint.h>
+#endif
 
 #if defined(__CUDACC__)
 #define BFP_HD __host__ __device__ __forceinline__

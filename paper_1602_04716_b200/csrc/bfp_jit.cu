@@ -1,0 +1,286 @@
+// bfp_jit.cu -- runtime-format backend: every legal
+// format_spec (format.hpp:57-64: e in [2,11], s in [1,52], n <= 64) is
+// accepted.  Formats without a compiled network get the SAME templates
+// (bfp_kernels.cuh) compiled on first use by NVRTC for sm_100a, per kernel,
+// cached for the life of the process -- the role of the paper's library
+// generator (exponent/mantissa/rounding in, library out).
+//
+// libnvrtc is dlopen'ed (no link-time dependency); the CUBIN is loaded with
+// cudaLibraryLoadData and launched with cudaLaunchKernelExC (PDL attribute as
+// for the compiled kernels).  Disabled with BFP_JIT=0.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "bfp_kernels.cuh"
+
+namespace bfpg {
+
+namespace {
+
+// ---- NVRTC, resolved at runtime
+typedef int nvrtcResult_t;
+typedef struct _nvrtcProgram* nvrtcProgram_t;
+struct Nvrtc {
+  nvrtcResult_t (*create)(nvrtcProgram_t*, const char*, const char*, int, const char* const*,
+                          const char* const*) = nullptr;
+  nvrtcResult_t (*add_name)(nvrtcProgram_t, const char*) = nullptr;
+  nvrtcResult_t (*compile)(nvrtcProgram_t, int, const char* const*) = nullptr;
+  nvrtcResult_t (*lowered)(nvrtcProgram_t, const char*, const char**) = nullptr;
+  nvrtcResult_t (*cubin_size)(nvrtcProgram_t, size_t*) = nullptr;
+  nvrtcResult_t (*cubin)(nvrtcProgram_t, char*) = nullptr;
+  nvrtcResult_t (*log_size)(nvrtcProgram_t, size_t*) = nullptr;
+  nvrtcResult_t (*log)(nvrtcProgram_t, char*) = nullptr;
+  nvrtcResult_t (*destroy)(nvrtcProgram_t*) = nullptr;
+  bool ok = false;
+};
+
+const Nvrtc& nvrtc() {
+  static Nvrtc n = [] {
+    Nvrtc r;
+    const char* env = std::getenv("BFP_JIT");
+    if (env && env[0] == '0') return r;
+    void* h = nullptr;
+    for (const char* name : {"libnvrtc.so.12", "libnvrtc.so", "/usr/local/cuda/lib64/libnvrtc.so.12"}) {
+      h = dlopen(name, RTLD_NOW | RTLD_LOCAL);
+      if (h) break;
+    }
+    if (!h) return r;
+#define SYM(field, name) r.field = reinterpret_cast<decltype(r.field)>(dlsym(h, name))
+    SYM(create, "nvrtcCreateProgram");
+    SYM(add_name, "nvrtcAddNameExpression");
+    SYM(compile, "nvrtcCompileProgram");
+    SYM(lowered, "nvrtcGetLoweredName");
+    SYM(cubin_size, "nvrtcGetCUBINSize");
+    SYM(cubin, "nvrtcGetCUBIN");
+    SYM(log_size, "nvrtcGetProgramLogSize");
+    SYM(log, "nvrtcGetProgramLog");
+    SYM(destroy, "nvrtcDestroyProgram");
+#undef SYM
+    r.ok = r.create && r.add_name && r.compile && r.lowered && r.cubin_size && r.cubin &&
+           r.log_size && r.log && r.destroy;
+    return r;
+  }();
+  return n;
+}
+
+// csrc/ next to this library: the headers NVRTC compiles.
+std::string csrc_dir() {
+  Dl_info info;
+  if (dladdr(reinterpret_cast<void*>(&csrc_dir), &info) && info.dli_fname) {
+    std::string p(info.dli_fname);
+    const auto slash = p.rfind('/');
+    return (slash == std::string::npos ? std::string(".") : p.substr(0, slash)) + "/csrc";
+  }
+  return "csrc";
+}
+
+struct JitKernel {
+  cudaKernel_t k = nullptr;
+  int wave = 0;
+};
+
+class JitFormat final : public Impl {
+ public:
+  JitFormat(unsigned e, unsigned s, int rn, int ftz) : e_(e), s_(s), rn_(rn), ftz_(ftz) {}
+
+  bool compiled() const override { return false; }
+
+  cudaError_t arith(int op, const w32* x, const w32* y, const w32* c, w32* z, size_t nblocks,
+                    cudaStream_t st) const override {
+    if (op < 0 || op > 4) return cudaErrorInvalidValue;
+    const size_t units = nblocks * 32;
+    if (!units) return cudaSuccess;
+    return run(fmt_expr("bfpg::k_arith<%s, %d>", op), units, st, {&x, &y, &c, &z, &units});
+  }
+  cudaError_t pack_enc(const void* enc, w32* planes, size_t n, cudaStream_t st) const override {
+    const int eb = enc_bytes();
+    if (!eb) return cudaErrorNotSupported;
+    const size_t units = ((n + 1023) / 1024) * 32;
+    if (!units) return cudaSuccess;
+    const bool al = (reinterpret_cast<uintptr_t>(enc) & 15) == 0;
+    const uint8_t* e = static_cast<const uint8_t*>(enc);
+    return run(layout_expr("bfpg::k_pack_enc<%d, %d>", eb), units, st, {&e, &planes, &n, &units, &al});
+  }
+  cudaError_t unpack_enc(const w32* planes, void* enc, size_t n, cudaStream_t st) const override {
+    const int eb = enc_bytes();
+    if (!eb) return cudaErrorNotSupported;
+    const size_t units = (n + 31) / 32;
+    if (!units) return cudaSuccess;
+    const bool al = (reinterpret_cast<uintptr_t>(enc) & 15) == 0;
+    uint8_t* e = static_cast<uint8_t*>(enc);
+    return run(layout_expr("bfpg::k_unpack_enc<%d, %d>", eb), units, st, {&planes, &e, &n, &units, &al});
+  }
+  cudaError_t pack_raw3(const void* bytes, w32* planes, size_t n, cudaStream_t st) const override {
+    if (N() <= 16 || N() > 24) return cudaErrorNotSupported;
+    const size_t units = ((n + 1023) / 1024) * 32;
+    if (!units) return cudaSuccess;
+    const bool al = (reinterpret_cast<uintptr_t>(bytes) & 15) == 0;
+    const uint8_t* b = static_cast<const uint8_t*>(bytes);
+    return run(layout_expr("bfpg::k_pack_enc<%d, %d>", 3), units, st, {&b, &planes, &n, &units, &al});
+  }
+  cudaError_t unpack_raw3(const w32* planes, void* bytes, size_t n, cudaStream_t st) const override {
+    if (N() <= 16 || N() > 24) return cudaErrorNotSupported;
+    const size_t units = (n + 31) / 32;
+    if (!units) return cudaSuccess;
+    const bool al = (reinterpret_cast<uintptr_t>(bytes) & 15) == 0;
+    uint8_t* b = static_cast<uint8_t*>(bytes);
+    return run(layout_expr("bfpg::k_unpack_enc<%d, %d>", 3), units, st, {&planes, &b, &n, &units, &al});
+  }
+  cudaError_t pack_f32(const float* in, w32* planes, size_t n, cudaStream_t st) const override {
+    if (e_ > 8 || s_ > 23) return cudaErrorNotSupported;
+    const size_t units = ((n + 1023) / 1024) * 32;
+    if (!units) return cudaSuccess;
+    const bool al = (reinterpret_cast<uintptr_t>(in) & 15) == 0;
+    return run(fmt_expr("bfpg::k_pack_f32<%s>", -1), units, st, {&in, &planes, &n, &units, &al});
+  }
+  cudaError_t unpack_f32(const w32* planes, float* out, size_t n, cudaStream_t st) const override {
+    if (e_ > 8 || s_ > 23) return cudaErrorNotSupported;
+    const size_t units = (n + 31) / 32;
+    if (!units) return cudaSuccess;
+    const bool al = (reinterpret_cast<uintptr_t>(out) & 15) == 0;
+    return run(fmt_expr("bfpg::k_unpack_f32<%s>", -1), units, st, {&planes, &out, &n, &units, &al});
+  }
+  cudaError_t arith_f32(int op, const float* x, const float* y, const float* c, float* z, size_t n,
+                        cudaStream_t st) const override {
+    if (e_ > 8 || s_ > 23) return cudaErrorNotSupported;
+    if (op < 0 || op > 4) return cudaErrorInvalidValue;
+    const size_t units = ((n + 1023) / 1024) * 32;
+    if (!units) return cudaSuccess;
+    const uintptr_t bits = reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y) |
+                           reinterpret_cast<uintptr_t>(z) |
+                           (op == 4 ? reinterpret_cast<uintptr_t>(c) : 0);
+    const bool al = (bits & 15) == 0;
+    return run(fmt_expr("bfpg::k_arith_f32<%s, %d>", op), units, st,
+               {&x, &y, &c, &z, &n, &units, &al});
+  }
+  const void* kernel(int id) const override {
+    std::string expr;
+    if (id >= 0 && id <= 4) expr = fmt_expr("bfpg::k_arith<%s, %d>", id);
+    else if (id == 12) expr = fmt_expr("bfpg::k_pack_f32<%s>", -1);
+    else if (id == 13) expr = fmt_expr("bfpg::k_unpack_f32<%s>", -1);
+    else return nullptr;
+    JitKernel k;
+    if (get(expr, &k) != cudaSuccess) return nullptr;
+    return reinterpret_cast<const void*>(k.k);
+  }
+
+ private:
+  int N() const { return int(1 + e_ + s_); }
+  int enc_bytes() const { return N() <= 8 ? 1 : N() <= 16 ? 2 : N() <= 32 ? 4 : 0; }
+  std::string fmt_expr(const char* pat, int op) const {
+    char f[96], out[192];
+    std::snprintf(f, sizeof f, "bfpg::Format<%u, %u, %s, %s>", e_, s_, rn_ ? "true" : "false",
+                  ftz_ ? "true" : "false");
+    if (op < 0) std::snprintf(out, sizeof out, pat, f);
+    else std::snprintf(out, sizeof out, pat, f, op);
+    return out;
+  }
+  std::string layout_expr(const char* pat, int eb) const {
+    char out[96];
+    std::snprintf(out, sizeof out, pat, N(), eb);
+    return out;
+  }
+
+  cudaError_t get(const std::string& expr, JitKernel* out) const {
+    std::lock_guard<std::mutex> lock(mu_);
+    auto it = cache_.find(expr);
+    if (it != cache_.end()) {
+      *out = it->second;
+      return cudaSuccess;
+    }
+    const Nvrtc& nv = nvrtc();
+    if (!nv.ok) return cudaErrorNotSupported;
+    const std::string inc = "--include-path=" + csrc_dir();
+    const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", inc.c_str(),
+                          "-default-device", "-lineinfo"};
+    nvrtcProgram_t prog = nullptr;
+    if (nv.create(&prog, "#include \"bfp_kernels.cuh\"\n", "bfp_jit.cu", 0, nullptr, nullptr))
+      return cudaErrorNotSupported;
+    nv.add_name(prog, expr.c_str());
+    if (nv.compile(prog, 5, opts) != 0) {
+      size_t ls = 0;
+      nv.log_size(prog, &ls);
+      std::string log(ls, '\0');
+      nv.log(prog, log.data());
+      std::fprintf(stderr, "[bfp jit] NVRTC failed for %s:\n%s\n", expr.c_str(), log.c_str());
+      nv.destroy(&prog);
+      return cudaErrorNotSupported;
+    }
+    const char* lowered = nullptr;
+    nv.lowered(prog, expr.c_str(), &lowered);
+    const std::string name = lowered ? lowered : "";
+    size_t n = 0;
+    nv.cubin_size(prog, &n);
+    std::vector<char> cubin(n);
+    nv.cubin(prog, cubin.data());
+    nv.destroy(&prog);
+    cudaLibrary_t lib = nullptr;
+    cudaError_t e = cudaLibraryLoadData(&lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
+    if (e != cudaSuccess) return e;
+    JitKernel k;
+    e = cudaLibraryGetKernel(&k.k, lib, name.c_str());
+    if (e != cudaSuccess) return e;
+    int dev = 0, sms = 0, occ = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, reinterpret_cast<const void*>(k.k),
+                                                      kThreads, 0) != cudaSuccess || occ <= 0) {
+      cudaGetLastError();
+      occ = 2;
+    }
+    k.wave = (sms > 0 ? sms : 148) * occ;
+    cache_[expr] = k;
+    *out = k;
+    return cudaSuccess;
+  }
+
+  cudaError_t run(const std::string& expr, size_t units, cudaStream_t st,
+                  std::initializer_list<const void*> args) const {
+    JitKernel k;
+    cudaError_t e = get(expr, &k);
+    if (e != cudaSuccess) return e;
+    std::vector<void*> argv;
+    for (const void* a : args) argv.push_back(const_cast<void*>(a));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid_for(k.wave, units));
+    cfg.blockDim = dim3(kThreads);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(k.k), argv.data());
+  }
+
+  unsigned e_, s_;
+  int rn_, ftz_;
+  mutable std::mutex mu_;
+  mutable std::map<std::string, JitKernel> cache_;
+};
+
+}  // namespace
+
+bool jit_available() { return nvrtc().ok; }
+
+const Impl* jit_impl(unsigned e, unsigned s, int rn, int ftz) {
+  if (!nvrtc().ok) return nullptr;
+  static std::mutex mu;
+  static std::map<unsigned, std::unique_ptr<JitFormat>> formats;
+  const unsigned key = (e << 8) | (s << 2) | (rn ? 2u : 0u) | (ftz ? 1u : 0u);
+  std::lock_guard<std::mutex> lock(mu);
+  auto& slot = formats[key];
+  if (!slot) slot = std::make_unique<JitFormat>(e, s, rn, ftz);
+  return slot.get();
+}
+
+}  // namespace bfpg

@@ -12,7 +12,9 @@
 // (bfp_layout.cuh); the plane side of every access is coalesced, the element
 // side is a 32..128-B contiguous chunk per thread (vector loads).
 #pragma once
+#if !defined(__CUDACC_RTC__)
 #include <cuda_runtime.h>
+#endif
 
 #include "bfp_circuits.cuh"
 #include "bfp_layout.cuh"
@@ -415,6 +417,7 @@ __global__ void __launch_bounds__(kThreads) k_arith_f32(const float* __restrict_
 }
 
 // ------------------------------------------------------- launch + table
+#if !defined(__CUDACC_RTC__)  // host-side launch code (not under NVRTC)
 bool pdl_enabled();  // bfp_capi.cu: BFP_PDL environment switch (default on)
 
 template <typename... KArgs, typename... Args>
@@ -448,22 +451,26 @@ inline int grid_for(int wave, size_t units) {
   return int(need < size_t(wave) ? (need ? need : 1) : size_t(wave));
 }
 
-// Per-format entry points (instantiated in inst/fmt_E_S.cu).
+// Per-format entry points: implemented by the compiled networks
+// (FormatImpl<F>, instantiated in inst/fmt_E_S.cu) and by the NVRTC
+// runtime-format backend (bfp_jit.cu) for every other legal format.
 struct Impl {
-  cudaError_t (*arith)(int op, const w32* x, const w32* y, const w32* c, w32* z, size_t nblocks,
-                       cudaStream_t st);
-  cudaError_t (*pack_enc)(const void* enc, w32* planes, size_t n, cudaStream_t st);
-  cudaError_t (*unpack_enc)(const w32* planes, void* enc, size_t n, cudaStream_t st);
-  cudaError_t (*pack_f32)(const float* in, w32* planes, size_t n, cudaStream_t st);
-  cudaError_t (*unpack_f32)(const w32* planes, float* out, size_t n, cudaStream_t st);
-  const void* (*kernel)(int op);  // device function handle (for attribute queries)
+  virtual ~Impl() = default;
+  virtual cudaError_t arith(int op, const w32* x, const w32* y, const w32* c, w32* z,
+                            size_t nblocks, cudaStream_t st) const = 0;
+  virtual cudaError_t pack_enc(const void* enc, w32* planes, size_t n, cudaStream_t st) const = 0;
+  virtual cudaError_t unpack_enc(const w32* planes, void* enc, size_t n, cudaStream_t st) const = 0;
+  virtual cudaError_t pack_f32(const float* in, w32* planes, size_t n, cudaStream_t st) const = 0;
+  virtual cudaError_t unpack_f32(const w32* planes, float* out, size_t n, cudaStream_t st) const = 0;
   // .bfpraw records with a 3-byte stride (17..24-bit formats; strides 1/2/4
   // are the pack_enc/unpack_enc byte layouts); cudaErrorNotSupported otherwise
-  cudaError_t (*pack_raw3)(const void* bytes, w32* planes, size_t n, cudaStream_t st);
+  virtual cudaError_t pack_raw3(const void* bytes, w32* planes, size_t n, cudaStream_t st) const = 0;
+  virtual cudaError_t unpack_raw3(const w32* planes, void* bytes, size_t n, cudaStream_t st) const = 0;
   // fused float32-in / float32-out arithmetic
-  cudaError_t (*arith_f32)(int op, const float* x, const float* y, const float* c, float* z,
-                           size_t n, cudaStream_t st);
-  cudaError_t (*unpack_raw3)(const w32* planes, void* bytes, size_t n, cudaStream_t st);
+  virtual cudaError_t arith_f32(int op, const float* x, const float* y, const float* c, float* z,
+                                size_t n, cudaStream_t st) const = 0;
+  virtual const void* kernel(int id) const = 0;  // device function handle (attribute queries)
+  virtual bool compiled() const { return true; }
 };
 
 template <class F>
@@ -603,15 +610,46 @@ struct FormatImpl {
       }
     }
   }
+  struct Backend final : Impl {
+    cudaError_t arith(int op, const w32* x, const w32* y, const w32* c, w32* z, size_t nb,
+                      cudaStream_t st) const override {
+      return FormatImpl::arith(op, x, y, c, z, nb, st);
+    }
+    cudaError_t pack_enc(const void* e, w32* p, size_t n, cudaStream_t st) const override {
+      return FormatImpl::pack_enc(e, p, n, st);
+    }
+    cudaError_t unpack_enc(const w32* p, void* e, size_t n, cudaStream_t st) const override {
+      return FormatImpl::unpack_enc(p, e, n, st);
+    }
+    cudaError_t pack_f32(const float* i, w32* p, size_t n, cudaStream_t st) const override {
+      return FormatImpl::pack_f32(i, p, n, st);
+    }
+    cudaError_t unpack_f32(const w32* p, float* o, size_t n, cudaStream_t st) const override {
+      return FormatImpl::unpack_f32(p, o, n, st);
+    }
+    cudaError_t pack_raw3(const void* b, w32* p, size_t n, cudaStream_t st) const override {
+      return FormatImpl::pack_raw3(b, p, n, st);
+    }
+    cudaError_t unpack_raw3(const w32* p, void* b, size_t n, cudaStream_t st) const override {
+      return FormatImpl::unpack_raw3(p, b, n, st);
+    }
+    cudaError_t arith_f32(int op, const float* x, const float* y, const float* c, float* z,
+                          size_t n, cudaStream_t st) const override {
+      return FormatImpl::arith_f32(op, x, y, c, z, n, st);
+    }
+    const void* kernel(int id) const override { return FormatImpl::kernel(id); }
+  };
   static const Impl* get() {
-    static const Impl impl = {&arith,  &pack_enc, &unpack_enc, &pack_f32,  &unpack_f32,
-                              &kernel, &pack_raw3, &arith_f32, &unpack_raw3};
+    static const Backend impl;
     return &impl;
   }
 };
 
+#endif  // !__CUDACC_RTC__
+
 }  // namespace bfpg
 
+#if !defined(__CUDACC_RTC__)
 #define BFP_INSTANTIATE(E_, S_)                                                       \
   namespace bfpg {                                                                    \
   const Impl* impl_##E_##_##S_(int rn, int ftz) {                                     \
@@ -621,3 +659,4 @@ struct FormatImpl {
     return FormatImpl<Format<E_, S_, false, true>>::get();                            \
   }                                                                                   \
   }
+#endif

@@ -19,7 +19,9 @@
 // The codec follows encode_scalar / decode_scalar (format.hpp:101-188) for
 // binary32 inputs / outputs.
 #pragma once
+#if !defined(__CUDACC_RTC__)
 #include <string.h>
+#endif
 
 #include "bfp_circuits.cuh"
 

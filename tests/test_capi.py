@@ -71,7 +71,9 @@ def test_sizes(L):
         for count in (0, 1, 1024, 1025, 5000):
             assert L.bfp_plane_bytes(C.byref(f), count) == ((count + 1023) // 1024) * n * 128
         assert L.bfp_enc_bytes(C.byref(f)) == (1 if n <= 8 else 2 if n <= 16 else 4)
-    assert L.bfp_is_supported(C.byref(fmt(7, 20))) == 0  # legal, not instantiated
+        assert L.bfp_is_compiled(C.byref(f)) == 1
+    assert L.bfp_is_compiled(C.byref(fmt(7, 20))) == 0  # legal, not instantiated: NVRTC backend
+    assert L.bfp_is_supported(C.byref(fmt(7, 20))) == 1
     assert L.bfp_is_supported(C.byref(fmt(12, 3))) == 0  # illegal
 
 

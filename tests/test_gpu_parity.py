@@ -220,8 +220,8 @@ def test_python_api_roundtrip(oracle):
 def test_unsupported_and_errors():
     L = _lib.lib()
     t = torch.zeros(4096, dtype=torch.int32, device="cuda")
-    f = _lib.BfpFormat(7, 20, 1, 0, b"")  # legal but not instantiated
-    assert L.bfp_add(C.byref(f), t.data_ptr(), t.data_ptr(), t.data_ptr(), 10, None) == _lib.BFP_EUNSUPPORTED
+    f = _lib.BfpFormat(12, 20, 1, 0, b"")  # illegal (validate: e <= 11)
+    assert L.bfp_add(C.byref(f), t.data_ptr(), t.data_ptr(), t.data_ptr(), 10, None) == _lib.BFP_EFORMAT
     f = _lib.BfpFormat(1, 3, 1, 0, b"")
     assert L.bfp_add(C.byref(f), t.data_ptr(), t.data_ptr(), t.data_ptr(), 10, None) == _lib.BFP_EFORMAT
     f = _lib.BfpFormat(4, 3, 1, 0, b"")
