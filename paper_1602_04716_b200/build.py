@@ -31,12 +31,40 @@ NVCC_FLAGS = ARCH + [
 ]
 
 
+GEN_DIR = CSRC / "gen"
+LUTMAP = PKG.parent / "tools" / "lutmap"
+
+
+def generate(verbose: bool = True) -> None:
+    """LOP3-mapped covers of the compiled networks (tools/lutmap/gen.cpp):
+    rebuilt when the circuits, the format list or the mapper change."""
+    deps = [CSRC / "bfp_circuits.cuh", CSRC / "bfp_formats.h"] + sorted(LUTMAP.glob("*.[ch]pp"))
+    outs = sorted(GEN_DIR.glob("gen_*.cuh"))
+    if len(outs) >= 9 and not any(_stale(o, deps) for o in outs):
+        return
+    GEN_DIR.mkdir(exist_ok=True)
+    BUILD.mkdir(exist_ok=True)
+    exe = BUILD / "lutmap_gen"
+    subprocess.run(["g++", "-O2", "-std=c++17", f"-I{CSRC}", str(LUTMAP / "gen.cpp"), "-o", str(exe)],
+                   check=True)
+    subprocess.run([str(exe), str(GEN_DIR)], check=True)
+    if verbose:
+        print(f"[bfp build] generated LOP3 covers in {GEN_DIR}", file=sys.stderr)
+
+
 def sources() -> list[Path]:
     return sorted(CSRC.glob("*.cu")) + sorted((CSRC / "inst").glob("*.cu"))
 
 
 def headers() -> list[Path]:
-    return sorted(CSRC.glob("*.cuh")) + sorted(CSRC.glob("*.h")) + sorted(INCLUDE.glob("*.h"))
+    return (sorted(CSRC.glob("*.cuh")) + sorted(CSRC.glob("*.h")) + sorted(INCLUDE.glob("*.h")))
+
+
+def _deps(src: Path) -> list[Path]:
+    d = [src] + headers()
+    if src.parent.name == "inst":  # its generated cover
+        d.append(GEN_DIR / src.name.replace("fmt_", "gen_").replace(".cu", ".cuh"))
+    return d
 
 
 def _obj(src: Path) -> Path:
@@ -53,7 +81,7 @@ def _stale(target: Path, deps: list[Path]) -> bool:
 
 def _compile(src: Path, force: bool) -> tuple[Path, str]:
     obj = _obj(src)
-    if not force and not _stale(obj, [src] + headers()):
+    if not force and not _stale(obj, _deps(src)):
         return obj, "up-to-date"
     cmd = [NVCC, *NVCC_FLAGS, "-c", str(src), "-o", str(obj)]
     r = subprocess.run(cmd, capture_output=True, text=True)
@@ -66,6 +94,7 @@ def _compile(src: Path, force: bool) -> tuple[Path, str]:
 
 def build(jobs: int | None = None, force: bool = False, verbose: bool = True) -> Path:
     BUILD.mkdir(exist_ok=True)
+    generate(verbose)
     srcs = sources()
     jobs = jobs or max(1, min(len(srcs), os.cpu_count() or 4))
     with ThreadPoolExecutor(jobs) as ex:

@@ -50,8 +50,14 @@ typedef unsigned long long uintptr_t;
 
 namespace bfpg {
 
+#if defined(BFP_SYMBOLIC_WORD)
+// tools/lutmap: the same networks evaluated on a symbolic word (a DAG node)
+typedef BFP_SYMBOLIC_WORD w32;
+static const w32 ONES = w32(0xffffffffu);
+#else
 typedef uint32_t w32;
 constexpr w32 ONES = 0xffffffffu;
+#endif
 
 template <int E_, int S_, bool RN_, bool FTZ_>
 struct Format {
@@ -229,6 +235,14 @@ BFP_HD void pack_round(const w32* expf, const w32* sig /*S+1*/, w32 rnd, w32* fr
     c = v & c;
   }
 }
+
+// Generated LOP3 covers (tools/lutmap, build time) specialise this per
+// (format, op) with `ok = true` and a straight-line `run`; the templates
+// below are the source they are generated from and the fallback.
+template <class F, int OP>
+struct Gen {
+  static constexpr bool ok = false;
+};
 
 // ================================================================= ADD
 // Z = X + Y (SUB: X - Y).  bfp_add / bfp_sub semantics, arith.hpp:235-328.

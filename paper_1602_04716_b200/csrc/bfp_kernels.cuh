@@ -54,7 +54,9 @@ struct Operands {
 
 template <class F, int OP>
 __device__ __forceinline__ void eval_unit(const w32* X, const w32* Y, const w32* Cc, w32* Z) {
-  if constexpr (OP == OP_ADD) {
+  if constexpr (Gen<F, OP>::ok) {
+    Gen<F, OP>::run(X, Y, Cc, Z);  // LOP3-mapped cover of the same network
+  } else if constexpr (OP == OP_ADD) {
     add_w<F, false>(X, Y, Z);
   } else if constexpr (OP == OP_SUB) {
     add_w<F, true>(X, Y, Z);

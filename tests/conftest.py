@@ -66,6 +66,9 @@ class HostCircuits:
 
     def __init__(self):
         native = ROOT / "tests" / "native"
+        if not (ROOT / "paper_1602_04716_b200" / "csrc" / "gen" / "gen_8_23.cuh").exists():
+            from paper_1602_04716_b200.build import generate
+            generate(verbose=False)
         subprocess.run(["make", "-s", "-C", str(native)], check=True)
         L = C.CDLL(str(native / "libhostcirc.so"))
         vp = C.c_void_p
@@ -75,8 +78,8 @@ class HostCircuits:
         L.host_unpack_enc.argtypes = [C.c_int, C.c_uint, vp, C.c_size_t, vp]
         self.L = L
 
-    def binop(self, op: str, fmt, px, py, pc=None):
-        code = {"add": 0, "sub": 1, "mul": 2, "div": 3, "mul_add": 4}[op]
+    def binop(self, op: str, fmt, px, py, pc=None, generated: bool = False):
+        code = {"add": 0, "sub": 1, "mul": 2, "div": 3, "mul_add": 4}[op] + (10 if generated else 0)
         nb = 1 + fmt[0] + fmt[1]
         z = np.zeros_like(px)
         rc = self.L.host_binop(code, fmt[0], fmt[1], fmt[2], fmt[3], px.ctypes.data, py.ctypes.data,

@@ -10,6 +10,16 @@
 #include "../../paper_1602_04716_b200/csrc/bfp_circuits.cuh"
 #include "../../paper_1602_04716_b200/csrc/bfp_formats.h"
 #include "../../paper_1602_04716_b200/csrc/bfp_layout.cuh"
+// the generated LOP3 covers (paper_1602_04716_b200/build.py writes them)
+#include "../../paper_1602_04716_b200/csrc/gen/gen_3_2.cuh"
+#include "../../paper_1602_04716_b200/csrc/gen/gen_4_3.cuh"
+#include "../../paper_1602_04716_b200/csrc/gen/gen_5_3.cuh"
+#include "../../paper_1602_04716_b200/csrc/gen/gen_5_7.cuh"
+#include "../../paper_1602_04716_b200/csrc/gen/gen_5_10.cuh"
+#include "../../paper_1602_04716_b200/csrc/gen/gen_6_9.cuh"
+#include "../../paper_1602_04716_b200/csrc/gen/gen_8_7.cuh"
+#include "../../paper_1602_04716_b200/csrc/gen/gen_8_15.cuh"
+#include "../../paper_1602_04716_b200/csrc/gen/gen_8_23.cuh"
 
 using namespace bfpg;
 
@@ -27,6 +37,11 @@ static void run(int op, const uint32_t* x, const uint32_t* y, const uint32_t* c,
         C[j] = c ? c[w] : 0u;
       }
       switch (op) {
+        case 10: Gen<F, 0>::run(X, Y, C, Z); break;  // generated covers
+        case 11: Gen<F, 1>::run(X, Y, C, Z); break;
+        case 12: Gen<F, 2>::run(X, Y, C, Z); break;
+        case 13: Gen<F, 3>::run(X, Y, C, Z); break;
+        case 14: Gen<F, 4>::run(X, Y, C, Z); break;
         case 0: add_w<F, false>(X, Y, Z); break;
         case 1: add_w<F, true>(X, Y, Z); break;
         case 2: mul_w<F>(X, Y, Z); break;

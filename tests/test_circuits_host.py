@@ -12,15 +12,18 @@ from conftest import FORMATS, MODES, all_pairs, operands, related, ROOT
 GOLDEN = ROOT / "tests" / "golden"
 
 
-def _check(O, host, op, fmt, x, y, c=None):
+def _check(O, host, op, fmt, x, y, c=None, generated=(False, True)):
+    """templates AND the generated LOP3 covers (the code the kernels run)."""
     nb = 1 + fmt[0] + fmt[1]
     px, py = O.pack_planes(x, nb), O.pack_planes(y, nb)
     pc = O.pack_planes(c, nb) if c is not None else None
-    got = O.unpack_planes(host.binop(op, fmt, px, py, pc), len(x), nb)
     want = O.binop(op, fmt, x, y, c)
-    bad = np.nonzero(want != got)[0]
-    assert len(bad) == 0, (op, fmt, len(bad), [(hex(int(x[i])), hex(int(y[i])), hex(int(want[i])),
-                                                hex(int(got[i]))) for i in bad[:5]])
+    for gen in generated:
+        got = O.unpack_planes(host.binop(op, fmt, px, py, pc, gen), len(x), nb)
+        bad = np.nonzero(want != got)[0]
+        assert len(bad) == 0, (op, fmt, gen, len(bad),
+                               [(hex(int(x[i])), hex(int(y[i])), hex(int(want[i])), hex(int(got[i])))
+                                for i in bad[:5]])
 
 
 @pytest.mark.parametrize("fmt2", [(3, 2), (4, 3), (5, 3)])
@@ -35,7 +38,7 @@ def test_exhaustive_small(oracle, host, fmt2, mode, op):
 def test_exhaustive_13bit(oracle, host, op):
     """1/5/7: all 2^26 pairs, RN + gradual."""
     x, y = all_pairs(13)
-    _check(oracle, host, op, (5, 7, 1, 0), x, y)
+    _check(oracle, host, op, (5, 7, 1, 0), x, y, generated=(False,))  # covers: GPU suite
 
 
 @pytest.mark.parametrize("fmt2", [f for f in FORMATS if 1 + f[0] + f[1] > 9])
@@ -71,9 +74,11 @@ def test_golden_host(oracle, host):
             x, y, c = (g[f"{k}_{key}"].astype(np.uint64) for k in "xyc")
             px, py, pc = (oracle.pack_planes(v, nb) for v in (x, y, c))
             for op in ("add", "sub", "mul", "div", "mul_add"):
-                z = host.binop(op, (e, s, rn, ftz), px, py, pc if op == "mul_add" else None)
-                got = oracle.unpack_planes(z, len(x), nb)
-                assert np.array_equal(got, g[f"{op}_{key}"].astype(np.uint64)), (op, key)
+                for generated in (False, True):
+                    z = host.binop(op, (e, s, rn, ftz), px, py, pc if op == "mul_add" else None,
+                                   generated)
+                    got = oracle.unpack_planes(z, len(x), nb)
+                    assert np.array_equal(got, g[f"{op}_{key}"].astype(np.uint64)), (op, key)
 
 
 # ----------------------------------------------------------------------- codec
