@@ -23,6 +23,21 @@ bool jit_available();
 using bfpg::Impl;
 
 namespace bfpg {
+int bulk_mode() {
+  static const int m = [] {
+    const char* v = std::getenv("BFP_BULK");
+    return v ? std::atoi(v) : 1;
+  }();
+  return m;
+}
+int grid_mult() {
+  static const int m = [] {
+    const char* v = std::getenv("BFP_GRID_MULT");
+    const int k = v ? std::atoi(v) : 4;
+    return k > 0 ? k : 1;
+  }();
+  return m;
+}
 bool pdl_enabled() {
   static const bool on = [] {
     const char* v = std::getenv("BFP_PDL");

@@ -14,6 +14,8 @@
 #pragma once
 #if !defined(__CUDACC_RTC__)
 #include <cuda_runtime.h>
+
+#include <algorithm>
 #endif
 
 #include "bfp_circuits.cuh"
@@ -89,6 +91,130 @@ __global__ void __launch_bounds__(kThreads) k_arith(const w32* __restrict__ x,
     eval_unit<F, OP>(cur.v[0], cur.v[1], cur.v[NIN - 1], Z);
     BFP_UNROLL for (int j = 0; j < N; ++j) st_stream(z + base + j * 32, Z[j]);
   }
+}
+
+// ---------------------------------------------- bulk-copy pipelined variant
+// Each warp streams its blocks through a STAGES-deep ring in shared memory:
+// one lane issues cp.async.bulk (global -> shared, completion counted on an
+// mbarrier with expect_tx) for the NIN operand tiles of a block -- a block's
+// N planes are contiguous, N x 128 B per operand -- STAGES blocks ahead; all
+// lanes wait on the stage's mbarrier phase, read their plane words with
+// conflict-free LDS.32, hand the stage back, evaluate the network and store
+// the result planes with coalesced STG.  Loads stay in flight during the
+// network instead of alternating with it.
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_addr(bar)),
+      "r"(phase)
+      : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+
+template <int N, int NIN>
+constexpr int bulk_stages() {
+  constexpr int stage_bytes = NIN * N * 128;
+  constexpr int s = (16 * 1024) / stage_bytes;
+  return s < 2 ? 2 : (s > 4 ? 4 : s);
+}
+
+template <class F, int OP>
+__global__ void __launch_bounds__(kThreads) k_arith_bulk(const w32* __restrict__ x,
+                                                         const w32* __restrict__ y,
+                                                         const w32* __restrict__ c,
+                                                         w32* __restrict__ z, size_t nblocks) {
+  constexpr int N = F::N;
+  constexpr int NIN = OP == OP_MUL_ADD ? 3 : 2;
+  constexpr int ST = bulk_stages<N, NIN>();
+  constexpr int TW = N * 32;  // words per operand tile
+  extern __shared__ __align__(128) w32 dsm[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  w32* ring = dsm + wib * ST * NIN * TW;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(dsm + (kThreads / 32) * ST * NIN * TW) + wib * ST;
+  if (lane == 0) {
+    BFP_UNROLL for (int s = 0; s < ST; ++s) mbar_init(bars + s, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  pdl_enter();
+  const size_t tw = size_t(gridDim.x) * (kThreads / 32);
+  const size_t gw = size_t(blockIdx.x) * (kThreads / 32) + wib;
+  const w32* src[3] = {x, y, c};
+  auto issue = [&](int s, size_t b) {
+    mbar_expect_tx(bars + s, NIN * TW * 4);
+    BFP_UNROLL for (int a = 0; a < NIN; ++a)
+      bulk_g2s(ring + (s * NIN + a) * TW, src[a] + b * TW, TW * 4, bars + s);
+  };
+  if (lane == 0) {
+    BFP_UNROLL for (int s = 0; s < ST; ++s) {
+      const size_t b = gw + size_t(s) * tw;
+      if (b < nblocks) issue(s, b);
+    }
+  }
+  size_t i = 0;
+  for (size_t b = gw; b < nblocks; b += tw, ++i) {
+    const int s = int(i % ST);
+    mbar_wait(bars + s, uint32_t((i / ST) & 1));
+    w32 ops[NIN][N];
+    BFP_UNROLL for (int a = 0; a < NIN; ++a)
+      BFP_UNROLL for (int j = 0; j < N; ++j) ops[a][j] = ring[(s * NIN + a) * TW + j * 32 + lane];
+    __syncwarp();
+    if (lane == 0) {
+      const size_t bn = b + size_t(ST) * tw;
+      if (bn < nblocks) issue(s, bn);
+    }
+    w32 Z[N];
+    eval_unit<F, OP>(ops[0], ops[1], ops[NIN - 1], Z);
+    const size_t base = b * size_t(TW) + lane;
+    BFP_UNROLL for (int j = 0; j < N; ++j) st_stream(z + base + j * 32, Z[j]);
+  }
+}
+
+// Logic-bound networks (LOP3 per byte of HBM traffic above the B200's
+// ~2.9 LOP3/byte balance point, with margin) take the bulk-copy pipeline;
+// HBM-bound ones keep the plain loop (measured: the ring's shared memory costs
+// them occupancy, and 1-KB bulk tiles underuse the copy engine).
+template <class F, int OP>
+constexpr bool prefer_bulk() {
+  if constexpr (Gen<F, OP>::ok) {
+    constexpr int NIN = OP == OP_MUL_ADD ? 3 : 2;
+    constexpr double lop3_per_elem = Gen<F, OP>::luts / 32.0;
+    constexpr double bytes_per_elem = (NIN + 1) * F::N / 8.0;
+    return lop3_per_elem / bytes_per_elem > 2.2;
+  } else {
+    return false;
+  }
+}
+
+template <class F, int OP>
+constexpr size_t bulk_smem_bytes() {
+  constexpr int NIN = OP == OP_MUL_ADD ? 3 : 2;
+  return size_t(kThreads / 32) * bulk_stages<F::N, NIN>() * (NIN * F::N * 128 + 8);
 }
 
 // ------------------------------------------------------------------ pack
@@ -181,7 +307,16 @@ __device__ __forceinline__ void tile_to_global(const w32* tile, w32* __restrict_
 }
 
 // Element side of one warp's 1024 elements (EB bytes each): coalesced via the
-// tile when the warp's range is complete and 16-B aligned, else per element.
+// tile when the warp's range is complete and 16-B aligned; otherwise each lane
+// moves its own unit's bytes between global memory and its tile row one byte
+// at a time (zero past n).  Either way the registers are filled from / drained
+// to the tile with static indices only -- a dynamically indexed register
+// array would be demoted to local memory for the fast path as well.
+template <int CH>
+__device__ __forceinline__ w32* tile_word(w32* tile, int row, int word) {
+  return tile + tile_off<CH>(row, word >> 2) + (word & 3);
+}
+
 template <int EB>
 __device__ __forceinline__ void warp_load_elems(const uint8_t* __restrict__ src, size_t u, size_t n,
                                                 bool aligned, w32* tile, int lane, w32* L) {
@@ -189,12 +324,21 @@ __device__ __forceinline__ void warp_load_elems(const uint8_t* __restrict__ src,
   const size_t e0w = (u - lane) * 32;
   if (aligned && e0w + 1024 <= n) {
     tile_from_global<CH>(tile, reinterpret_cast<const w32*>(src + e0w * EB), lane);
-    __syncwarp();
-    tile_load_rows<CH>(tile, L, lane);
-    __syncwarp();
   } else {
-    load_unit<EB>(src, u, n, aligned, L);
+    const size_t e0 = u * 32;
+    const size_t nb = (n > e0) ? ((n - e0 < 32 ? n - e0 : 32) * EB) : 0;
+    for (int w = 0; w < 8 * EB; ++w) {
+      w32 v = 0;
+      for (int t = 0; t < 4; ++t) {
+        const size_t b = size_t(4 * w + t);
+        if (b < nb) v |= w32(src[e0 * EB + b]) << (8 * t);
+      }
+      *tile_word<CH>(tile, lane, w) = v;
+    }
   }
+  __syncwarp();
+  tile_load_rows<CH>(tile, L, lane);
+  __syncwarp();
 }
 
 template <int EB>
@@ -202,14 +346,17 @@ __device__ __forceinline__ void warp_store_elems(uint8_t* __restrict__ dst, size
                                                  bool aligned, w32* tile, int lane, const w32* L) {
   constexpr int CH = 2 * EB;
   const size_t e0w = (u - lane) * 32;
+  tile_store_rows<CH>(tile, L, lane);
+  __syncwarp();
   if (aligned && e0w + 1024 <= n) {
-    tile_store_rows<CH>(tile, L, lane);
-    __syncwarp();
     tile_to_global<CH>(tile, reinterpret_cast<w32*>(dst + e0w * EB), lane);
-    __syncwarp();
   } else {
-    store_unit<EB>(dst, u, n, aligned, L);
+    const size_t e0 = u * 32;
+    const size_t nb = (n > e0) ? ((n - e0 < 32 ? n - e0 : 32) * EB) : 0;
+    for (size_t b = 0; b < nb; ++b)
+      dst[e0 * EB + b] = uint8_t(*tile_word<CH>(tile, lane, int(b >> 2)) >> (8 * (b & 3)));
   }
+  __syncwarp();
 }
 
 // Raw encodings (EB = 1/2/4 bytes each) -> planes.  Every unit of every
@@ -436,21 +583,47 @@ inline cudaError_t launch(void (*k)(KArgs...), int grid, cudaStream_t st, Args..
   return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
 }
 
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_smem(void (*k)(KArgs...), int grid, size_t smem, cudaStream_t st,
+                               Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
+
+int bulk_mode();   // bfp_capi.cu: BFP_BULK = 0 off / 1 auto (default) / 2 force
+int grid_mult();   // bfp_capi.cu: BFP_GRID_MULT (default 4): CTA waves per grid
+
 // Resident CTAs for a full wave of `kernel`: #SM x occupancy.
 template <typename K>
-inline int wave_ctas(K kernel) {
+inline int wave_ctas(K kernel, size_t smem = 0) {
   int dev = 0, sms = 0, occ = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (sms <= 0) sms = 148;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kThreads, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kThreads, smem);
   if (occ <= 0) occ = 1;
   return sms * occ;
 }
 
+// Grid: up to grid_mult() (default 4) resident waves of CTAs -- oversubscription
+// lets the CTA scheduler backfill SMs at the tail, measured +5-8% on HBM-bound
+// kernels -- but never below two units per thread (single-unit CTAs measured
+// slower) and never below one wave.
 inline int grid_for(int wave, size_t units) {
   const size_t need = (units + kThreads - 1) / kThreads;
-  return int(need < size_t(wave) ? (need ? need : 1) : size_t(wave));
+  if (need <= size_t(wave)) return int(need ? need : 1);
+  const size_t cap = size_t(wave) * size_t(grid_mult());
+  const size_t two = (need + 1) / 2;
+  return int(std::min(cap, std::max(size_t(wave), two)));
 }
 
 // Per-format entry points: implemented by the compiled networks
@@ -483,6 +656,19 @@ struct FormatImpl {
   template <int OP>
   static cudaError_t launch_arith(const w32* x, const w32* y, const w32* c, w32* z, size_t units,
                                   cudaStream_t st) {
+    const int bulk = bulk_mode();  // 0 off, 1 auto (prefer_bulk), 2 force
+    if (bulk == 2 || (bulk == 1 && prefer_bulk<F, OP>())) {
+      auto kb = k_arith_bulk<F, OP>;
+      constexpr size_t smem = bulk_smem_bytes<F, OP>();
+      static const int wave_b = [&] {
+        cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        return wave_ctas(kb, smem);
+      }();
+      const size_t nblocks = units / 32;
+      const size_t warps = (nblocks + 0);  // one block per warp-iteration
+      const int grid = int(std::min<size_t>(size_t(wave_b), (warps + kThreads / 32 - 1) / (kThreads / 32)));
+      return launch_smem(kb, grid > 0 ? grid : 1, smem, st, x, y, c, z, nblocks);
+    }
     auto k = k_arith<F, OP>;
     static const int wave = wave_ctas(k);
     return launch(k, grid_for(wave, units), st, x, y, c, z, units);
