@@ -129,6 +129,11 @@ void bfp_host_ctx_destroy(bfp_host_ctx* ctx);
 bfp_status bfp_arith_host(bfp_host_ctx* ctx, int op, const bfp_format* f, const uint32_t* h_x,
                           const uint32_t* h_y, const uint32_t* h_c, uint32_t* h_z,
                           size_t count);
+/* nops ops (0..4) over the same host operands; each input chunk crosses PCIe
+ * once, result k goes to h_z[k]. */
+bfp_status bfp_arith_host_batch(bfp_host_ctx* ctx, int nops, const int* ops, const bfp_format* f,
+                                const uint32_t* h_x, const uint32_t* h_y, const uint32_t* h_c,
+                                uint32_t* const* h_z, size_t count);
 bfp_status bfp_pack_f32_host(bfp_host_ctx* ctx, const bfp_format* f, const float* h_in,
                              uint32_t* h_planes, size_t count);
 bfp_status bfp_unpack_f32_host(bfp_host_ctx* ctx, const bfp_format* f,

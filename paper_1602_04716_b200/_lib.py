@@ -59,6 +59,8 @@ SIGNATURES = {
     "bfp_host_ctx_destroy": (None, [C.c_void_p]),
     "bfp_arith_host": (C.c_int, [C.c_void_p, C.c_int, _F, C.c_void_p, C.c_void_p, C.c_void_p,
                                  C.c_void_p, C.c_size_t]),
+    "bfp_arith_host_batch": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_int), _F, C.c_void_p,
+                                       C.c_void_p, C.c_void_p, C.POINTER(C.c_void_p), C.c_size_t]),
     "bfp_pack_f32_host": (C.c_int, [C.c_void_p, _F, C.c_void_p, C.c_void_p, C.c_size_t]),
     "bfp_unpack_f32_host": (C.c_int, [C.c_void_p, _F, C.c_void_p, C.c_void_p, C.c_size_t]),
     "bfp_host_alloc": (C.c_void_p, [C.c_size_t]),

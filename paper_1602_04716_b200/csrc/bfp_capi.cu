@@ -420,6 +420,59 @@ bfp_status bfp_arith_host(bfp_host_ctx* c, int op, const bfp_format* f, const ui
                        });
 }
 
+// Several ops over the SAME host operands: each chunk's inputs cross PCIe
+// once, every op runs on them, each op's result comes back (a caller doing
+// z1 = x * y, z2 = x - y on host vectors).
+bfp_status bfp_arith_host_batch(bfp_host_ctx* c, int nops, const int* ops, const bfp_format* f,
+                                const uint32_t* h_x, const uint32_t* h_y, const uint32_t* h_c,
+                                uint32_t* const* h_z, size_t count) {
+  const Impl* impl = nullptr;
+  bfp_status s = resolve(f, &impl);
+  if (s != BFP_OK) return s;
+  if (!c) return fail(BFP_EARG, "null host context");
+  if (nops <= 0 || nops > 8 || !ops || !h_z) return fail(BFP_EARG, "bad op list");
+  bool need_c = false;
+  for (int k = 0; k < nops; ++k) {
+    if (ops[k] < 0 || ops[k] > 4) return fail(BFP_EARG, "bad op");
+    if (!h_z[k]) return fail(BFP_EARG, "null output");
+    need_c |= ops[k] == 4;
+  }
+  if (!h_x || !h_y || (need_c && !h_c)) return fail(BFP_EARG, "null operand");
+  const size_t stride = nplanes(f) * 128;
+  const size_t blocks = nblocks(count);
+  // per chunk: inputs into in[i][0..2], outputs staged in out[i] one op at a
+  // time (out[i] is reused; the D2H of op k is ordered before the kernel of op
+  // k+1 on the same stream)
+  for (size_t b0 = 0, k = 0; b0 < blocks; b0 += c->chunk_blocks, ++k) {
+    const int i = int(k % bfp_host_ctx::kDepth);
+    const size_t nb = (blocks - b0 < c->chunk_blocks) ? blocks - b0 : c->chunk_blocks;
+    const size_t bytes = nb * stride;
+    const void* ins[3] = {h_x, h_y, h_c};
+    for (int a = 0; a < (need_c ? 3 : 2); ++a) {
+      cudaError_t e = cudaMemcpyAsync(c->in[i][a], static_cast<const char*>(ins[a]) + b0 * stride,
+                                      bytes, cudaMemcpyHostToDevice, c->st[i]);
+      if (e != cudaSuccess) return cuda_status(e, "H2D");
+    }
+    for (int q = 0; q < nops; ++q) {
+      ++g_launches;
+      s = cuda_status(impl->arith(ops[q], static_cast<const uint32_t*>(c->in[i][0]),
+                                  static_cast<const uint32_t*>(c->in[i][1]),
+                                  static_cast<const uint32_t*>(c->in[i][2]),
+                                  static_cast<uint32_t*>(c->out[i]), nb, c->st[i]),
+                      "arith launch");
+      if (s != BFP_OK) return s;
+      cudaError_t e = cudaMemcpyAsync(reinterpret_cast<char*>(h_z[q]) + b0 * stride, c->out[i], bytes,
+                                      cudaMemcpyDeviceToHost, c->st[i]);
+      if (e != cudaSuccess) return cuda_status(e, "D2H");
+    }
+  }
+  for (int i = 0; i < bfp_host_ctx::kDepth; ++i) {
+    cudaError_t e = cudaStreamSynchronize(c->st[i]);
+    if (e != cudaSuccess) return cuda_status(e, "sync");
+  }
+  return BFP_OK;
+}
+
 bfp_status bfp_pack_f32_host(bfp_host_ctx* c, const bfp_format* f, const float* h_in,
                              uint32_t* h_planes, size_t count) {
   const Impl* impl = nullptr;

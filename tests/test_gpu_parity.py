@@ -457,3 +457,26 @@ def test_arith_f32_unaligned():
                            torch.cuda.current_stream().cuda_stream) == 0
     ref = bfp.unpack_f32(bfp.bfp_mul(bfp.pack_f32(x, spec), bfp.pack_f32(y, spec)))
     assert torch.equal(z.view(torch.int32), ref.view(torch.int32))
+
+
+def test_host_batch_matches_device(oracle):
+    """bfp_arith_host_batch: several ops over one H2D of shared host operands."""
+    L = _lib.lib()
+    fmt = (4, 3, 1, 0)
+    n = 3 * (1 << 20) + 777
+    rng = np.random.default_rng(8)
+    x, y = operands(4, 3, n, rng), operands(4, 3, n, rng)
+    px, py = oracle.pack_planes(x, 8), oracle.pack_planes(y, 8)
+    outs = [np.zeros_like(px) for _ in range(3)]
+    ops = [2, 1, 3]
+    ctx = L.bfp_host_ctx_create(1 << 20)
+    try:
+        f = cfmt(fmt)
+        arr = (C.c_int * 3)(*ops)
+        ptrs = (C.c_void_p * 3)(*[o.ctypes.data for o in outs])
+        assert L.bfp_arith_host_batch(ctx, 3, arr, C.byref(f), px.ctypes.data, py.ctypes.data, None,
+                                      ptrs, n) == 0
+    finally:
+        L.bfp_host_ctx_destroy(ctx)
+    for o, op in zip(outs, ("mul", "sub", "div")):
+        assert np.array_equal(oracle.unpack_planes(o, n, 8), oracle.binop(op, fmt, x, y)), op
