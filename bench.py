@@ -362,7 +362,7 @@ def run_e2e(cfg: str, jobs, steps: int, world: int, rank: int, local: int) -> di
 
     device = torch.device("cuda", local)
     L = bfp.lib()
-    ctx = L.bfp_host_ctx_create(1 << 22)
+    ctx = L.bfp_host_ctx_create(int(os.environ.get("BFP_E2E_CHUNK", 1 << 24)))
     bufs = []
 
     def pinned(nbytes):
@@ -439,6 +439,44 @@ def run_e2e(cfg: str, jobs, steps: int, world: int, rank: int, local: int) -> di
         for p in bufs:
             L.bfp_host_free(p)
         L.bfp_host_ctx_destroy(ctx)
+
+
+def pcie_probe(local: int, nbytes: int = 1 << 28) -> dict:
+    """Pinned-host <-> device copy bandwidth on this box (the e2e ceiling):
+    H2D alone, D2H alone, and both directions at once on two streams."""
+    import torch
+    dev = torch.device("cuda", local)
+    h_in = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    h_out = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    d_a = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    d_b = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    s1, s2 = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+
+    def timed(fn, reps=3):
+        best = 1e9
+        for _ in range(reps):
+            torch.cuda.synchronize(dev)
+            t = time.perf_counter()
+            fn()
+            torch.cuda.synchronize(dev)
+            best = min(best, time.perf_counter() - t)
+        return best
+
+    def h2d():
+        d_a.copy_(h_in, non_blocking=True)
+
+    def d2h():
+        h_out.copy_(d_b, non_blocking=True)
+
+    def both():
+        with torch.cuda.stream(s1):
+            d_a.copy_(h_in, non_blocking=True)
+        with torch.cuda.stream(s2):
+            h_out.copy_(d_b, non_blocking=True)
+
+    t1, t2, t3 = timed(h2d), timed(d2h), timed(both)
+    return {"h2d_gbs": round(nbytes / t1 / 1e9, 1), "d2h_gbs": round(nbytes / t2 / 1e9, 1),
+            "bidir_gbs": round(2 * nbytes / t3 / 1e9, 1)}
 
 
 def lop3_peak() -> float | None:
@@ -685,7 +723,13 @@ def main_ours(args) -> None:
             "gpu_launches": res["launches"],
         }
         if e2e is not None:
+            pcie = pcie_probe(local)
+            # copy-only time of the step's traffic at the measured link rates
+            bound_s = max(e2e["h2d"] / (pcie["h2d_gbs"] * 1e9), e2e["d2h"] / (pcie["d2h_gbs"] * 1e9),
+                          (e2e["h2d"] + e2e["d2h"]) / (pcie["bidir_gbs"] * 1e9))
             line["e2e"] = {"value": round(e2e["elems"] * world / e2e["s_per_step"] / 1e9, 3),
+                           "pcie_measured": pcie,
+                           "frac_of_pcie_bound": round(bound_s / e2e["s_per_step"], 4),
                            "unit": UNIT, "h2d_bytes_per_step": int(e2e["h2d"]),
                            "d2h_bytes_per_step": int(e2e["d2h"]),
                            "path": "C ABI host entry points (bfp_arith_host_batch / "

@@ -315,13 +315,19 @@ uint64_t bfp_launch_count(void) { return g_launches.load(); }
 
 // ------------------------------------------------------------ host pipeline
 struct bfp_host_ctx {
-  static constexpr int kDepth = 3;
+  static constexpr int kDepth = 4;   // chunks in flight (one stream each)
+  static constexpr int kMaxOut = 8;  // outputs per chunk (batched ops)
   size_t chunk_blocks = 0;
   size_t cap_bytes = 0;  // per buffer
   cudaStream_t st[kDepth] = {};
   void* in[kDepth][3] = {};
-  void* out[kDepth] = {};
+  void* out[kDepth][kMaxOut] = {};
   int dev = 0;
+  // lazily allocated output buffer j of slot i
+  void* out_buf(int i, int j) {
+    if (!out[i][j] && cudaMalloc(&out[i][j], cap_bytes) != cudaSuccess) out[i][j] = nullptr;
+    return out[i][j];
+  }
 };
 
 bfp_host_ctx* bfp_host_ctx_create(size_t chunk_elems) {
@@ -335,7 +341,7 @@ bfp_host_ctx* bfp_host_ctx_create(size_t chunk_elems) {
     if (cudaStreamCreateWithFlags(&c->st[i], cudaStreamNonBlocking) != cudaSuccess) goto bad;
     for (int k = 0; k < 3; ++k)
       if (cudaMalloc(&c->in[i][k], c->cap_bytes) != cudaSuccess) goto bad;
-    if (cudaMalloc(&c->out[i], c->cap_bytes) != cudaSuccess) goto bad;
+    if (!c->out_buf(i, 0)) goto bad;
   }
   return c;
 bad:
@@ -350,7 +356,8 @@ void bfp_host_ctx_destroy(bfp_host_ctx* c) {
     if (c->st[i]) cudaStreamSynchronize(c->st[i]);
     for (int k = 0; k < 3; ++k)
       if (c->in[i][k]) cudaFree(c->in[i][k]);
-    if (c->out[i]) cudaFree(c->out[i]);
+    for (int k = 0; k < bfp_host_ctx::kMaxOut; ++k)
+      if (c->out[i][k]) cudaFree(c->out[i][k]);
     if (c->st[i]) cudaStreamDestroy(c->st[i]);
   }
   delete c;
@@ -384,7 +391,7 @@ bfp_status host_pipeline(bfp_host_ctx* c, size_t count, int n_in, const void* co
     if (s != BFP_OK) return s;
     const size_t obytes = out_elems ? ecount * 4 : nb * out_stride;
     char* dst = static_cast<char*>(h_out) + (out_elems ? e0 * 4 : b0 * out_stride);
-    cudaError_t e = cudaMemcpyAsync(dst, c->out[i], obytes, cudaMemcpyDeviceToHost, c->st[i]);
+    cudaError_t e = cudaMemcpyAsync(dst, c->out[i][0], obytes, cudaMemcpyDeviceToHost, c->st[i]);
     if (e != cudaSuccess) return cuda_status(e, "D2H");
   }
   for (int i = 0; i < bfp_host_ctx::kDepth; ++i) {
@@ -415,7 +422,7 @@ bfp_status bfp_arith_host(bfp_host_ctx* c, int op, const bfp_format* f, const ui
                              impl->arith(op, static_cast<const uint32_t*>(c->in[i][0]),
                                          static_cast<const uint32_t*>(c->in[i][1]),
                                          static_cast<const uint32_t*>(c->in[i][2]),
-                                         static_cast<uint32_t*>(c->out[i]), nblocks(ecount), st),
+                                         static_cast<uint32_t*>(c->out[i][0]), nblocks(ecount), st),
                              "arith launch");
                        });
 }
@@ -430,7 +437,7 @@ bfp_status bfp_arith_host_batch(bfp_host_ctx* c, int nops, const int* ops, const
   bfp_status s = resolve(f, &impl);
   if (s != BFP_OK) return s;
   if (!c) return fail(BFP_EARG, "null host context");
-  if (nops <= 0 || nops > 8 || !ops || !h_z) return fail(BFP_EARG, "bad op list");
+  if (nops <= 0 || nops > bfp_host_ctx::kMaxOut || !ops || !h_z) return fail(BFP_EARG, "bad op list");
   bool need_c = false;
   for (int k = 0; k < nops; ++k) {
     if (ops[k] < 0 || ops[k] > 4) return fail(BFP_EARG, "bad op");
@@ -440,9 +447,8 @@ bfp_status bfp_arith_host_batch(bfp_host_ctx* c, int nops, const int* ops, const
   if (!h_x || !h_y || (need_c && !h_c)) return fail(BFP_EARG, "null operand");
   const size_t stride = nplanes(f) * 128;
   const size_t blocks = nblocks(count);
-  // per chunk: inputs into in[i][0..2], outputs staged in out[i] one op at a
-  // time (out[i] is reused; the D2H of op k is ordered before the kernel of op
-  // k+1 on the same stream)
+  // per chunk: inputs into in[i][0..2], op q's result into out[i][q] (own
+  // buffer, so op q+1's kernel does not wait for op q's D2H)
   for (size_t b0 = 0, k = 0; b0 < blocks; b0 += c->chunk_blocks, ++k) {
     const int i = int(k % bfp_host_ctx::kDepth);
     const size_t nb = (blocks - b0 < c->chunk_blocks) ? blocks - b0 : c->chunk_blocks;
@@ -454,15 +460,19 @@ bfp_status bfp_arith_host_batch(bfp_host_ctx* c, int nops, const int* ops, const
       if (e != cudaSuccess) return cuda_status(e, "H2D");
     }
     for (int q = 0; q < nops; ++q) {
+      void* ob = c->out_buf(i, q);
+      if (!ob) return fail(BFP_ECUDA, "host ctx: output buffer allocation failed");
       ++g_launches;
       s = cuda_status(impl->arith(ops[q], static_cast<const uint32_t*>(c->in[i][0]),
                                   static_cast<const uint32_t*>(c->in[i][1]),
                                   static_cast<const uint32_t*>(c->in[i][2]),
-                                  static_cast<uint32_t*>(c->out[i]), nb, c->st[i]),
+                                  static_cast<uint32_t*>(ob), nb, c->st[i]),
                       "arith launch");
       if (s != BFP_OK) return s;
-      cudaError_t e = cudaMemcpyAsync(reinterpret_cast<char*>(h_z[q]) + b0 * stride, c->out[i], bytes,
-                                      cudaMemcpyDeviceToHost, c->st[i]);
+    }
+    for (int q = 0; q < nops; ++q) {
+      cudaError_t e = cudaMemcpyAsync(reinterpret_cast<char*>(h_z[q]) + b0 * stride, c->out[i][q],
+                                      bytes, cudaMemcpyDeviceToHost, c->st[i]);
       if (e != cudaSuccess) return cuda_status(e, "D2H");
     }
   }
@@ -484,7 +494,7 @@ bfp_status bfp_pack_f32_host(bfp_host_ctx* c, const bfp_format* f, const float* 
                        [&](int i, size_t ecount, cudaStream_t st) {
                          ++g_launches;
                          return cuda_status(impl->pack_f32(static_cast<const float*>(c->in[i][0]),
-                                                           static_cast<uint32_t*>(c->out[i]),
+                                                           static_cast<uint32_t*>(c->out[i][0]),
                                                            ecount, st),
                                             "pack_f32 launch");
                        });
@@ -502,7 +512,7 @@ bfp_status bfp_unpack_f32_host(bfp_host_ctx* c, const bfp_format* f, const uint3
                          ++g_launches;
                          return cuda_status(
                              impl->unpack_f32(static_cast<const uint32_t*>(c->in[i][0]),
-                                              static_cast<float*>(c->out[i]), ecount, st),
+                                              static_cast<float*>(c->out[i][0]), ecount, st),
                              "unpack_f32 launch");
                        });
 }

@@ -1,10 +1,10 @@
-timeout 1500 python -m pytest tests -q -x -m "gpu" > gpurun_out/pytest_gpu.log 2>&1; echo pytest_rc=$?
+timeout 600 python -m pytest tests -q -x -m "gpu and not slow" -k "host" > gpurun_out/pytest_gpu.log 2>&1; echo pytest_rc=$?
 tail -2 gpurun_out/pytest_gpu.log
-for p in 1 0 1 0; do
-BFP_PDL=$p timeout 900 python bench.py --config C3,C1,C2 --steps 30 --warmup 5 --no-cpu-baseline --no-e2e > gpurun_out/bench_p$p.log 2>/dev/null
+for c in 1048576 4194304 16777216; do
+BFP_E2E_CHUNK=$c timeout 900 python bench.py --config C2 --steps 20 --warmup 3 --no-cpu-baseline > gpurun_out/bench_e2e$c.log 2>/dev/null
 python3 -c "
-import json,sys
-for l in open('gpurun_out/bench_p$p.log'):
-    d=json.loads(l); print('PDL=$p', d['config']['workload'][:3], d['value'], d['ms_per_step'], d['clocks']['sm_mhz'], {k:(v['ms'],v['hbm_frac']) for k,v in d['roofline']['per_op'].items()})
+import json
+for l in open('gpurun_out/bench_e2e$c.log'):
+    d=json.loads(l); print('chunk=$c', d['value'], d['e2e'])
 "
 done
