@@ -70,12 +70,12 @@ bfp_status bfp_same_shape(const bfp_format* a, const bfp_format* b);
 /* 1 when the format can run: a compiled network (1/3/2, 1/4/3, 1/5/3, 1/5/7,
  * 1/5/10, 1/6/9, 1/8/7, 1/8/15, 1/8/23 x RN/RZ x gradual/FTZ) or, for every
  * other legal format, the NVRTC runtime backend (compiled on first use;
- * disable with BFP_JIT=0).  Layout kernels need n <= 32 bits, float32
- * conversions e <= 8 and s <= 23 (BFP_EUNSUPPORTED otherwise). */
+ * disable with BFP_JIT=0).  float32 conversions need e <= 8 and s <= 23
+ * (BFP_EUNSUPPORTED otherwise); everything else covers n <= 64. */
 int bfp_is_supported(const bfp_format* f);
 int bfp_is_compiled(const bfp_format* f); /* 1 when an ahead-of-time network exists */
 size_t bfp_plane_bytes(const bfp_format* f, size_t count);
-size_t bfp_enc_bytes(const bfp_format* f); /* device encoding width: 1, 2 or 4 */
+size_t bfp_enc_bytes(const bfp_format* f); /* device encoding width: 1, 2, 4 or 8 */
 
 /* ---- layout (device buffers) -------------------------------------------- */
 /* d_enc holds `count` encodings of bfp_enc_bytes(f) bytes each,
@@ -90,6 +90,13 @@ bfp_status bfp_pack_f32(const bfp_format* f, const float* d_in, uint32_t* d_plan
 bfp_status bfp_unpack_f32(const bfp_format* f, const uint32_t* d_planes, float* d_out,
                           size_t count, void* stream);
 
+/* binary64 <-> format: encode_scalar(double) / decode_scalar -> double
+ * (format.hpp:101-188) exactly -- the reference converter's own interface;
+ * every legal format. */
+bfp_status bfp_pack_f64(const bfp_format* f, const double* d_in, uint32_t* d_planes,
+                        size_t count, void* stream);
+bfp_status bfp_unpack_f64(const bfp_format* f, const uint32_t* d_planes, double* d_out,
+                          size_t count, void* stream);
 /* .bfpraw records (pack.hpp:78-109): count = nbytes / bfp_bfpraw_stride(f)
  * little-endian ceil(n/8)-byte encodings, back to back, no padding.
  * BFP_ESIZE when nbytes is not a multiple of the stride (pack.hpp:98-100). */

@@ -196,3 +196,13 @@ void orc_binop_exhaustive(int op, unsigned e, unsigned s, int rn, int ftz, uint6
   for (uint64_t x = 0; x < cnt; ++x)
     for (uint64_t y = 0; y < cnt; ++y) z[x * cnt + y] = orc_binop(op, e, s, rn, ftz, x, y);
 }
+
+/* binary64 array forms of encode_scalar / decode_scalar (format.hpp:101-188) */
+void orc_encode_f64_array(const double* in, size_t n, uint64_t* out, unsigned e, unsigned s,
+                          int rn, int ftz) {
+  for (size_t i = 0; i < n; ++i) out[i] = orc_encode(in[i], e, s, rn, ftz);
+}
+
+void orc_decode_f64_array(const uint64_t* enc, size_t n, double* out, unsigned e, unsigned s) {
+  for (size_t i = 0; i < n; ++i) out[i] = orc_decode(enc[i], e, s);
+}

@@ -69,6 +69,11 @@ def orc():
         L.orc_encode_f32_array.argtypes = [_f32p, C.c_size_t, _u64p, C.c_uint, C.c_uint, C.c_int, C.c_int]
         L.orc_decode_f32_array.restype = None
         L.orc_decode_f32_array.argtypes = [_u64p, C.c_size_t, _f32p, C.c_uint, C.c_uint]
+        L.orc_encode_f64_array.restype = None
+        L.orc_encode_f64_array.argtypes = [C.POINTER(C.c_double), C.c_size_t, _u64p, C.c_uint, C.c_uint,
+                                           C.c_int, C.c_int]
+        L.orc_decode_f64_array.restype = None
+        L.orc_decode_f64_array.argtypes = [_u64p, C.c_size_t, C.POINTER(C.c_double), C.c_uint, C.c_uint]
         L.orc_binop_exhaustive.restype = None
         L.orc_binop_exhaustive.argtypes = [C.c_int, C.c_uint, C.c_uint, C.c_int, C.c_int, _u64p]
         _orc = L
@@ -191,6 +196,23 @@ def decode_f32(fmt, enc: np.ndarray) -> np.ndarray:
     enc = np.ascontiguousarray(enc, dtype=np.uint64)
     out = np.empty(len(enc), dtype=np.float32)
     orc().orc_decode_f32_array(_p(enc, _u64p), len(enc), _p(out, _f32p), e, s)
+    return out
+
+
+def encode_f64(fmt, xs: np.ndarray) -> np.ndarray:
+    e, s, rn, ftz = fmt
+    xs = np.ascontiguousarray(xs, dtype=np.float64)
+    out = np.empty(len(xs), dtype=np.uint64)
+    orc().orc_encode_f64_array(xs.ctypes.data_as(C.POINTER(C.c_double)), len(xs), _p(out, _u64p),
+                               e, s, int(rn), int(ftz))
+    return out
+
+
+def decode_f64(fmt, enc: np.ndarray) -> np.ndarray:
+    enc = np.ascontiguousarray(enc, dtype=np.uint64)
+    out = np.empty(len(enc), dtype=np.float64)
+    orc().orc_decode_f64_array(_p(enc, _u64p), len(enc), out.ctypes.data_as(C.POINTER(C.c_double)),
+                               fmt[0], fmt[1])
     return out
 
 

@@ -27,12 +27,14 @@ from .bfp import (  # noqa: F401
     make_spec,
     pack,
     pack_f32,
+    pack_f64,
     require_same_shape,
     rounding_mode,
     subnormal_policy,
     to_u64,
     unpack,
     unpack_f32,
+    unpack_f64,
     validate,
 )
 from ._lib import LIB_PATH, lib  # noqa: F401

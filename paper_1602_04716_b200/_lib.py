@@ -42,6 +42,8 @@ SIGNATURES = {
     "bfp_unpack_enc": (C.c_int, [_F, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
     "bfp_pack_f32": (C.c_int, [_F, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
     "bfp_unpack_f32": (C.c_int, [_F, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
+    "bfp_pack_f64": (C.c_int, [_F, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
+    "bfp_unpack_f64": (C.c_int, [_F, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
     "bfp_bfpraw_stride": (C.c_size_t, [_F]),
     "bfp_pack_bfpraw": (C.c_int, [_F, C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p]),
     "bfp_unpack_bfpraw": (C.c_int, [_F, C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p]),

@@ -159,7 +159,7 @@ def empty(spec: format_spec, count: int, device=None) -> bfp_vector:
 
 
 def _enc_dtype(spec: format_spec) -> torch.dtype:
-    return {1: torch.uint8, 2: torch.int16, 4: torch.int32, 8: torch.int64}[spec.enc_bytes()]
+    return {1: torch.uint8, 2: torch.int16, 4: torch.int32, 8: torch.int64}[spec.enc_bytes()]  # bit patterns
 
 
 def pack(encs: torch.Tensor, spec: format_spec) -> bfp_vector:
@@ -218,6 +218,8 @@ def unpack_bfpraw(v: bfp_vector, count: int | None = None) -> torch.Tensor:
 
 def to_u64(encs: torch.Tensor, spec: format_spec) -> torch.Tensor:
     """Bit patterns of `unpack` as non-negative int64."""
+    if spec.total_bits() >= 64:
+        return encs.to(torch.int64)
     mask = (1 << spec.total_bits()) - 1
     return encs.to(torch.int64) & mask
 
@@ -240,6 +242,27 @@ def unpack_f32(v: bfp_vector, count: int | None = None) -> torch.Tensor:
     out = torch.empty(count, dtype=torch.float32, device=v.planes.device)
     check(lib().bfp_unpack_f32(v.spec.c, v.planes.data_ptr(), out.data_ptr(), count, _stream()),
           "unpack_f32")
+    return out
+
+
+def pack_f64(x: torch.Tensor, spec: format_spec) -> bfp_vector:
+    """binary64 -> encode_scalar (format.hpp:125-188, its own input type) -> planes."""
+    validate(spec)
+    x = x.to(torch.float64).contiguous()
+    out = empty(spec, x.numel(), x.device)
+    check(lib().bfp_pack_f64(spec.c, x.data_ptr(), out.planes.data_ptr(), x.numel(), _stream()),
+          "pack_f64")
+    return out
+
+
+def unpack_f64(v: bfp_vector, count: int | None = None) -> torch.Tensor:
+    """planes -> decode_scalar (format.hpp:101-123), exact binary64."""
+    count = v.count if count is None else count
+    if count > v.count:
+        raise ValueError("unpack_f64: count exceeds vector width")
+    out = torch.empty(count, dtype=torch.float64, device=v.planes.device)
+    check(lib().bfp_unpack_f64(v.spec.c, v.planes.data_ptr(), out.data_ptr(), count, _stream()),
+          "unpack_f64")
     return out
 
 

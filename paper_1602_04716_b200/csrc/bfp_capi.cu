@@ -268,11 +268,9 @@ bfp_status bfp_pack_bfpraw(const bfp_format* f, const void* d_bytes, size_t nbyt
   const size_t count = nbytes / stride;
   if (count == 0) return BFP_OK;
   if (!d_bytes || !d_planes) return fail(BFP_EARG, "null buffer");
-  if (stride > 4) return fail(BFP_EUNSUPPORTED, "bfpraw: records wider than 4 bytes");
   ++g_launches;
-  const cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (stride == 3) return cuda_status(impl->pack_raw3(d_bytes, d_planes, count, st), "pack_bfpraw");
-  return cuda_status(impl->pack_enc(d_bytes, d_planes, count, st), "pack_bfpraw");
+  return cuda_status(impl->pack_raw(d_bytes, d_planes, count, static_cast<cudaStream_t>(stream)),
+                     "pack_bfpraw");
 }
 
 bfp_status bfp_unpack_bfpraw(const bfp_format* f, const uint32_t* d_planes, size_t count,
@@ -282,12 +280,33 @@ bfp_status bfp_unpack_bfpraw(const bfp_format* f, const uint32_t* d_planes, size
   if (s != BFP_OK) return s;
   if (count == 0) return BFP_OK;
   if (!d_bytes || !d_planes) return fail(BFP_EARG, "null buffer");
-  const size_t stride = bfp_bfpraw_stride(f);
-  if (stride > 4) return fail(BFP_EUNSUPPORTED, "bfpraw: records wider than 4 bytes");
   ++g_launches;
-  const cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (stride == 3) return cuda_status(impl->unpack_raw3(d_planes, d_bytes, count, st), "unpack_bfpraw");
-  return cuda_status(impl->unpack_enc(d_planes, d_bytes, count, st), "unpack_bfpraw");
+  return cuda_status(impl->unpack_raw(d_planes, d_bytes, count, static_cast<cudaStream_t>(stream)),
+                     "unpack_bfpraw");
+}
+
+bfp_status bfp_pack_f64(const bfp_format* f, const double* d_in, uint32_t* d_planes,
+                        size_t count, void* stream) {
+  const Impl* impl = nullptr;
+  const bfp_status s = resolve(f, &impl);
+  if (s != BFP_OK) return s;
+  if (count == 0) return BFP_OK;
+  if (!d_in || !d_planes) return fail(BFP_EARG, "null buffer");
+  ++g_launches;
+  return cuda_status(impl->pack_f64(d_in, d_planes, count, static_cast<cudaStream_t>(stream)),
+                     "pack_f64 launch");
+}
+
+bfp_status bfp_unpack_f64(const bfp_format* f, const uint32_t* d_planes, double* d_out,
+                          size_t count, void* stream) {
+  const Impl* impl = nullptr;
+  const bfp_status s = resolve(f, &impl);
+  if (s != BFP_OK) return s;
+  if (count == 0) return BFP_OK;
+  if (!d_out || !d_planes) return fail(BFP_EARG, "null buffer");
+  ++g_launches;
+  return cuda_status(impl->unpack_f64(d_planes, d_out, count, static_cast<cudaStream_t>(stream)),
+                     "unpack_f64 launch");
 }
 
 bfp_status bfp_kernel_attrs(const bfp_format* f, int kernel, int* regs, int* ctas_per_sm,

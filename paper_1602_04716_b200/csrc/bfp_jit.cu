@@ -119,21 +119,21 @@ class JitFormat final : public Impl {
     uint8_t* e = static_cast<uint8_t*>(enc);
     return run(layout_expr("bfpg::k_unpack_enc<%d, %d>", eb), units, st, {&planes, &e, &n, &units, &al});
   }
-  cudaError_t pack_raw3(const void* bytes, w32* planes, size_t n, cudaStream_t st) const override {
-    if (N() <= 16 || N() > 24) return cudaErrorNotSupported;
+  cudaError_t pack_raw(const void* bytes, w32* planes, size_t n, cudaStream_t st) const override {
+    if (raw() == enc_bytes()) return pack_enc(bytes, planes, n, st);
     const size_t units = ((n + 1023) / 1024) * 32;
     if (!units) return cudaSuccess;
     const bool al = (reinterpret_cast<uintptr_t>(bytes) & 15) == 0;
     const uint8_t* b = static_cast<const uint8_t*>(bytes);
-    return run(layout_expr("bfpg::k_pack_enc<%d, %d>", 3), units, st, {&b, &planes, &n, &units, &al});
+    return run(layout_expr("bfpg::k_pack_enc<%d, %d>", raw()), units, st, {&b, &planes, &n, &units, &al});
   }
-  cudaError_t unpack_raw3(const w32* planes, void* bytes, size_t n, cudaStream_t st) const override {
-    if (N() <= 16 || N() > 24) return cudaErrorNotSupported;
+  cudaError_t unpack_raw(const w32* planes, void* bytes, size_t n, cudaStream_t st) const override {
+    if (raw() == enc_bytes()) return unpack_enc(planes, bytes, n, st);
     const size_t units = (n + 31) / 32;
     if (!units) return cudaSuccess;
     const bool al = (reinterpret_cast<uintptr_t>(bytes) & 15) == 0;
     uint8_t* b = static_cast<uint8_t*>(bytes);
-    return run(layout_expr("bfpg::k_unpack_enc<%d, %d>", 3), units, st, {&planes, &b, &n, &units, &al});
+    return run(layout_expr("bfpg::k_unpack_enc<%d, %d>", raw()), units, st, {&planes, &b, &n, &units, &al});
   }
   cudaError_t pack_f32(const float* in, w32* planes, size_t n, cudaStream_t st) const override {
     if (e_ > 8 || s_ > 23) return cudaErrorNotSupported;
@@ -148,6 +148,18 @@ class JitFormat final : public Impl {
     if (!units) return cudaSuccess;
     const bool al = (reinterpret_cast<uintptr_t>(out) & 15) == 0;
     return run(fmt_expr("bfpg::k_unpack_f32<%s>", -1), units, st, {&planes, &out, &n, &units, &al});
+  }
+  cudaError_t pack_f64(const double* in, w32* planes, size_t n, cudaStream_t st) const override {
+    const size_t units = ((n + 1023) / 1024) * 32;
+    if (!units) return cudaSuccess;
+    const bool al = (reinterpret_cast<uintptr_t>(in) & 15) == 0;
+    return run(fmt_expr("bfpg::k_pack_f64<%s>", -1), units, st, {&in, &planes, &n, &units, &al});
+  }
+  cudaError_t unpack_f64(const w32* planes, double* out, size_t n, cudaStream_t st) const override {
+    const size_t units = (n + 31) / 32;
+    if (!units) return cudaSuccess;
+    const bool al = (reinterpret_cast<uintptr_t>(out) & 15) == 0;
+    return run(fmt_expr("bfpg::k_unpack_f64<%s>", -1), units, st, {&planes, &out, &n, &units, &al});
   }
   cudaError_t arith_f32(int op, const float* x, const float* y, const float* c, float* z, size_t n,
                         cudaStream_t st) const override {
@@ -175,7 +187,8 @@ class JitFormat final : public Impl {
 
  private:
   int N() const { return int(1 + e_ + s_); }
-  int enc_bytes() const { return N() <= 8 ? 1 : N() <= 16 ? 2 : N() <= 32 ? 4 : 0; }
+  int enc_bytes() const { return N() <= 8 ? 1 : N() <= 16 ? 2 : N() <= 32 ? 4 : 8; }
+  int raw() const { return (N() + 7) / 8; }
   std::string fmt_expr(const char* pat, int op) const {
     char f[96], out[192];
     std::snprintf(f, sizeof f, "bfpg::Format<%u, %u, %s, %s>", e_, s_, rn_ ? "true" : "false",

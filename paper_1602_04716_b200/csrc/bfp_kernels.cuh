@@ -359,32 +359,24 @@ __device__ __forceinline__ void warp_store_elems(uint8_t* __restrict__ dst, size
   __syncwarp();
 }
 
-// Raw encodings (EB = 1/2/4 bytes each) -> planes.  Every unit of every
-// block is written; elements >= n are zero (pack.hpp:50).
+// Raw encodings / .bfpraw records (EB bytes each: 1, 2, 4, 8 = the device
+// encoding widths; 3, 5, 6, 7 = .bfpraw strides) -> planes.  Every unit of
+// every block is written; elements >= n are zero (pack.hpp:50).
 template <int N, int EB>
 __global__ void __launch_bounds__(kThreads) k_pack_enc(const uint8_t* __restrict__ enc,
                                                        w32* __restrict__ planes, size_t n,
                                                        size_t units, bool aligned) {
   pdl_enter();
+  constexpr int PW = EB > 4 ? 64 : 32;
   __shared__ __align__(16) w32 tiles[kThreads / 32][256 * EB];
   const int lane = threadIdx.x & 31;
   w32* tile = tiles[threadIdx.x >> 5];
   const size_t stride = size_t(gridDim.x) * kThreads;
   for (size_t u = size_t(blockIdx.x) * kThreads + threadIdx.x; u < units; u += stride) {
-    w32 L[32 * EB / 4];
+    w32 L[8 * EB];
     warp_load_elems<EB>(enc, u, n, aligned, tile, lane, L);
-    w32 P[32];
-    if constexpr (EB == 1) {
-      enc8_to_planes(L, P);
-    } else if constexpr (EB == 2) {
-      enc16_to_planes(L, P);
-    } else if constexpr (EB == 3) {
-      bytes24_to_enc32(L, P);
-      enc32_to_planes(P);
-    } else {
-      BFP_UNROLL for (int i = 0; i < 32; ++i) P[i] = L[i];
-      enc32_to_planes(P);
-    }
+    w32 P[PW];
+    elems_to_planes<EB>(L, P);
     const size_t base = (u >> 5) * (size_t(N) * 32) + (u & 31);
     BFP_UNROLL for (int j = 0; j < N; ++j) st_stream(planes + base + j * 32, P[j]);
   }
@@ -395,6 +387,7 @@ __global__ void __launch_bounds__(kThreads) k_unpack_enc(const w32* __restrict__
                                                          uint8_t* __restrict__ enc, size_t n,
                                                          size_t units, bool aligned) {
   pdl_enter();
+  constexpr int PW = EB > 4 ? 64 : 32;
   __shared__ __align__(16) w32 tiles[kThreads / 32][256 * EB];
   const int lane = threadIdx.x & 31;
   w32* tile = tiles[threadIdx.x >> 5];
@@ -402,20 +395,10 @@ __global__ void __launch_bounds__(kThreads) k_unpack_enc(const w32* __restrict__
   const size_t wunits = (units + 31) & ~size_t(31);  // whole warps (planes exist)
   for (size_t u = size_t(blockIdx.x) * kThreads + threadIdx.x; u < wunits; u += stride) {
     const size_t base = (u >> 5) * (size_t(N) * 32) + (u & 31);
-    w32 P[32];
-    BFP_UNROLL for (int j = 0; j < 32; ++j) P[j] = (j < N) ? ld_stream(planes + base + j * 32) : 0u;
-    w32 L[32 * EB / 4];
-    if constexpr (EB == 1) {
-      planes_to_enc8(P, L);
-    } else if constexpr (EB == 2) {
-      planes_to_enc16(P, L);
-    } else if constexpr (EB == 3) {
-      planes_to_enc32(P);
-      enc32_to_bytes24(P, L);
-    } else {
-      planes_to_enc32(P);
-      BFP_UNROLL for (int i = 0; i < 32; ++i) L[i] = P[i];
-    }
+    w32 P[PW];
+    BFP_UNROLL for (int j = 0; j < PW; ++j) P[j] = (j < N) ? ld_stream(planes + base + j * 32) : 0u;
+    w32 L[8 * EB];
+    planes_to_elems<EB>(P, L);
     warp_store_elems<EB>(enc, u, n, aligned, tile, lane, L);
   }
 }
@@ -529,6 +512,62 @@ __global__ void __launch_bounds__(kThreads) k_unpack_f32(const w32* __restrict__
   }
 }
 
+// binary64 -> encode_scalar -> planes (format.hpp:125-188, the reference
+// converter's own input type), any legal format.
+template <class F>
+__global__ void __launch_bounds__(kThreads) k_pack_f64(const double* __restrict__ in,
+                                                       w32* __restrict__ planes, size_t n,
+                                                       size_t units, bool aligned) {
+  pdl_enter();
+  constexpr int N = F::N;
+  __shared__ __align__(16) w32 tiles[kThreads / 32][2048];
+  const int lane = threadIdx.x & 31;
+  w32* tile = tiles[threadIdx.x >> 5];
+  const size_t stride = size_t(gridDim.x) * kThreads;
+  const uint8_t* inb = reinterpret_cast<const uint8_t*>(in);
+  for (size_t u = size_t(blockIdx.x) * kThreads + threadIdx.x; u < units; u += stride) {
+    w32 L[64];
+    warp_load_elems<8>(inb, u, n, aligned, tile, lane, L);  // zero past n -> +0 -> 0
+    BFP_UNROLL for (int k = 0; k < 32; ++k) {
+      const uint64_t e = encode_f64<F>(uint64_t(L[2 * k]) | (uint64_t(L[2 * k + 1]) << 32));
+      L[2 * k] = w32(e);
+      L[2 * k + 1] = w32(e >> 32);
+    }
+    w32 P[64];
+    elems_to_planes<8>(L, P);
+    const size_t base = (u >> 5) * (size_t(N) * 32) + (u & 31);
+    BFP_UNROLL for (int j = 0; j < N; ++j) st_stream(planes + base + j * 32, P[j]);
+  }
+}
+
+// planes -> decode_scalar -> binary64 (exact).
+template <class F>
+__global__ void __launch_bounds__(kThreads) k_unpack_f64(const w32* __restrict__ planes,
+                                                         double* __restrict__ out, size_t n,
+                                                         size_t units, bool aligned) {
+  pdl_enter();
+  constexpr int N = F::N;
+  __shared__ __align__(16) w32 tiles[kThreads / 32][2048];
+  const int lane = threadIdx.x & 31;
+  w32* tile = tiles[threadIdx.x >> 5];
+  const size_t stride = size_t(gridDim.x) * kThreads;
+  uint8_t* outb = reinterpret_cast<uint8_t*>(out);
+  const size_t wunits = (units + 31) & ~size_t(31);
+  for (size_t u = size_t(blockIdx.x) * kThreads + threadIdx.x; u < wunits; u += stride) {
+    const size_t base = (u >> 5) * (size_t(N) * 32) + (u & 31);
+    w32 P[64];
+    BFP_UNROLL for (int j = 0; j < 64; ++j) P[j] = (j < N) ? ld_stream(planes + base + j * 32) : 0u;
+    w32 L[64];
+    planes_to_elems<8>(P, L);
+    BFP_UNROLL for (int k = 0; k < 32; ++k) {
+      const uint64_t d = decode_f64<F>(uint64_t(L[2 * k]) | (uint64_t(L[2 * k + 1]) << 32));
+      L[2 * k] = w32(d);
+      L[2 * k + 1] = w32(d >> 32);
+    }
+    warp_store_elems<8>(outb, u, n, aligned, tile, lane, L);
+  }
+}
+
 // Fused float32-in / float32-out arithmetic: the
 // operands are converted to planes in registers, the network runs, the
 // result is converted back -- the bitslice intermediate never reaches HBM
@@ -637,13 +676,16 @@ struct Impl {
   virtual cudaError_t unpack_enc(const w32* planes, void* enc, size_t n, cudaStream_t st) const = 0;
   virtual cudaError_t pack_f32(const float* in, w32* planes, size_t n, cudaStream_t st) const = 0;
   virtual cudaError_t unpack_f32(const w32* planes, float* out, size_t n, cudaStream_t st) const = 0;
-  // .bfpraw records with a 3-byte stride (17..24-bit formats; strides 1/2/4
-  // are the pack_enc/unpack_enc byte layouts); cudaErrorNotSupported otherwise
-  virtual cudaError_t pack_raw3(const void* bytes, w32* planes, size_t n, cudaStream_t st) const = 0;
-  virtual cudaError_t unpack_raw3(const w32* planes, void* bytes, size_t n, cudaStream_t st) const = 0;
+  // .bfpraw records (stride ceil(N/8) bytes; equal to pack_enc/unpack_enc when
+  // the stride is the device encoding width 1/2/4/8)
+  virtual cudaError_t pack_raw(const void* bytes, w32* planes, size_t n, cudaStream_t st) const = 0;
+  virtual cudaError_t unpack_raw(const w32* planes, void* bytes, size_t n, cudaStream_t st) const = 0;
   // fused float32-in / float32-out arithmetic
   virtual cudaError_t arith_f32(int op, const float* x, const float* y, const float* c, float* z,
                                 size_t n, cudaStream_t st) const = 0;
+  // binary64 codec (encode_scalar / decode_scalar), any legal format
+  virtual cudaError_t pack_f64(const double* in, w32* planes, size_t n, cudaStream_t st) const = 0;
+  virtual cudaError_t unpack_f64(const w32* planes, double* out, size_t n, cudaStream_t st) const = 0;
   virtual const void* kernel(int id) const = 0;  // device function handle (attribute queries)
   virtual bool compiled() const { return true; }
 };
@@ -651,7 +693,8 @@ struct Impl {
 template <class F>
 struct FormatImpl {
   static constexpr int N = F::N;
-  static constexpr int EB = N <= 8 ? 1 : (N <= 16 ? 2 : 4);
+  static constexpr int EB = N <= 8 ? 1 : (N <= 16 ? 2 : (N <= 32 ? 4 : 8));
+  static constexpr int RAW = (N + 7) / 8;  // .bfpraw stride
 
   template <int OP>
   static cudaError_t launch_arith(const w32* x, const w32* y, const w32* c, w32* z, size_t units,
@@ -745,31 +788,47 @@ struct FormatImpl {
       return launch(k, grid_for(wave, units), st, planes, out, n, units, al);
     }
   }
-  static cudaError_t pack_raw3(const void* bytes, w32* planes, size_t n, cudaStream_t st) {
-    if constexpr (N <= 16 || N > 24) {
-      return cudaErrorNotSupported;
+  static cudaError_t pack_raw(const void* bytes, w32* planes, size_t n, cudaStream_t st) {
+    if constexpr (RAW == EB) {
+      return pack_enc(bytes, planes, n, st);
     } else {
       const size_t units = units_for(n);
       if (!units) return cudaSuccess;
       const bool al = (reinterpret_cast<uintptr_t>(bytes) & 15) == 0;
-      auto k = k_pack_enc<N, 3>;
+      auto k = k_pack_enc<N, RAW>;
       static const int wave = wave_ctas(k);
       return launch(k, grid_for(wave, units), st, static_cast<const uint8_t*>(bytes), planes, n,
                     units, al);
     }
   }
-  static cudaError_t unpack_raw3(const w32* planes, void* bytes, size_t n, cudaStream_t st) {
-    if constexpr (N <= 16 || N > 24) {
-      return cudaErrorNotSupported;
+  static cudaError_t unpack_raw(const w32* planes, void* bytes, size_t n, cudaStream_t st) {
+    if constexpr (RAW == EB) {
+      return unpack_enc(planes, bytes, n, st);
     } else {
       const size_t units = (n + 31) / 32;
       if (!units) return cudaSuccess;
       const bool al = (reinterpret_cast<uintptr_t>(bytes) & 15) == 0;
-      auto k = k_unpack_enc<N, 3>;
+      auto k = k_unpack_enc<N, RAW>;
       static const int wave = wave_ctas(k);
       return launch(k, grid_for(wave, units), st, planes, static_cast<uint8_t*>(bytes), n, units,
                     al);
     }
+  }
+  static cudaError_t pack_f64(const double* in, w32* planes, size_t n, cudaStream_t st) {
+    const size_t units = units_for(n);
+    if (!units) return cudaSuccess;
+    const bool al = (reinterpret_cast<uintptr_t>(in) & 15) == 0;
+    auto k = k_pack_f64<F>;
+    static const int wave = wave_ctas(k);
+    return launch(k, grid_for(wave, units), st, in, planes, n, units, al);
+  }
+  static cudaError_t unpack_f64(const w32* planes, double* out, size_t n, cudaStream_t st) {
+    const size_t units = (n + 31) / 32;
+    if (!units) return cudaSuccess;
+    const bool al = (reinterpret_cast<uintptr_t>(out) & 15) == 0;
+    auto k = k_unpack_f64<F>;
+    static const int wave = wave_ctas(k);
+    return launch(k, grid_for(wave, units), st, planes, out, n, units, al);
   }
   template <int OP>
   static cudaError_t launch_arith_f32(const float* x, const float* y, const float* c, float* z,
@@ -815,15 +874,21 @@ struct FormatImpl {
     cudaError_t unpack_f32(const w32* p, float* o, size_t n, cudaStream_t st) const override {
       return FormatImpl::unpack_f32(p, o, n, st);
     }
-    cudaError_t pack_raw3(const void* b, w32* p, size_t n, cudaStream_t st) const override {
-      return FormatImpl::pack_raw3(b, p, n, st);
+    cudaError_t pack_raw(const void* b, w32* p, size_t n, cudaStream_t st) const override {
+      return FormatImpl::pack_raw(b, p, n, st);
     }
-    cudaError_t unpack_raw3(const w32* p, void* b, size_t n, cudaStream_t st) const override {
-      return FormatImpl::unpack_raw3(p, b, n, st);
+    cudaError_t unpack_raw(const w32* p, void* b, size_t n, cudaStream_t st) const override {
+      return FormatImpl::unpack_raw(p, b, n, st);
     }
     cudaError_t arith_f32(int op, const float* x, const float* y, const float* c, float* z,
                           size_t n, cudaStream_t st) const override {
       return FormatImpl::arith_f32(op, x, y, c, z, n, st);
+    }
+    cudaError_t pack_f64(const double* i, w32* p, size_t n, cudaStream_t st) const override {
+      return FormatImpl::pack_f64(i, p, n, st);
+    }
+    cudaError_t unpack_f64(const w32* p, double* o, size_t n, cudaStream_t st) const override {
+      return FormatImpl::unpack_f64(p, o, n, st);
     }
     const void* kernel(int id) const override { return FormatImpl::kernel(id); }
   };

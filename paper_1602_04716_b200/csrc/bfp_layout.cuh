@@ -158,9 +158,93 @@ BFP_HD void enc32_to_bytes24(const w32* V, w32* L) {
   }
 }
 
+// .bfpraw records of any stride (pack.hpp:78-109): 32 records = 32*ST bytes =
+// 8*ST words (little-endian) <-> 32 encodings as (lo, hi) 32-bit halves.
+template <int ST>
+BFP_HD void bytes_to_enc(const w32* L, w32* lo, w32* hi) {
+  constexpr int NW = 8 * ST;
+  BFP_UNROLL for (int k = 0; k < 32; ++k) {
+    BFP_UNROLL for (int part = 0; part < (ST > 4 ? 2 : 1); ++part) {
+      const int b = ST * k + 4 * part;  // first byte of this 32-bit half
+      const int nbytes = (ST - 4 * part) < 4 ? (ST - 4 * part) : 4;
+      const int w = b >> 2, off = b & 3;
+      const w32 sel = w32(off) | (w32(off + 1) << 4) | (w32(off + 2) << 8) | (w32(off + 3) << 12);
+      w32 v = prmt(L[w], (w + 1 < NW) ? L[w + 1] : 0u, sel);
+      if (nbytes < 4) v &= (1u << (8 * nbytes)) - 1u;
+      if (part == 0) lo[k] = v;
+      else hi[k] = v;
+    }
+  }
+}
+
+template <int ST>
+BFP_HD void enc_to_bytes(const w32* lo, const w32* hi, w32* L) {
+  constexpr int NW = 8 * ST;
+  BFP_UNROLL for (int i = 0; i < NW; ++i) {
+    // bytes 4i..4i+3: byte b belongs to record b / ST, byte (b % ST) of it
+    const int r0 = (4 * i) / ST;
+    w32 v = 0;
+    BFP_UNROLL for (int t = 0; t < 4; ++t) {
+      const int b = 4 * i + t, r = b / ST, byte = b % ST;
+      const w32 src = (byte < 4) ? lo[r] : hi[r];
+      v |= ((src >> (8 * (byte & 3))) & 0xffu) << (8 * t);
+    }
+    (void)r0;
+    L[i] = v;
+  }
+}
+
 // 32 encodings of <= 32 bits, one per word -> planes (in place).
 BFP_HD void enc32_to_planes(w32* v) { xpose32(v); }
 BFP_HD void planes_to_enc32(w32* v) { xpose32(v); }
+
+// One unit's element side (8*EB words: EB = 1, 2, 4, 8 device encoding widths,
+// 3, 5, 6, 7 .bfpraw strides) <-> its planes (32 words, 64 when EB > 4).
+template <int EB>
+BFP_HD void elems_to_planes(const w32* L, w32* P /*32 or 64*/) {
+  if constexpr (EB == 1) {
+    enc8_to_planes(L, P);
+  } else if constexpr (EB == 2) {
+    enc16_to_planes(L, P);
+  } else if constexpr (EB == 4) {
+    BFP_UNROLL for (int i = 0; i < 32; ++i) P[i] = L[i];
+    enc32_to_planes(P);
+  } else if constexpr (EB == 8) {
+    BFP_UNROLL for (int k = 0; k < 32; ++k) {
+      P[k] = L[2 * k];
+      P[32 + k] = L[2 * k + 1];
+    }
+    enc32_to_planes(P);
+    enc32_to_planes(P + 32);
+  } else {
+    bytes_to_enc<EB>(L, P, P + 32);
+    enc32_to_planes(P);
+    if constexpr (EB > 4) enc32_to_planes(P + 32);
+  }
+}
+
+template <int EB>
+BFP_HD void planes_to_elems(w32* P /*32 or 64, rows >= N zero*/, w32* L) {
+  if constexpr (EB == 1) {
+    planes_to_enc8(P, L);
+  } else if constexpr (EB == 2) {
+    planes_to_enc16(P, L);
+  } else if constexpr (EB == 4) {
+    planes_to_enc32(P);
+    BFP_UNROLL for (int i = 0; i < 32; ++i) L[i] = P[i];
+  } else if constexpr (EB == 8) {
+    planes_to_enc32(P);
+    planes_to_enc32(P + 32);
+    BFP_UNROLL for (int k = 0; k < 32; ++k) {
+      L[2 * k] = P[k];
+      L[2 * k + 1] = P[32 + k];
+    }
+  } else {
+    planes_to_enc32(P);
+    if constexpr (EB > 4) planes_to_enc32(P + 32);
+    enc_to_bytes<EB>(P, P + 32, L);
+  }
+}
 
 // ------------------------------------------------------------- codec
 // encode_scalar((double)f) for a binary32 input f (format.hpp:125-188):
@@ -324,6 +408,79 @@ BFP_HD w32 decode_f32_fast(w32 enc) {
   r = (be == EMASK) ? 0x7f800000u : r;
   r |= ((enc >> (E + S)) & 1u) << 31;
   return (be == EMASK && (mag & ((1u << S) - 1u))) ? 0x7fc00000u : r;
+}
+
+// ------------------------------------------------------ binary64 codec
+// encode_scalar(double) / decode_scalar -> double, format.hpp:101-188, for
+// any legal format (n <= 64): the reference converter restated on 64-bit
+// integers (decode is exact: every finite value of a legal format is a
+// binary64 value).
+BFP_HD int clz64(uint64_t v) {
+#if defined(__CUDA_ARCH__)
+  return __clzll(static_cast<long long>(v));
+#else
+  return v ? __builtin_clzll(v) : 64;
+#endif
+}
+
+template <class F>
+BFP_HD uint64_t encode_f64(uint64_t bits) {
+  constexpr int E = F::E, S = F::S;
+  constexpr int EMIN = 1 - F::BIAS, EMAX = F::BIAS;
+  constexpr uint64_t EMASK = (uint64_t(1) << E) - 1;
+  constexpr uint64_t FMASK = (uint64_t(1) << S) - 1;
+  const uint64_t sign = (bits >> 63) << (E + S);
+  const uint64_t e64 = (bits >> 52) & 0x7ff, f64 = bits & ((uint64_t(1) << 52) - 1);
+  if (e64 == 0x7ff) return f64 ? ((EMASK << S) | (uint64_t(1) << (S - 1))) : (sign | (EMASK << S));
+  if (e64 == 0 && f64 == 0) return sign;
+  const uint64_t sig = e64 ? ((uint64_t(1) << 52) | f64) : f64;
+  const int exp2 = e64 ? int(e64) - 1075 : -1074;
+  const int unb = exp2 + (63 - clz64(sig));
+  const int ulp_exp = (unb >= EMIN ? unb : EMIN) - S;
+  const int shift = ulp_exp - exp2;
+  uint64_t kept;
+  bool guard = false, sticky = false;
+  if (shift <= 0) {
+    kept = sig << (-shift);
+  } else if (shift > 64) {
+    kept = 0;
+    sticky = true;
+  } else {
+    kept = shift == 64 ? 0 : (sig >> shift);
+    guard = (sig >> (shift - 1)) & 1u;
+    if (shift > 1) sticky = (sig & ((uint64_t(1) << (shift - 1)) - 1)) != 0;
+  }
+  if (F::RN && guard && (sticky || (kept & 1u))) ++kept;
+  int res_exp = ulp_exp + S;
+  if (S < 63 && kept >= (uint64_t(2) << S)) {
+    kept >>= 1;
+    ++res_exp;
+  }
+  if (kept == 0) return sign;
+  if (kept < (uint64_t(1) << S)) return F::FTZ ? sign : (sign | kept);
+  if (res_exp > EMAX) return F::RN ? (sign | (EMASK << S)) : (sign | ((EMASK - 1) << S) | FMASK);
+  return sign | (uint64_t(res_exp + F::BIAS) << S) | (kept & FMASK);
+}
+
+template <class F>
+BFP_HD uint64_t decode_f64(uint64_t enc) {
+  constexpr int E = F::E, S = F::S;
+  constexpr int EMIN = 1 - F::BIAS;
+  constexpr uint64_t EMASK = (uint64_t(1) << E) - 1;
+  constexpr uint64_t FMASK = (uint64_t(1) << S) - 1;
+  const uint64_t sign = ((enc >> (E + S)) & 1u) << 63;
+  const uint64_t be = (enc >> S) & EMASK, fr = enc & FMASK;
+  if (be == EMASK) return fr ? 0x7ff8000000000000ull : (sign | 0x7ff0000000000000ull);
+  if (be == 0) {
+    if (fr == 0) return sign;
+    const int p = 63 - clz64(fr);
+    const int dexp = p + EMIN - S;  // unbiased exponent of the leading bit
+    if constexpr (EMIN - S < -1022) {  // binary64 subnormals occur (e = 11 formats)
+      if (dexp < -1022) return sign | (fr << (EMIN - S + 1074));
+    }
+    return sign | (uint64_t(dexp + 1023) << 52) | ((fr << (52 - p)) & ((uint64_t(1) << 52) - 1));
+  }
+  return sign | (uint64_t(int(be) - F::BIAS + 1023) << 52) | (fr << (52 - S));
 }
 
 // Canonical NaN in the bitslice domain: every element whose exponent planes

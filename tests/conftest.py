@@ -74,6 +74,7 @@ class HostCircuits:
         vp = C.c_void_p
         L.host_binop.argtypes = [C.c_int, C.c_uint, C.c_uint, C.c_int, C.c_int, vp, vp, vp, vp, C.c_size_t]
         L.host_codec.argtypes = [C.c_int, C.c_uint, C.c_uint, C.c_int, C.c_int, vp, vp, C.c_size_t]
+        L.host_codec64.argtypes = [C.c_int, C.c_uint, C.c_uint, C.c_int, C.c_int, vp, vp, C.c_size_t]
         L.host_pack_enc.argtypes = [C.c_int, C.c_uint, vp, C.c_size_t, vp]
         L.host_unpack_enc.argtypes = [C.c_int, C.c_uint, vp, C.c_size_t, vp]
         self.L = L
@@ -96,16 +97,26 @@ class HostCircuits:
         assert rc == 0
         return out
 
+    def codec64(self, direction: int, fmt, vals: np.ndarray) -> np.ndarray:
+        vals = np.ascontiguousarray(vals, dtype=np.uint64)
+        out = np.zeros_like(vals)
+        assert self.L.host_codec64(direction, fmt[0], fmt[1], fmt[2], fmt[3], vals.ctypes.data,
+                                   out.ctypes.data, len(vals)) == 0
+        return out
+
     def pack_enc(self, eb: int, nbits: int, enc: np.ndarray) -> np.ndarray:
-        enc = np.ascontiguousarray(enc.astype({1: np.uint8, 2: np.uint16, 4: np.uint32}[eb]))
+        """eb-byte little-endian records (eb = 1..8) -> planes."""
+        raw = np.ascontiguousarray(enc.astype(np.uint64)).view(np.uint8).reshape(-1, 8)[:, :eb].copy()
         planes = np.zeros(O.nblocks(len(enc)) * nbits * 32, dtype=np.uint32)
-        self.L.host_pack_enc(eb, nbits, enc.ctypes.data, len(enc), planes.ctypes.data)
+        self.L.host_pack_enc(eb, nbits, raw.ctypes.data, len(enc), planes.ctypes.data)
         return planes
 
     def unpack_enc(self, eb: int, nbits: int, planes: np.ndarray, n: int) -> np.ndarray:
-        out = np.zeros(n, dtype={1: np.uint8, 2: np.uint16, 4: np.uint32}[eb])
-        self.L.host_unpack_enc(eb, nbits, np.ascontiguousarray(planes).ctypes.data, n, out.ctypes.data)
-        return out.astype(np.uint64)
+        raw = np.zeros((n, 8), dtype=np.uint8)
+        buf = np.zeros(n * eb, dtype=np.uint8)
+        self.L.host_unpack_enc(eb, nbits, np.ascontiguousarray(planes).ctypes.data, n, buf.ctypes.data)
+        raw[:, :eb] = buf.reshape(n, eb)
+        return raw.view(np.uint64).reshape(n)
 
 
 @pytest.fixture(scope="session")

@@ -96,45 +96,66 @@ extern "C" int host_codec(int dir, unsigned e, unsigned s, int rn, int ftz, cons
   return dispatch(e, s, rn, ftz, [&](auto f) { codec<decltype(f)>(dir, in, out, n); });
 }
 
-// Encodings (width eb = 1/2/4 bytes) <-> planes of nbits planes, through the
-// same register transposes the kernels use.  n elements, tail zero-filled.
-extern "C" int host_pack_enc(int eb, unsigned nbits, const uint8_t* enc, size_t n,
-                             uint32_t* planes) {
+// Encodings / .bfpraw records (eb = 1..8 bytes each) <-> planes of nbits
+// planes, through the same register transposes the kernels use (tail zero).
+template <int EB>
+static void pack_t(unsigned nbits, const uint8_t* enc, size_t n, uint32_t* planes) {
   const size_t blocks = (n + 1023) / 1024;
   for (size_t u = 0; u < blocks * 32; ++u) {
-    w32 L[32] = {0};
-    for (int k = 0; k < 32; ++k) {
-      const size_t i = u * 32 + k;
-      if (i >= n) break;
-      w32 v = 0;
-      std::memcpy(&v, enc + i * eb, eb);
-      L[(k * eb) / 4] |= (eb == 4) ? v : (v << ((k * eb * 8) & 31));
+    w32 L[8 * EB] = {0};
+    for (int b = 0; b < 32 * EB; ++b) {
+      const size_t i = u * 32 + size_t(b / EB);
+      if (i < n) L[b >> 2] |= w32(enc[u * 32 * EB + b]) << (8 * (b & 3));
     }
-    w32 P[32];
-    if (eb == 1) enc8_to_planes(L, P);
-    else if (eb == 2) enc16_to_planes(L, P);
-    else { std::memcpy(P, L, sizeof P); enc32_to_planes(P); }
+    w32 P[EB > 4 ? 64 : 32];
+    elems_to_planes<EB>(L, P);
     for (unsigned j = 0; j < nbits; ++j) planes[((u >> 5) * nbits + j) * 32 + (u & 31)] = P[j];
+  }
+}
+
+template <int EB>
+static void unpack_t(unsigned nbits, const uint32_t* planes, size_t n, uint8_t* enc) {
+  const size_t units = (n + 31) / 32;
+  for (size_t u = 0; u < units; ++u) {
+    w32 P[EB > 4 ? 64 : 32] = {0};
+    for (unsigned j = 0; j < nbits; ++j) P[j] = planes[((u >> 5) * nbits + j) * 32 + (u & 31)];
+    w32 L[8 * EB];
+    planes_to_elems<EB>(P, L);
+    for (int b = 0; b < 32 * EB; ++b) {
+      const size_t i = u * 32 + size_t(b / EB);
+      if (i < n) enc[u * 32 * EB + b] = uint8_t(L[b >> 2] >> (8 * (b & 3)));
+    }
+  }
+}
+
+extern "C" int host_pack_enc(int eb, unsigned nbits, const uint8_t* enc, size_t n,
+                             uint32_t* planes) {
+  switch (eb) {
+    case 1: pack_t<1>(nbits, enc, n, planes); break;
+    case 2: pack_t<2>(nbits, enc, n, planes); break;
+    case 3: pack_t<3>(nbits, enc, n, planes); break;
+    case 4: pack_t<4>(nbits, enc, n, planes); break;
+    case 5: pack_t<5>(nbits, enc, n, planes); break;
+    case 6: pack_t<6>(nbits, enc, n, planes); break;
+    case 7: pack_t<7>(nbits, enc, n, planes); break;
+    case 8: pack_t<8>(nbits, enc, n, planes); break;
+    default: return 1;
   }
   return 0;
 }
 
 extern "C" int host_unpack_enc(int eb, unsigned nbits, const uint32_t* planes, size_t n,
                                uint8_t* enc) {
-  const size_t units = (n + 31) / 32;
-  for (size_t u = 0; u < units; ++u) {
-    w32 P[32] = {0};
-    for (unsigned j = 0; j < nbits; ++j) P[j] = planes[((u >> 5) * nbits + j) * 32 + (u & 31)];
-    w32 L[32];
-    if (eb == 1) planes_to_enc8(P, L);
-    else if (eb == 2) planes_to_enc16(P, L);
-    else { planes_to_enc32(P); std::memcpy(L, P, sizeof L); }
-    for (int k = 0; k < 32; ++k) {
-      const size_t i = u * 32 + k;
-      if (i >= n) break;
-      const w32 v = (eb == 4) ? L[k] : (L[(k * eb) / 4] >> ((k * eb * 8) & 31));
-      std::memcpy(enc + i * eb, &v, eb);
-    }
+  switch (eb) {
+    case 1: unpack_t<1>(nbits, planes, n, enc); break;
+    case 2: unpack_t<2>(nbits, planes, n, enc); break;
+    case 3: unpack_t<3>(nbits, planes, n, enc); break;
+    case 4: unpack_t<4>(nbits, planes, n, enc); break;
+    case 5: unpack_t<5>(nbits, planes, n, enc); break;
+    case 6: unpack_t<6>(nbits, planes, n, enc); break;
+    case 7: unpack_t<7>(nbits, planes, n, enc); break;
+    case 8: unpack_t<8>(nbits, planes, n, enc); break;
+    default: return 1;
   }
   return 0;
 }
@@ -148,4 +169,21 @@ extern "C" int host_raw3(const uint8_t* bytes96, uint32_t* enc32, uint8_t* back9
   enc32_to_bytes24(V, B);
   std::memcpy(back96, B, 96);
   return 0;
+}
+
+// binary64 codec (encode_f64 / decode_f64) on u64 bit patterns: dir 0 encode,
+// 1 decode; the listed formats plus a few wide ones (n up to 64).
+template <class F>
+static void codec64(int dir, const uint64_t* in, uint64_t* out, size_t n) {
+  for (size_t i = 0; i < n; ++i) out[i] = dir == 0 ? encode_f64<F>(in[i]) : decode_f64<F>(in[i]);
+}
+
+extern "C" int host_codec64(int dir, unsigned e, unsigned s, int rn, int ftz, const uint64_t* in,
+                            uint64_t* out, size_t n) {
+  auto fn = [&](auto f) { codec64<decltype(f)>(dir, in, out, n); };
+  if (e == 11 && s == 52) { with_fmt<11, 52>(rn, ftz, fn); return 0; }
+  if (e == 10 && s == 40) { with_fmt<10, 40>(rn, ftz, fn); return 0; }
+  if (e == 11 && s == 20) { with_fmt<11, 20>(rn, ftz, fn); return 0; }
+  if (e == 2 && s == 1) { with_fmt<2, 1>(rn, ftz, fn); return 0; }
+  return dispatch(e, s, rn, ftz, fn);
 }

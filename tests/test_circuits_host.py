@@ -105,7 +105,8 @@ def test_codec_host(oracle, host, fmt2):
 
 
 # ---------------------------------------------------------------------- layout
-@pytest.mark.parametrize("eb,nb", [(1, 6), (1, 8), (2, 9), (2, 16), (4, 24), (4, 32)])
+@pytest.mark.parametrize("eb,nb", [(1, 6), (1, 8), (2, 9), (2, 16), (3, 24), (4, 24), (4, 32),
+                                   (5, 40), (6, 41), (7, 56), (8, 33), (8, 64)])
 def test_transpose_host(oracle, host, eb, nb):
     rng = np.random.default_rng(nb)
     for n in (1, 33, 1024, 2500):
@@ -138,3 +139,33 @@ def test_bfpraw_stride3_host(host):
         want = want[:, 0] | (want[:, 1] << 8) | (want[:, 2] << 16)
         assert np.array_equal(enc, want)
         assert np.array_equal(back, raw)
+
+
+@pytest.mark.parametrize("fmt2", FORMATS + [(11, 52), (10, 40), (11, 20), (2, 1)])
+def test_codec64_host(oracle, ref_oracle, host, fmt2):
+    """encode_scalar(double) / decode_scalar (format.hpp:101-188) for any legal
+    format, against the C restatement and (sampled) the reference itself."""
+    e, s = fmt2
+    rng = np.random.default_rng(e * 1000 + s)
+    bits = rng.integers(0, 1 << 63, size=1 << 15, dtype=np.uint64) * np.uint64(2) + \
+        rng.integers(0, 2, size=1 << 15, dtype=np.uint64)
+    ex = rng.integers(1023 - 1100, 1023 + 1100, size=1 << 14).clip(0, 2047).astype(np.uint64)
+    bits[: 1 << 14] = (bits[: 1 << 14] & np.uint64(0x800FFFFFFFFFFFFF)) | (ex << np.uint64(52))
+    xs = bits.view(np.float64)
+    for mode in MODES:
+        fmt = fmt2 + mode
+        want = oracle.encode_f64(fmt, xs)
+        assert np.array_equal(host.codec64(0, fmt, bits), want), fmt
+        R = ref_oracle.ref()
+        for v in xs[:200]:
+            assert R.ref_encode_f64(float(v), e, s, mode[0], mode[1]) == oracle.orc().orc_encode(
+                float(v), e, s, mode[0], mode[1])
+    nb = 1 + e + s
+    encs = rng.integers(0, 1 << min(nb, 63), size=1 << 14, dtype=np.uint64)
+    if nb == 64:
+        encs = encs * np.uint64(2) + rng.integers(0, 2, size=len(encs), dtype=np.uint64)
+    got = host.codec64(1, fmt2 + (1, 0), encs)
+    want = oracle.decode_f64(fmt2 + (1, 0), encs).view(np.uint64)
+    nan = np.isnan(want.view(np.float64))
+    assert np.array_equal(got[~nan], want[~nan])
+    assert np.all(got[nan] == np.uint64(0x7FF8000000000000))  # quiet_NaN()

@@ -80,10 +80,65 @@ def test_jit_codec(oracle, fmt2):
         assert np.array_equal(back, oracle.decode_f32(fmt2 + mode, want).view(np.uint32))
 
 
-def test_jit_unsupported_layout():
-    """Encodings wider than 32 bits have no device layout kernel: EUNSUPPORTED."""
+def test_jit_unsupported_f32_codec():
+    """float32 conversion needs e <= 8, s <= 23: EUNSUPPORTED beyond (binary64 works)."""
     L = _lib.lib()
     f = _lib.BfpFormat(10, 40, 1, 0, b"")
-    t = torch.zeros(1 << 16, dtype=torch.int64, device="cuda")
+    t = torch.zeros(1 << 16, dtype=torch.float32, device="cuda")
     p = torch.zeros(1 << 16, dtype=torch.int32, device="cuda")
-    assert L.bfp_pack_enc(C.byref(f), t.data_ptr(), p.data_ptr(), 100, None) == _lib.BFP_EUNSUPPORTED
+    assert L.bfp_pack_f32(C.byref(f), t.data_ptr(), p.data_ptr(), 100, None) == _lib.BFP_EUNSUPPORTED
+
+
+WIDE = [(7, 30), (9, 35), (10, 40), (11, 52), (6, 3), (8, 23)]  # n = 38, 45, 51, 64, 10, 32
+
+
+@pytest.mark.parametrize("fmt2", WIDE)
+def test_wide_layout_and_bfpraw(ref_oracle, fmt2):
+    """64-bit encodings and .bfpraw strides 5..8 through the layout kernels
+    (JIT for the uncompiled formats) against field_from_elements and the
+    reference's own to_bfpraw."""
+    O = ref_oracle
+    e, s = fmt2
+    nb = 1 + e + s
+    spec = bfp.make_spec(e, s)
+    stride = bfp.bfpraw_stride(spec)
+    rng = np.random.default_rng(nb)
+    n = 3000
+    enc = rng.integers(0, 1 << min(nb, 63), size=n, dtype=np.uint64)
+    if nb == 64:
+        enc = enc * np.uint64(2) + rng.integers(0, 2, size=n, dtype=np.uint64)
+    t = torch.from_numpy(enc.view(np.int64).copy()).cuda()
+    v = bfp.pack(t, spec)
+    assert np.array_equal(v.planes.cpu().numpy().view(np.uint32), O.pack_planes(enc, nb))
+    assert np.array_equal(bfp.to_u64(bfp.unpack(v), spec).cpu().numpy().view(np.uint64), enc)
+    raw = np.zeros(n * stride, dtype=np.uint8)
+    O.ref().ref_to_bfpraw(enc.ctypes.data_as(O._u64p), n, raw.ctypes.data_as(O._u8p), e, s)
+    vr = bfp.pack_bfpraw(torch.from_numpy(raw).cuda(), spec)
+    assert np.array_equal(vr.planes.cpu().numpy().view(np.uint32), O.pack_planes(enc, nb))
+    assert np.array_equal(bfp.unpack_bfpraw(vr).cpu().numpy(), raw)
+
+
+@pytest.mark.parametrize("fmt2", [(4, 3), (5, 10), (8, 23), (7, 30), (11, 52), (2, 1)])
+@pytest.mark.parametrize("mode", [(1, 0), (0, 1)])
+def test_pack_unpack_f64(oracle, fmt2, mode):
+    """binary64 -> encode_scalar -> planes and planes -> decode_scalar (exact
+    binary64), compiled and JIT formats, against the C restatement."""
+    e, s = fmt2
+    fmt = fmt2 + mode
+    nb = 1 + e + s
+    spec = bfp.make_spec(e, s, mode[0], mode[1])
+    rng = np.random.default_rng(nb * 7 + mode[0])
+    n = 40000 + 123
+    bits = rng.integers(0, 1 << 63, size=n, dtype=np.uint64) * np.uint64(2) + \
+        rng.integers(0, 2, size=n, dtype=np.uint64)
+    ex = rng.integers(1023 - 1100, 1023 + 1100, size=n // 2).clip(0, 2047).astype(np.uint64)
+    bits[: n // 2] = (bits[: n // 2] & np.uint64(0x800FFFFFFFFFFFFF)) | (ex << np.uint64(52))
+    xs = bits.view(np.float64)
+    v = bfp.pack_f64(torch.from_numpy(xs.copy()).cuda(), spec)
+    want = oracle.encode_f64(fmt, xs)
+    assert np.array_equal(v.planes.cpu().numpy().view(np.uint32), oracle.pack_planes(want, nb))
+    back = bfp.unpack_f64(v).cpu().numpy()
+    ref = oracle.decode_f64(fmt, want)
+    nan = np.isnan(ref)
+    assert np.array_equal(back.view(np.uint64)[~nan], ref.view(np.uint64)[~nan])
+    assert np.all(back.view(np.uint64)[nan] == np.uint64(0x7FF8000000000000))
