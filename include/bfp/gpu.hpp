@@ -149,7 +149,6 @@ inline bfp_vector pack(std::span<const encoding> encs, const format_spec& spec,
   validate(spec);
   const bfp_format f = spec.c();
   const std::size_t eb = bfp_enc_bytes(&f);
-  if (eb > 4) throw std::invalid_argument("pack: formats wider than 32 bits are not supported on the device");
   bfp_vector v(spec, encs.size());
   if (encs.empty()) return v;
   std::vector<std::uint8_t> narrow(encs.size() * eb);
@@ -197,6 +196,83 @@ inline bfp_vector pack_f32(const float* d_in, std::size_t count, const format_sp
 inline void unpack_f32(const bfp_vector& v, float* d_out, cudaStream_t stream = nullptr) {
   const bfp_format f = v.spec.c();
   detail::check(bfp_unpack_f32(&f, v.planes(), d_out, v.size(), stream), "unpack_f32");
+}
+
+// binary64 -> encode_scalar -> planes (format.hpp:125-188), device input; any
+// legal format.
+inline bfp_vector pack_f64(const double* d_in, std::size_t count, const format_spec& spec,
+                           cudaStream_t stream = nullptr) {
+  validate(spec);
+  bfp_vector v(spec, count);
+  const bfp_format f = spec.c();
+  detail::check(bfp_pack_f64(&f, d_in, v.planes(), count, stream), "pack_f64");
+  return v;
+}
+
+// planes -> decode_scalar (exact binary64) into device memory.
+inline void unpack_f64(const bfp_vector& v, double* d_out, cudaStream_t stream = nullptr) {
+  const bfp_format f = v.spec.c();
+  detail::check(bfp_unpack_f64(&f, v.planes(), d_out, v.size(), stream), "unpack_f64");
+}
+
+// .bfpraw (pack.hpp:78-109): host codec, same as the reference's ...
+inline std::size_t bfpraw_stride(const format_spec& spec) { return (spec.total_bits() + 7) / 8; }
+
+inline std::vector<std::uint8_t> to_bfpraw(std::span<const encoding> encs, const format_spec& spec) {
+  const std::size_t stride = bfpraw_stride(spec);
+  std::vector<std::uint8_t> out;
+  out.reserve(encs.size() * stride);
+  for (const encoding e : encs)
+    for (std::size_t b = 0; b < stride; ++b) out.push_back(static_cast<std::uint8_t>(e >> (8 * b)));
+  return out;
+}
+
+inline std::vector<encoding> from_bfpraw(std::span<const std::uint8_t> bytes, const format_spec& spec) {
+  const std::size_t stride = bfpraw_stride(spec);
+  if (bytes.size() % stride != 0)
+    throw std::invalid_argument("bfpraw: byte count not a multiple of the encoding stride");
+  std::vector<encoding> out(bytes.size() / stride);
+  for (std::size_t i = 0; i < out.size(); ++i) {
+    encoding e = 0;
+    for (std::size_t b = 0; b < stride; ++b) e |= static_cast<encoding>(bytes[i * stride + b]) << (8 * b);
+    out[i] = e;
+  }
+  return out;
+}
+
+// ... and straight between .bfpraw bytes and device planes.
+inline bfp_vector pack_bfpraw(std::span<const std::uint8_t> bytes, const format_spec& spec,
+                              cudaStream_t stream = nullptr) {
+  validate(spec);
+  const std::size_t stride = bfpraw_stride(spec);
+  if (bytes.size() % stride != 0)
+    throw std::invalid_argument("bfpraw: byte count not a multiple of the encoding stride");
+  bfp_vector v(spec, bytes.size() / stride);
+  if (bytes.empty()) return v;
+  void* d = nullptr;
+  detail::cuda(cudaMalloc(&d, bytes.size()), "cudaMalloc bfpraw");
+  detail::cuda(cudaMemcpyAsync(d, bytes.data(), bytes.size(), cudaMemcpyHostToDevice, stream), "H2D");
+  const bfp_format f = spec.c();
+  const bfp_status s = bfp_pack_bfpraw(&f, d, bytes.size(), v.planes(), stream);
+  cudaStreamSynchronize(stream);
+  cudaFree(d);
+  detail::check(s, "pack_bfpraw");
+  return v;
+}
+
+inline std::vector<std::uint8_t> unpack_bfpraw(const bfp_vector& v, cudaStream_t stream = nullptr) {
+  const std::size_t nb = v.size() * bfpraw_stride(v.spec);
+  std::vector<std::uint8_t> out(nb);
+  if (!nb) return out;
+  void* d = nullptr;
+  detail::cuda(cudaMalloc(&d, nb), "cudaMalloc bfpraw");
+  const bfp_format f = v.spec.c();
+  const bfp_status s = bfp_unpack_bfpraw(&f, v.planes(), v.size(), d, stream);
+  detail::cuda(cudaMemcpyAsync(out.data(), d, nb, cudaMemcpyDeviceToHost, stream), "D2H");
+  cudaStreamSynchronize(stream);
+  cudaFree(d);
+  detail::check(s, "unpack_bfpraw");
+  return out;
 }
 
 namespace detail {

@@ -36,6 +36,17 @@ int main() {
         if (g::encode_scalar(v, spec) != orc_encode(v, e, s, rn, 0)) ++fails;
     }
   }
+  // .bfpraw round trip through the device, a 51-bit format (runtime backend)
+  {
+    const auto spec = g::make_spec(10, 40);
+    std::vector<g::encoding> xs(2000);
+    for (auto& v : xs) v = rng() & ((1ull << spec.total_bits()) - 1);
+    const auto raw = g::to_bfpraw(xs, spec);
+    const g::bfp_vector v = g::pack_bfpraw(raw, spec);
+    if (g::unpack_bfpraw(v) != raw) ++fails;
+    if (g::unpack(v, xs.size()) != xs) ++fails;
+    if (g::from_bfpraw(raw, spec) != xs) ++fails;
+  }
   // error behaviour mirrors the reference: std::invalid_argument
   bool threw = false;
   try {
