@@ -74,8 +74,11 @@ __device__ __forceinline__ void eval_unit(const w32* X, const w32* Y, const w32*
 // One thread per unit, grid-stride.  (A register double-buffered variant --
 // next unit's loads issued before the current network -- measured slower on
 // the B200: the extra registers cost more occupancy than the overlap gained.)
+#ifndef BFP_ARITH_MINB
+#define BFP_ARITH_MINB 1
+#endif
 template <class F, int OP>
-__global__ void __launch_bounds__(kThreads) k_arith(const w32* __restrict__ x,
+__global__ void __launch_bounds__(kThreads, BFP_ARITH_MINB) k_arith(const w32* __restrict__ x,
                                                     const w32* __restrict__ y,
                                                     const w32* __restrict__ c,
                                                     w32* __restrict__ z, size_t units) {
