@@ -25,7 +25,7 @@ INCLUDE = PKG.parent / "include"
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-NVCC_FLAGS = ARCH + [
+NVCC_FLAGS = ARCH + os.environ.get("BFP_EXTRA_NVCC", "").split() + [
     "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
     "-Xptxas", "-v", "--expt-relaxed-constexpr", f"-I{INCLUDE}", f"-I{CSRC}",
 ]
