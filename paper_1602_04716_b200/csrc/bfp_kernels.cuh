@@ -194,22 +194,27 @@ __global__ void __launch_bounds__(kThreads) k_arith_bulk(const w32* __restrict__
       if (b < nblocks) issue(s, b);
     }
   }
-  size_t i = 0;
-  for (size_t b = gw; b < nblocks; b += tw, ++i) {
-    const int s = int(i % ST);
-    mbar_wait(bars + s, uint32_t((i / ST) & 1));
+  int s = 0;
+  uint32_t phase = 0;
+  for (size_t b = gw; b < nblocks; b += tw) {
+    mbar_wait(bars + s, phase);
+    const w32* rs = ring + s * (NIN * TW) + lane;  // this stage, this lane's word column
     w32 ops[NIN][N];
     BFP_UNROLL for (int a = 0; a < NIN; ++a)
-      BFP_UNROLL for (int j = 0; j < N; ++j) ops[a][j] = ring[(s * NIN + a) * TW + j * 32 + lane];
+      BFP_UNROLL for (int j = 0; j < N; ++j) ops[a][j] = rs[a * TW + j * 32];
     __syncwarp();
     if (lane == 0) {
       const size_t bn = b + size_t(ST) * tw;
       if (bn < nblocks) issue(s, bn);
     }
+    if (++s == ST) {
+      s = 0;
+      phase ^= 1u;
+    }
     w32 Z[N];
     eval_unit<F, OP>(ops[0], ops[1], ops[NIN - 1], Z);
-    const size_t base = b * size_t(TW) + lane;
-    BFP_UNROLL for (int j = 0; j < N; ++j) st_stream(z + base + j * 32, Z[j]);
+    w32* zb = z + b * size_t(TW) + lane;
+    BFP_UNROLL for (int j = 0; j < N; ++j) st_stream(zb + j * 32, Z[j]);
   }
   pdl_release();
 }
