@@ -1,10 +1,14 @@
-for v in early late; do
-cp tools/variants/lib_$v.so paper_1602_04716_b200/libbfpgpu.so
-for p in 1 0; do
-BFP_PDL=$p timeout 900 python bench.py --config C2,C4,C5,C3 --steps 30 --warmup 5 --no-cpu-baseline --no-e2e > gpurun_out/b.log 2>/dev/null
+timeout 1800 python -m pytest tests -q -x -m "gpu" > gpurun_out/pytest_gpu.log 2>&1; echo pytest_rc=$?
+tail -2 gpurun_out/pytest_gpu.log
+timeout 1500 python bench.py --config all --steps 50 --warmup 5 > gpurun_out/bench_all.log 2> gpurun_out/bench_all.err; echo bench_rc=$?
 python3 -c "
 import json
-for l in open('gpurun_out/b.log'):
-    d=json.loads(l); r=d['roofline']; print('$v PDL=$p', d['config']['workload'][:3], d['value'], d['ms_per_step'], r['step']['ms_per_step_with_kernel_events'], d['clocks']['sm_mhz'])
+for l in open('gpurun_out/bench_all.log'):
+    d=json.loads(l); r=d['roofline']; print(d['config']['workload'][:3], d['value'], 'step_frac', r['step']['frac'], 'kern frac', r['frac'], 'e2e', d.get('e2e',{}).get('value'), d.get('e2e',{}).get('frac_of_pcie_bound'), 'cpu', d.get('cpu_baseline',{}).get('value'), d['clocks']['sm_mhz'], d['clocks']['reasons'])
 "
-done; done
+timeout 900 python bench.py --impl reference > gpurun_out/bench_ref.log 2>&1; echo ref_rc=$?
+python3 -c "
+import json
+for l in open('gpurun_out/bench_ref.log'):
+    d=json.loads(l); print('REF', d['value'], d['cpu_baseline']['cores'], d['cpu_baseline']['per_op'])
+"
