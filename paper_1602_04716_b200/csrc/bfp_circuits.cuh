@@ -551,8 +551,13 @@ BFP_HD void mul_w(const w32* X, const w32* Y, w32* Z) {
     }
   }
 
-  // Normalise: leading one to position 2S+1.
-  constexpr int KP = clog2(WP);
+  // Normalise: leading one to position 2S+1.  With at most one subnormal
+  // operand the leading zeros are <= S+1.  When emin <= -S-1, two subnormal
+  // operands give |x*y| < 2^(2 emin) <= half the smallest subnormal, which
+  // rounds to a signed zero in every mode: that case is forced through the
+  // zero mask below and the normaliser only needs to reach S+1.
+  constexpr bool BOTH_SUB_ZERO = (1 - F::BIAS) <= -S - 1 && clog2(S + 2) < clog2(WP);
+  constexpr int KP = BOTH_SUB_ZERO ? clog2(S + 2) : clog2(WP);
   w32 lz[KP];
   normalize_stages<WP, KP, KP - 1>(P, lz);
 
@@ -589,7 +594,9 @@ BFP_HD void mul_w(const w32* X, const w32* Y, w32* Z) {
   }
   // Special-value rules of bfp_mul (arith.hpp:193-199).
   const w32 use_nan = cx.nan | cy.nan | (cx.inf & cy.z) | (cx.z & cy.inf);
-  const w32 zero_res = (cx.z | cy.z) & ~use_nan;
+  w32 zero_src = cx.z | cy.z;
+  if constexpr (BOTH_SUB_ZERO) zero_src |= ~cx.h & ~cy.h;  // underflows to a signed zero
+  const w32 zero_res = zero_src & ~use_nan;
   const w32 inf_res = (cx.inf | cy.inf) & ~use_nan;
   finish_round<F>(R, ez, sign, zero_res, inf_res, use_nan, Z);
 }
