@@ -1,5 +1,9 @@
-timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 1 --steps 20 --warmup 3 --no-cpu-baseline > gpurun_out/torchrun.log 2> gpurun_out/torchrun.err; echo torchrun_rc=$?
-cut -c1-300 gpurun_out/torchrun.log; tail -3 gpurun_out/torchrun.err
-timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29534 bench.py --impl reference --gpus 1 --steps 3 --warmup 3 > gpurun_out/torchrun_ref.log 2>&1; echo ref_rc=$?
-cut -c1-200 gpurun_out/torchrun_ref.log
-python -c "import __graft_entry__ as g; g.smoke()"; echo smoke_rc=$?
+timeout 1800 python -m pytest tests -q -x -m "gpu" > gpurun_out/pytest_gpu.log 2>&1; echo pytest_rc=$?
+tail -2 gpurun_out/pytest_gpu.log
+timeout 1500 python bench.py --config C3,C5 --steps 30 --warmup 5 --no-cpu-baseline --no-e2e > gpurun_out/b.log 2>/dev/null; echo bench_rc=$?
+python3 -c "
+import json
+for l in open('gpurun_out/b.log'):
+    d=json.loads(l); r=d['roofline']; print(d['config']['workload'][:3], d['value'], 'step_frac', r['step']['frac'], d['clocks']['sm_mhz'])
+    for k,v in r['per_op'].items(): print('   ',k, v['ms'], v['gelem_s'], v['hbm_frac'], v.get('logic_frac'), v.get('binding'), v.get('frac_of_binding'))
+"
