@@ -176,6 +176,19 @@ def _chunked_pack_f32(gen, n, spec, device, chunk=1 << 27):
 
 L2_BYTES = 126 * 1024 * 1024
 
+# (rn, ftz) of every config: the reference default RN + gradual
+# (format.hpp:26-27); --rounding / --subnormals select the secondary rows.
+MODE = (1, 0)
+
+
+def mode_text() -> str:
+    return ("rn" if MODE[0] else "rz") + ("+ftz" if MODE[1] else "")
+
+
+def spec_of(e: int, s: int):
+    import paper_1602_04716_b200 as bfp
+    return bfp.make_spec(e, s, bfp.rounding_mode(MODE[0]), bfp.subnormal_policy(MODE[1]))
+
 
 def input_sets(spec, n, n_inputs: int) -> int:
     """Rotating input sets so that consecutive uses of one set are separated
@@ -216,7 +229,7 @@ def make_jobs(cfg: str, rank: int, world: int, device) -> list:
     L = bfp.lib()
     if cfg == "C1":
         n = 1 << 24
-        spec = bfp.make_spec(4, 3)
+        spec = spec_of(4, 3)
         lo = rank * n
         sets = []
         for r in range(input_sets(spec, n, 2)):  # same data, distinct buffers
@@ -227,7 +240,7 @@ def make_jobs(cfg: str, rank: int, world: int, device) -> list:
         return [_arith_job("add", "add", spec, n, sets, device)]
     if cfg == "C2":
         n = 1 << 26
-        spec = bfp.make_spec(4, 3)
+        spec = spec_of(4, 3)
         lo = rank * n
         a = bfp.pack(W.c2_encodings(lo, lo + n, W.SEED_A, device), spec)
         b = bfp.pack(W.c2_encodings(lo, lo + n, W.SEED_B, device), spec)
@@ -237,7 +250,7 @@ def make_jobs(cfg: str, rank: int, world: int, device) -> list:
                 _arith_job("sub", "sub", spec, n, sets, device)]
     if cfg == "C3":
         n = 1 << 28
-        spec = bfp.make_spec(5, 10)
+        spec = spec_of(5, 10)
         lo = rank * n
         xa = W.c3_floats(lo, lo + n, W.SEED_A, device)
         xb = W.c3_floats(lo, lo + n, W.SEED_B, device)
@@ -269,7 +282,7 @@ def make_jobs(cfg: str, rank: int, world: int, device) -> list:
         lo = rank * n
         jobs = []
         for (e, s) in W.CONFIGS["C4"]["fmts"]:
-            spec = bfp.make_spec(e, s)
+            spec = spec_of(e, s)
             a = bfp.pack(W.c4_encodings(e, s, lo, lo + n, W.SEED_A, device), spec)
             b = bfp.pack(W.c4_encodings(e, s, lo, lo + n, W.SEED_B, device), spec)
             torch.cuda.empty_cache()
@@ -280,7 +293,7 @@ def make_jobs(cfg: str, rank: int, world: int, device) -> list:
         total = 1 << 32
         lo, hi = W.shard(total, rank, world)
         n = hi - lo
-        spec = bfp.make_spec(6, 9)
+        spec = spec_of(6, 9)
         ops = [_chunked_pack_f32(lambda a_, b_, sd=sd: W.c5_floats(lo + a_, lo + b_, sd, device), n,
                                  spec, device)
                for sd in (W.SEED_A, W.SEED_B, W.SEED_C)]
@@ -303,69 +316,91 @@ def run_device(cfg: str, steps: int, warmup: int, world: int, rank: int, local: 
     stream = torch.cuda.current_stream(device)
     st = stream.cuda_stream
 
-    def step(i, evs=None):
-        for k, j in enumerate(jobs):
-            if evs is not None:
-                evs[k][0].record(stream)
+    def step(i):
+        for j in jobs:
             j.launch(i, st)
-            if evs is not None:
-                evs[k][1].record(stream)
-
 
     for i in range(warmup):
         step(i)
     torch.cuda.synchronize()
 
-    # sustained window of the same step for the clock record (~1.5 s)
+    # The K timed steps are issued through the C ABI exactly as a caller does,
+    # captured once into a CUDA graph (launch-bound small steps such as C1 --
+    # a 48 MiB, ~8 us kernel -- would otherwise measure the host's per-call
+    # overhead, not the device) and replayed; consecutive kernels keep their
+    # programmatic-dependent-launch edges inside the graph.
+    cap = torch.cuda.Stream(device)
+
+    def capture(fn) -> tuple:
+        g = torch.cuda.CUDAGraph()
+        torch.cuda.synchronize()
+        l0 = L.bfp_launch_count()
+        with torch.cuda.graph(g, stream=cap):
+            fn(cap.cuda_stream)
+        torch.cuda.synchronize()
+        return g, L.bfp_launch_count() - l0
+
+    def all_steps(s):
+        for i in range(steps):
+            for j in jobs:
+                j.launch(i, s)
+
+    g_all, launches = capture(all_steps)
+    g_all.replay()  # untimed: graph upload + one more warm pass
+    torch.cuda.synchronize()
+
+    # sustained window of the same graph for the clock record (~1.5 s)
     t_probe = time.perf_counter()
-    step(0)
+    g_all.replay()
     torch.cuda.synchronize()
     one = max(time.perf_counter() - t_probe, 1e-5)
-    reps = max(1, int(1.5 / one))
     with ClockSampler(local) as cs:
-        for i in range(reps):
-            step(i)
+        for _ in range(max(1, int(1.5 / one))):
+            g_all.replay()
         torch.cuda.synchronize()
     clocks = cs.summary()
 
-    # Timed region A (the value): K back-to-back steps exactly as a caller issues
-    # them -- no per-kernel events, which would serialise consecutive launches
-    # and defeat the programmatic-dependent-launch overlap.
-    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    launches0 = L.bfp_launch_count()
-    t0.record(stream)
-    for i in range(steps):
-        step(i)
-    t1.record(stream)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    launches = L.bfp_launch_count() - launches0
-    ms_total = t0.elapsed_time(t1)
+    def timed_replay(g) -> float:
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0.record(stream)  # replay() launches the graph on the current stream
+        g.replay()
+        t1.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        return t0.elapsed_time(t1)
+
+    # Timed region (the value): K whole steps, back to back.
+    ms_total = timed_replay(g_all)
     if world > 1:
         t = torch.tensor([ms_total], device=device)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_total = float(t.item())
-    # Timed region B (the roofline): the same K steps with CUDA events around
-    # every kernel on its stream -> each kernel's mean launch duration
-    # (conservative: the events serialise the launches).
-    per_kernel = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-                   for _ in range(steps)] for _ in jobs]
+    # The same K steps issued eagerly (one host call per kernel), for reference.
+    te0, te1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
-    tb0, tb1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    tb0.record(stream)
+    te0.record(stream)
     for i in range(steps):
-        step(i, [[per_kernel[k][i][0], per_kernel[k][i][1]] for k in range(len(jobs))])
-    tb1.record(stream)
+        step(i)
+    te1.record(stream)
     torch.cuda.synchronize()
-    ms_total_events = tb0.elapsed_time(tb1)
-    kern_ms = [sum(per_kernel[k][i][0].elapsed_time(per_kernel[k][i][1]) for i in range(steps)) / steps
-               for k in range(len(jobs))]
+    ms_total_eager = te0.elapsed_time(te1)
+    # Per-kernel durations (the roofline): for each kernel of the step, a graph
+    # of its K launches (same rotating operands) timed with events around the
+    # replay on the launching stream -> mean launch duration.
+    kern_ms = []
+    for k, j in enumerate(jobs):
+        g, _ = capture(lambda s, j=j: [j.launch(i, s) for i in range(steps)])
+        g.replay()
+        torch.cuda.synchronize()
+        kern_ms.append(timed_replay(g) / steps)
+        del g
+    del g_all
     return {"jobs": jobs, "ms_total": ms_total, "kern_ms": kern_ms, "clocks": clocks,
-            "launches": int(launches), "ms_total_events": ms_total_events}
+            "launches": int(launches), "ms_total_eager": ms_total_eager}
 
 
 def run_e2e(cfg: str, jobs, steps: int, world: int, rank: int, local: int) -> dict:
@@ -494,12 +529,27 @@ def pcie_probe(local: int, nbytes: int = 1 << 28) -> dict:
             "bidir_gbs": round(2 * nbytes / t3 / 1e9, 1)}
 
 
-def lop3_peak() -> float | None:
+def lop3_peak(local: int = 0) -> dict | None:
+    """LOP3 issue rate of the probe kernel (bfp_probe_lop3: 8 independent
+    chains per thread on every SM).  burst = one launch on a cool GPU (the
+    clock ceiling); sustained = back-to-back launches for ~2 s, median of the
+    second half, with the SM clock it settled at (the denominator for kernels
+    timed inside long steps, which run under the same power cap)."""
     import paper_1602_04716_b200 as bfp
+    L = bfp.lib()
     ms, rate = C.c_float(), C.c_double()
-    if bfp.lib().bfp_probe_lop3(4000, C.byref(ms), C.byref(rate)) != 0:
+    if L.bfp_probe_lop3(4000, C.byref(ms), C.byref(rate)) != 0:
         return None
-    return rate.value
+    burst = rate.value
+    rates = []
+    with ClockSampler(local) as cs:
+        t = time.perf_counter()
+        while time.perf_counter() - t < 2.0:
+            if L.bfp_probe_lop3(4000, C.byref(ms), C.byref(rate)) != 0:
+                return None
+            rates.append(rate.value)
+    sus = statistics.median(rates[len(rates) // 2:])
+    return {"burst": burst, "sustained": sus, "sustained_sm_mhz": cs.summary().get("sm_mhz")}
 
 
 # --------------------------------------------------------- reference (CPU)
@@ -527,16 +577,16 @@ def ref_cpu_jobs(cfg: str, sample: int, threads: int):
                                                         threads=threads)))
 
     if cfg == "C1":
-        fmt = (4, 3, 1, 0)
+        fmt = (4, 3) + MODE
         encs = [O.encode_f32(fmt, W.c1_floats(0, sample, sd, "cpu").numpy()) for sd in (1, 2)]
         arith("add", "add", fmt, encs)
     elif cfg == "C2":
-        fmt = (4, 3, 1, 0)
+        fmt = (4, 3) + MODE
         encs = [W.c2_encodings(0, sample, sd, "cpu").numpy().astype(np.uint64) for sd in (1, 2)]
         arith("mul", "mul", fmt, encs)
         arith("sub", "sub", fmt, encs)
     elif cfg == "C3":
-        fmt = (5, 10, 1, 0)
+        fmt = (5, 10) + MODE
         xs = [W.c3_floats(0, sample, sd, "cpu").numpy() for sd in (1, 2)]
         encs = [O.encode_f32(fmt, x) for x in xs]
         planes_out = np.zeros(O.nblocks(sample) * 16 * 32, dtype=np.uint32)
@@ -544,7 +594,7 @@ def ref_cpu_jobs(cfg: str, sample: int, threads: int):
         pa = O.pack_planes(encs[0], 16)
         x0 = np.ascontiguousarray(xs[0])
         jobs.append(("pack_f32", lambda: R.ref_pack_f32_path(
-            x0.ctypes.data_as(O._f32p), sample, planes_out.ctypes.data_as(O._u32p), 5, 10, 1, 0,
+            x0.ctypes.data_as(O._f32p), sample, planes_out.ctypes.data_as(O._u32p), 5, 10, MODE[0], MODE[1],
             threads)))
         arith("add", "add", fmt, encs)
         arith("mul", "mul", fmt, encs)
@@ -552,13 +602,13 @@ def ref_cpu_jobs(cfg: str, sample: int, threads: int):
             pa.ctypes.data_as(O._u32p), sample, fl_out.ctypes.data_as(O._f32p), 5, 10, threads)))
     elif cfg == "C4":
         for (e, s) in W.CONFIGS["C4"]["fmts"]:
-            fmt = (e, s, 1, 0)
+            fmt = (e, s) + MODE
             encs = [W.c4_encodings(e, s, 0, sample, sd, "cpu").numpy().astype(np.uint64)
                     for sd in (1, 2)]
             arith(f"add_1/{e}/{s}", "add", fmt, encs)
             arith(f"mul_1/{e}/{s}", "mul", fmt, encs)
     elif cfg == "C5":
-        fmt = (6, 9, 1, 0)
+        fmt = (6, 9) + MODE
         encs = [O.encode_f32(fmt, W.c5_floats(0, sample, sd, "cpu").numpy()) for sd in (1, 2, 3)]
         arith("mul_add", "mul_add", fmt, encs)
     else:
@@ -621,7 +671,8 @@ CONFIG_TEXT = {
 
 def config_block(cfg: str, world: int, jobs=None) -> dict:
     text, fmt, n = CONFIG_TEXT[cfg]
-    d = {"workload": text, "format": fmt, "rounding": "rn", "subnormals": "gradual",
+    d = {"workload": text, "format": fmt, "rounding": "rn" if MODE[0] else "rz",
+         "subnormals": "ftz" if MODE[1] else "gradual",
          "parallelism": f"dp{world} (independent block-aligned shards, no collective)",
          "l2": "inputs larger than L2: operand sets rotate step by step so each set is reused "
                "only after >= 2x L2 (126 MB) of other traffic; outputs rotate over two buffers"}
@@ -643,6 +694,7 @@ def main_reference(args) -> None:
         sample = REF_SAMPLE[cfg]
         r = ref_cpu_run(cfg, sample, reps=args.warmup)  # warm-up steps
         r = ref_cpu_run(cfg, sample, reps=args.steps)
+        r1 = ref_cpu_run(cfg, sample, reps=3, threads=1)  # thread-scaling check
         value = r["value"]
         line = {
             "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": UNIT,
@@ -656,7 +708,9 @@ def main_reference(args) -> None:
                              "sample": f"{r['sample']} elements x {r['ops']} per step, "
                                        f"lane<1024>, {r['cores']} threads, {cpu_model()}, "
                                        f"{r['lib']}",
-                             "per_op": r["per_op_gelems"]},
+                             "per_op": r["per_op_gelems"], "nproc": os.cpu_count(),
+                             "value_1_thread": round(r1["value"], 4),
+                             "thread_scaling": round(value / r1["value"], 2)},
             "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0},
         }
@@ -683,7 +737,7 @@ def main_ours(args) -> None:
         e2e = run_e2e(cfg, jobs, args.steps, world, rank, local) if not args.no_e2e else None
         if peak_lop3 is None and rank == 0:
             log("lop3 probe")
-            peak_lop3 = lop3_peak()
+            peak_lop3 = lop3_peak(local)
 
         total_elems = sum(j.n for j in jobs) * world
         ms_step = res["ms_total"] / args.steps
@@ -702,9 +756,10 @@ def main_ours(args) -> None:
                 if lop3 is not None and peak_lop3:
                     pe = lop3 / 32.0
                     hbm_t = j.algo_bytes / (peaks["hbm_gbs"] * 1e9)
-                    logic_t = pe * j.n / peak_lop3
+                    logic_t = pe * j.n / peak_lop3["burst"]
                     ent.update({"lop3_per_elem": round(pe, 3),
                                 "logic_frac": round(logic_t / dur, 4),
+                                "logic_frac_sustained": round(pe * j.n / peak_lop3["sustained"] / dur, 4),
                                 "binding": "logic" if logic_t > hbm_t else "hbm",
                                 "frac_of_binding": round(max(hbm_t, logic_t) / dur, 4)})
             per_op[j.label] = ent
@@ -713,25 +768,35 @@ def main_ours(args) -> None:
         traffic = None
         tfile = ROOT / "profiles" / "ncu_traffic.json"
         if tfile.exists():
-            traffic = json.loads(tfile.read_text()).get(f"{cfg}:{jd.label}")
-        roof = {"bound": "hbm", "kernel": f"{jd.label} (1/{jd.spec.exp_bits}/{jd.spec.sig_bits} rn)",
+            key = f"{cfg}:{jd.label}" + ("" if MODE == (1, 0) else f":{mode_text()}")
+            traffic = json.loads(tfile.read_text()).get(key)
+        roof = {"bound": "hbm", "kernel": f"{jd.label} (1/{jd.spec.exp_bits}/{jd.spec.sig_bits} {mode_text()})",
                 "achieved": round(ach, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": round(ach / peaks["hbm_gbs"], 4), "traffic": traffic,
                 "peak_source": peaks["source"],
                 "algorithmic_bytes_per_launch": int(jd.algo_bytes),
                 "launch_ms": round(ms_dom, 4), "per_op": per_op}
         if peak_lop3:
-            roof["peak_lop3_per_s_measured"] = peak_lop3
+            roof["peak_lop3_per_s_measured"] = peak_lop3["burst"]
+            roof["peak_lop3_per_s_sustained"] = peak_lop3["sustained"]
+            roof["peak_lop3_sustained_sm_mhz"] = peak_lop3["sustained_sm_mhz"]
         step_bytes = sum(j.algo_bytes for j in jobs)
         step_gbs = step_bytes / (ms_step * 1e-3) / 1e9
+        # self-check: inputs rotate through > 2x L2, so no step or kernel can
+        # beat the HBM copy peak; a faster figure means the timing is broken
+        for j, ms in zip(jobs, res["kern_ms"]):
+            if j.algo_bytes / (ms * 1e-3) / 1e9 > 1.1 * peaks["hbm_gbs"] * world:
+                raise RuntimeError(f"{cfg}:{j.label}: {ms} ms per launch is faster than HBM allows")
+        if step_gbs > 1.1 * peaks["hbm_gbs"] * world:
+            raise RuntimeError(f"{cfg}: step time {ms_step} ms is faster than HBM allows")
         roof["step"] = {"algorithmic_bytes": int(step_bytes), "ms": round(ms_step, 5),
                         "achieved_gbs": round(step_gbs, 1),
                         "frac": round(step_gbs / peaks["hbm_gbs"], 4),
-                        "note": "whole step, back-to-back launches (consecutive kernels overlap "
-                                "through programmatic dependent launch); the per-kernel figures "
-                                "above come from a second pass with CUDA events around every "
-                                "kernel, which serialises them",
-                        "ms_per_step_with_kernel_events": round(res["ms_total_events"] / args.steps, 5)}
+                        "note": "whole step: K steps captured once into a CUDA graph through the "
+                                "C ABI and replayed (consecutive kernels overlap through "
+                                "programmatic dependent launch); per-kernel figures above come "
+                                "from one graph per kernel holding its K launches",
+                        "ms_per_step_eager": round(res["ms_total_eager"] / args.steps, 5)}
         dd = per_op[jd.label]
         if "binding" in dd:
             roof["binding_leg"] = dd["binding"]
@@ -765,13 +830,16 @@ def main_ours(args) -> None:
         if rank == 0 and world == 1 and not args.no_cpu_baseline:
             log("cpu baseline")
             cb = ref_cpu_run(cfg, REF_SAMPLE[cfg], seconds=args.cpu_seconds)
+            c1 = ref_cpu_run(cfg, REF_SAMPLE[cfg], reps=3, threads=1)  # thread-scaling check
             line["cpu_baseline"] = {
                 "value": round(cb["value"], 4), "unit": UNIT, "cores": cb["cores"],
                 "kind": "reference",
                 "sample": f"{cb['sample']} elements x {cb['ops']} per step, best of {cb['reps']} "
                           f"steps (~{args.cpu_seconds:.0f} s), lane<1024>, {cb['cores']} threads, "
                           f"{cpu_model()}, {cb['lib']}",
-                "per_op": cb["per_op_gelems"]}
+                "per_op": cb["per_op_gelems"], "nproc": os.cpu_count(),
+                "value_1_thread": round(c1["value"], 4),
+                "thread_scaling": round(cb["value"] / c1["value"], 2)}
         del jobs, res
         torch.cuda.empty_cache()
         if rank == 0:
@@ -791,7 +859,11 @@ def main() -> None:
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--rounding", choices=["rn", "rz"], default="rn")
+    ap.add_argument("--subnormals", choices=["gradual", "ftz"], default="gradual")
     args = ap.parse_args()
+    global MODE
+    MODE = (int(args.rounding == "rn"), int(args.subnormals == "ftz"))
     args.configs = (["C1", "C2", "C3", "C4", "C5"] if args.config == "all"
                     else args.config.split(","))
     if args.warmup < 3:

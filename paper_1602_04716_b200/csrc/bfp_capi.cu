@@ -386,6 +386,17 @@ void bfp_host_ctx_destroy(bfp_host_ctx* c) {
 
 namespace {
 
+// Chunk size of one call: the context's chunk, but small enough that the call
+// splits into >= 2 x depth chunks (a 2^24-element call in one 2^24 chunk runs
+// H2D, kernel and D2H back to back), and never below 1024 blocks (2^20
+// elements) so per-copy overhead stays small.
+size_t chunk_for(const bfp_host_ctx* c, size_t blocks) {
+  constexpr size_t kMinBlocks = 1024;
+  const size_t split = (blocks + 2 * bfp_host_ctx::kDepth - 1) / (2 * bfp_host_ctx::kDepth);
+  size_t cb = split < kMinBlocks ? kMinBlocks : split;
+  return cb < c->chunk_blocks ? cb : c->chunk_blocks;
+}
+
 // Generic chunked pipeline: chunk k uses stream/buffer set k % depth, so the
 // H2D of chunk k+1, the kernel of chunk k and the D2H of chunk k-1 overlap.
 // in_stride / out_stride: bytes per 1024-element block on each side.
@@ -395,9 +406,10 @@ bfp_status host_pipeline(bfp_host_ctx* c, size_t count, int n_in, const void* co
                          Body body) {
   if (!c) return fail(BFP_EARG, "null host context");
   const size_t blocks = nblocks(count);
-  for (size_t b0 = 0, k = 0; b0 < blocks; b0 += c->chunk_blocks, ++k) {
+  const size_t cb = chunk_for(c, blocks);
+  for (size_t b0 = 0, k = 0; b0 < blocks; b0 += cb, ++k) {
     const int i = int(k % bfp_host_ctx::kDepth);
-    const size_t nb = (blocks - b0 < c->chunk_blocks) ? blocks - b0 : c->chunk_blocks;
+    const size_t nb = (blocks - b0 < cb) ? blocks - b0 : cb;
     const size_t e0 = b0 * 1024;
     const size_t ecount = (count - e0 < nb * 1024) ? count - e0 : nb * 1024;
     for (int a = 0; a < n_in; ++a) {
@@ -466,11 +478,12 @@ bfp_status bfp_arith_host_batch(bfp_host_ctx* c, int nops, const int* ops, const
   if (!h_x || !h_y || (need_c && !h_c)) return fail(BFP_EARG, "null operand");
   const size_t stride = nplanes(f) * 128;
   const size_t blocks = nblocks(count);
+  const size_t cb = chunk_for(c, blocks);
   // per chunk: inputs into in[i][0..2], op q's result into out[i][q] (own
   // buffer, so op q+1's kernel does not wait for op q's D2H)
-  for (size_t b0 = 0, k = 0; b0 < blocks; b0 += c->chunk_blocks, ++k) {
+  for (size_t b0 = 0, k = 0; b0 < blocks; b0 += cb, ++k) {
     const int i = int(k % bfp_host_ctx::kDepth);
-    const size_t nb = (blocks - b0 < c->chunk_blocks) ? blocks - b0 : c->chunk_blocks;
+    const size_t nb = (blocks - b0 < cb) ? blocks - b0 : cb;
     const size_t bytes = nb * stride;
     const void* ins[3] = {h_x, h_y, h_c};
     for (int a = 0; a < (need_c ? 3 : 2); ++a) {

@@ -154,10 +154,13 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+#ifndef BFP_BULK_BUDGET
+#define BFP_BULK_BUDGET (16 * 1024)  // ring bytes per warp
+#endif
 template <int N, int NIN>
 constexpr int bulk_stages() {
   constexpr int stage_bytes = NIN * N * 128;
-  constexpr int s = (16 * 1024) / stage_bytes;
+  constexpr int s = (BFP_BULK_BUDGET) / stage_bytes;
   return s < 2 ? 2 : (s > 4 ? 4 : s);
 }
 
@@ -684,16 +687,18 @@ inline int wave_ctas(K kernel, size_t smem = 0) {
   return sms * occ;
 }
 
-// Grid: up to grid_mult() (default 4) resident waves of CTAs -- oversubscription
-// lets the CTA scheduler backfill SMs at the tail, measured +5-8% on HBM-bound
-// kernels -- but never below two units per thread (single-unit CTAs measured
-// slower) and never below one wave.
+// Grid: a whole number k <= grid_mult() (default 4) of resident waves
+// (#SM x occupancy).  Oversubscription lets the CTA scheduler backfill SMs at
+// the tail (+5-8% on large HBM-bound launches); k is the largest that still
+// gives every thread >= 2 units (single-unit CTAs measured slower).  Whole
+// waves only: a partial last wave (the old "need/2 CTAs" rule gave 1.38 waves
+// at 2^24 elements) leaves most SMs idle while its CTAs run.
 inline int grid_for(int wave, size_t units) {
   const size_t need = (units + kThreads - 1) / kThreads;
   if (need <= size_t(wave)) return int(need ? need : 1);
-  const size_t cap = size_t(wave) * size_t(grid_mult());
-  const size_t two = (need + 1) / 2;
-  return int(std::min(cap, std::max(size_t(wave), two)));
+  size_t k = size_t(grid_mult());
+  while (k > 1 && k * size_t(wave) * kThreads * 2 > units) --k;
+  return int(k * size_t(wave));
 }
 
 // Per-format entry points: implemented by the compiled networks

@@ -229,16 +229,17 @@ def test_unsupported_and_errors():
     assert L.bfp_add(C.byref(f), t.data_ptr(), t.data_ptr(), t.data_ptr(), 0, None) == _lib.BFP_OK
 
 
-def test_host_pipeline_matches_device(oracle):
+@pytest.mark.parametrize("chunk,n", [(1 << 20, 3 * (1 << 20) + 5000),  # ctx chunk binds
+                                     (1 << 24, 9 * (1 << 20) + 123)])  # split into 8 ragged chunks
+def test_host_pipeline_matches_device(oracle, chunk, n):
     L = _lib.lib()
     fmt = (5, 10, 1, 0)
     nb = 16
-    n = 3 * (1 << 20) + 5000
     rng = np.random.default_rng(4)
     x, y = operands(5, 10, n, rng), operands(5, 10, n, rng)
     px, py = oracle.pack_planes(x, nb), oracle.pack_planes(y, nb)
     pz = np.zeros_like(px)
-    ctx = L.bfp_host_ctx_create(1 << 20)
+    ctx = L.bfp_host_ctx_create(chunk)
     try:
         f = cfmt(fmt)
         rc = L.bfp_arith_host(ctx, 2, C.byref(f), px.ctypes.data, py.ctypes.data, None, pz.ctypes.data, n)
@@ -463,13 +464,13 @@ def test_host_batch_matches_device(oracle):
     """bfp_arith_host_batch: several ops over one H2D of shared host operands."""
     L = _lib.lib()
     fmt = (4, 3, 1, 0)
-    n = 3 * (1 << 20) + 777
+    n = 5 * (1 << 20) + 777
     rng = np.random.default_rng(8)
     x, y = operands(4, 3, n, rng), operands(4, 3, n, rng)
     px, py = oracle.pack_planes(x, 8), oracle.pack_planes(y, 8)
     outs = [np.zeros_like(px) for _ in range(3)]
     ops = [2, 1, 3]
-    ctx = L.bfp_host_ctx_create(1 << 20)
+    ctx = L.bfp_host_ctx_create(1 << 24)  # the call splits itself into ragged chunks
     try:
         f = cfmt(fmt)
         arr = (C.c_int * 3)(*ops)
