@@ -25,8 +25,12 @@ using bfpg::Impl;
 namespace bfpg {
 int bulk_mode() {
   static const int m = [] {
+    // Default off: under steady-state (graph-replayed) timing the plain loop
+    // beat the bulk-copy ring on every network, logic-bound ones included
+    // (its occupancy, limited by registers only, hides the LOP3 chains
+    // better than the ring's smem-limited 12-16 warps/SM).
     const char* v = std::getenv("BFP_BULK");
-    return v ? std::atoi(v) : 1;
+    return v ? std::atoi(v) : 0;
   }();
   return m;
 }

@@ -510,60 +510,55 @@ BFP_HD Classes classify(const w32* X) {
 }
 
 // ================================================================= MUL
+// Exact product of two (S+1)-bit significands: shift-add rows, one carry
+// chain per row; each cell = AND (partial product) + XOR3 + MAJ, pinned.
+template <int S>
+BFP_HD void sig_product(const w32* mx, const w32* my, w32* P /*2S+2*/) {
+  BFP_UNROLL for (int j = 0; j <= S; ++j) P[j] = lop3<L_AND2>(mx[j], my[0], 0u);
+  BFP_UNROLL for (int i = 1; i <= S; ++i) {
+    // j = 0: carry-in 0 -> sum = a ^ pp, carry = a & pp (AND fused)
+    w32 c = lop3<L_AND3>(mx[0], my[i], P[i]);
+    P[i] = lop3<L_XOR_AND>(mx[0], my[i], P[i]);
+    BFP_UNROLL for (int j = 1; j <= S; ++j) {
+      if (i == 1 && j == S) {  // nothing accumulated above row 0 yet
+        const w32 s0 = lop3<L_XOR_AND>(mx[j], my[i], c);
+        c = lop3<L_AND3>(mx[j], my[i], c);
+        P[i + j] = s0;
+        continue;
+      }
+      const w32 pp = lop3<L_AND2>(mx[j], my[i], 0u);
+      const w32 a = P[i + j];
+      P[i + j] = lop3<L_XOR3>(a, pp, c);
+      c = lop3<L_MAJ>(a, pp, c);
+    }
+    P[i + S + 1] = c;
+  }
+}
+
 // Z = X * Y.  bfp_mul semantics, arith.hpp:330-373.
+//
+// When emin <= -S-1 (every format here but 1/3/2), two subnormal operands
+// give |x*y| < 2^(2 emin) <= half the smallest subnormal, which rounds to a
+// signed zero in every mode; that case is forced through the zero mask, so at
+// most one operand needs normalising.  That operand's significand (S+1 bits)
+// is normalised BEFORE the product -- the operands are ordered by hidden bit
+// (two muxes per significand bit; the exponent sum is symmetric) -- and the
+// product, then in [2^2S, 2^(2S+2)), needs a single 1-bit normalise instead of
+// a log shifter over all 2S+2 product bits.
 template <class F>
 BFP_HD void mul_w(const w32* X, const w32* Y, w32* Z) {
   constexpr int E = F::E, S = F::S, M = E + S;
   constexpr int EW = E + 2;  // signed working exponent
+  constexpr bool BOTH_SUB_ZERO = (1 - F::BIAS) <= -S - 1;
   const w32 sign = X[M] ^ Y[M];
   const Classes cx = classify<F>(X), cy = classify<F>(Y);
 
-  // Exact product of the (S+1)-bit significands: shift-add rows, one carry
-  // chain per row; each cell = AND (partial product) + XOR3 + MAJ, pinned.
   constexpr int WP = 2 * S + 2;
   w32 P[WP];
-  {
-    w32 mx[S + 1], my[S + 1];
-    BFP_UNROLL for (int i = 0; i < S; ++i) {
-      mx[i] = X[i];
-      my[i] = Y[i];
-    }
-    mx[S] = cx.h;
-    my[S] = cy.h;
-    BFP_UNROLL for (int j = 0; j <= S; ++j) P[j] = lop3<L_AND2>(mx[j], my[0], 0u);
-    BFP_UNROLL for (int i = 1; i <= S; ++i) {
-      // j = 0: carry-in 0 -> sum = a ^ pp, carry = a & pp (AND fused)
-      w32 c = lop3<L_AND3>(mx[0], my[i], P[i]);
-      P[i] = lop3<L_XOR_AND>(mx[0], my[i], P[i]);
-      BFP_UNROLL for (int j = 1; j <= S; ++j) {
-        if (i == 1 && j == S) {  // nothing accumulated above row 0 yet
-          const w32 s0 = lop3<L_XOR_AND>(mx[j], my[i], c);
-          c = lop3<L_AND3>(mx[j], my[i], c);
-          P[i + j] = s0;
-          continue;
-        }
-        const w32 pp = lop3<L_AND2>(mx[j], my[i], 0u);
-        const w32 a = P[i + j];
-        P[i + j] = lop3<L_XOR3>(a, pp, c);
-        c = lop3<L_MAJ>(a, pp, c);
-      }
-      P[i + S + 1] = c;
-    }
-  }
-
-  // Normalise: leading one to position 2S+1.  With at most one subnormal
-  // operand the leading zeros are <= S+1.  When emin <= -S-1, two subnormal
-  // operands give |x*y| < 2^(2 emin) <= half the smallest subnormal, which
-  // rounds to a signed zero in every mode: that case is forced through the
-  // zero mask below and the normaliser only needs to reach S+1.
-  constexpr bool BOTH_SUB_ZERO = (1 - F::BIAS) <= -S - 1 && clog2(S + 2) < clog2(WP);
-  constexpr int KP = BOTH_SUB_ZERO ? clog2(S + 2) : clog2(WP);
-  w32 lz[KP];
-  normalize_stages<WP, KP, KP - 1>(P, lz);
-
-  // ez = ex_eff + ey_eff - bias - lz  (biased result exponent minus one).
+  w32 R[S + 3];  // [jam, guard, sig(S+1)]
   w32 ez[EW];
-  {
+  // ez = ex_eff + ey_eff - bias - lz  (biased result exponent minus one).
+  auto exponent = [&](const w32* lz, int KL, w32 borrow_in_sub) {
     w32 a[EW], b[EW];
     BFP_UNROLL for (int i = 0; i < EW; ++i) {
       a[i] = (i < E) ? X[S + i] : 0u;
@@ -578,20 +573,56 @@ BFP_HD void mul_w(const w32* X, const w32* Y, w32* Z) {
     BFP_UNROLL for (int i = 0; i < EW; ++i) nb[i] = ((NB >> i) & 1) ? ONES : 0u;
     w32 u[EW];
     (void)add_k<EW>(t, nb, 0, u);
-    w32 l[EW];
-    BFP_UNROLL for (int i = 0; i < EW; ++i) l[i] = (i < KP) ? lz[i] : 0u;
-    (void)sub_k<EW>(u, l, ez);
-  }
-
-  // [jam, guard, sig(S+1)] from the normalised product.
-  w32 R[S + 3];
-  {
+    // ez = u - lz - borrow_in_sub = u + ~lz + (1 - borrow_in_sub)
+    w32 c = ~borrow_in_sub;
+    BFP_UNROLL for (int i = 0; i < EW; ++i) {
+      const w32 ui = u[i], nl = ~((i < KL) ? lz[i] : 0u);
+      ez[i] = ui ^ nl ^ c;
+      c = maj(ui, nl, c);
+    }
+  };
+  if constexpr (BOTH_SUB_ZERO) {
+    // s: the operand that may be subnormal (X unless X is normal), n: the other.
+    w32 ms[S + 1], mn[S + 1];
+    BFP_UNROLL for (int i = 0; i < S; ++i) {
+      ms[i] = pmux(cx.h, Y[i], X[i]);
+      mn[i] = pmux(cx.h, X[i], Y[i]);
+    }
+    ms[S] = cx.h & cy.h;  // hidden bit of s: clear iff either is subnormal
+    mn[S] = ONES;         // n is normal (or the result is forced to zero)
+    constexpr int KN = clog2(S + 1) > 0 ? clog2(S + 1) : 1;
+    w32 lz[KN];
+    normalize_stages<S + 1, KN, KN - 1>(ms, lz);
+    sig_product<S>(ms, mn, P);
+    // 1-bit normalise: top = P[2S+1]; otherwise the leading one is at 2S.
+    const w32 top = P[WP - 1];
+    w32 st = 0;
+    BFP_UNROLL for (int i = 0; i + 1 < S; ++i) st |= P[i];
+    R[0] = st | (top & P[S - 1]);
+    R[1] = pmux(top, P[S], P[S - 1]);
+    BFP_UNROLL for (int i = 0; i <= S; ++i) R[2 + i] = pmux(top, P[S + 1 + i], P[S + i]);
+    exponent(lz, KN, ~top);
+  } else {
+    w32 mx[S + 1], my[S + 1];
+    BFP_UNROLL for (int i = 0; i < S; ++i) {
+      mx[i] = X[i];
+      my[i] = Y[i];
+    }
+    mx[S] = cx.h;
+    my[S] = cy.h;
+    sig_product<S>(mx, my, P);
+    // Normalise: leading one to position 2S+1.
+    constexpr int KP = clog2(WP);
+    w32 lz[KP];
+    normalize_stages<WP, KP, KP - 1>(P, lz);
     w32 st = 0;
     BFP_UNROLL for (int i = 0; i < S; ++i) st |= P[i];
     R[0] = st;
     R[1] = P[S];
     BFP_UNROLL for (int i = 0; i <= S; ++i) R[2 + i] = P[S + 1 + i];
+    exponent(lz, KP, 0u);
   }
+
   // Special-value rules of bfp_mul (arith.hpp:193-199).
   const w32 use_nan = cx.nan | cy.nan | (cx.inf & cy.z) | (cx.z & cy.inf);
   w32 zero_src = cx.z | cy.z;

@@ -672,7 +672,7 @@ inline cudaError_t launch_smem(void (*k)(KArgs...), int grid, size_t smem, cudaS
   return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
 }
 
-int bulk_mode();   // bfp_capi.cu: BFP_BULK = 0 off / 1 auto (default) / 2 force
+int bulk_mode();   // bfp_capi.cu: BFP_BULK = 0 off (default) / 1 auto / 2 force
 int grid_mult();   // bfp_capi.cu: BFP_GRID_MULT (default 4): CTA waves per grid
 
 // Resident CTAs for a full wave of `kernel`: #SM x occupancy.
