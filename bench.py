@@ -491,6 +491,30 @@ def run_e2e(cfg: str, jobs, steps: int, world: int, rank: int, local: int) -> di
         L.bfp_host_ctx_destroy(ctx)
 
 
+def hbm_2r1w_probe(local: int, nbytes: int = 1 << 30) -> float:
+    """HBM rate of a plain 2-read : 1-write stream (torch bitwise_xor over
+    1 GiB int32 operands, best of 10 by CUDA events) -- the access mix of a
+    binary op.  MEASURED_PEAKS.json's copy is 1:1, which HBM serves slightly
+    slower, so the binary-op kernels can exceed it; this is the context."""
+    import torch
+    dev = torch.device("cuda", local)
+    n = nbytes // 4
+    a = torch.randint(0, 1 << 30, (n,), dtype=torch.int32, device=dev)
+    b = torch.randint(0, 1 << 30, (n,), dtype=torch.int32, device=dev)
+    c = torch.empty_like(a)
+    best = 1e9
+    for _ in range(12):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        torch.bitwise_xor(a, b, out=c)
+        e1.record()
+        torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    del a, b, c
+    torch.cuda.empty_cache()
+    return round(3 * nbytes / (best * 1e-3) / 1e9, 1)
+
+
 def pcie_probe(local: int, nbytes: int = 1 << 28) -> dict:
     """Pinned-host <-> device copy bandwidth on this box (the e2e ceiling):
     H2D alone, D2H alone, and both directions at once on two streams."""
@@ -738,6 +762,7 @@ def main_ours(args) -> None:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     log = (lambda m: print(f"[bench r{rank}] {m}", file=sys.stderr, flush=True))
     peak_lop3 = None
+    hbm_2r1w = None
     for cfg in args.configs:
         log(f"device timing {cfg}")
         res = run_device(cfg, args.steps, args.warmup, world, rank, local)
@@ -750,6 +775,7 @@ def main_ours(args) -> None:
         if peak_lop3 is None and rank == 0:
             log("lop3 probe")
             peak_lop3 = lop3_peak(local)
+            hbm_2r1w = hbm_2r1w_probe(local)
 
         total_elems = sum(j.n for j in jobs) * world
         ms_step = res["ms_total"] / args.steps
@@ -787,6 +813,7 @@ def main_ours(args) -> None:
                 "achieved": round(ach, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": round(ach / peaks["hbm_gbs"], 4), "traffic": traffic,
                 "peak_source": peaks["source"],
+                "hbm_2r1w_probe_gbs": hbm_2r1w,
                 "algorithmic_bytes_per_launch": int(jd.algo_bytes),
                 "launch_ms": round(ms_dom, 4), "per_op": per_op}
         if peak_lop3:

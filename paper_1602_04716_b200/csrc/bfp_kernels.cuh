@@ -91,8 +91,23 @@ __device__ __forceinline__ void eval_unit(const w32* X, const w32* Y, const w32*
 #ifndef BFP_ARITH_MINB
 #define BFP_ARITH_MINB 1
 #endif
+// Minimum resident CTAs per SM asked of ptxas.  Mid-size logic-bound networks
+// (mul / div of 300-800 LOP3 per word: 1/5/7, 1/5/10, 1/6/9, 1/8/7) come out
+// at 90-100 registers unconstrained (5 CTAs/SM); capping them for 6 CTAs
+// costs no spills and measured +10% on 1/8/7 mul, +2-5% on 1/5/10 mul.  Small
+// networks are HBM-bound (the cap measured -2..-3% there) and the widest
+// (1/8/15 mul, mul_add) gained nothing.
 template <class F, int OP>
-__global__ void __launch_bounds__(kThreads, BFP_ARITH_MINB) k_arith(const w32* __restrict__ x,
+constexpr int arith_minb() {
+  if constexpr (Gen<F, OP>::ok) {
+    constexpr int l = Gen<F, OP>::luts;
+    if ((OP == OP_MUL || OP == OP_DIV) && l >= 300 && l <= 800) return 6;
+  }
+  return BFP_ARITH_MINB;
+}
+
+template <class F, int OP>
+__global__ void __launch_bounds__(kThreads, arith_minb<F, OP>()) k_arith(const w32* __restrict__ x,
                                                     const w32* __restrict__ y,
                                                     const w32* __restrict__ c,
                                                     w32* __restrict__ z, size_t units) {
