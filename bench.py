@@ -783,6 +783,9 @@ def main_ours(args) -> None:
         peaks = measured_peaks()
         per_op = {}
         roofs = []
+        tfile = ROOT / "profiles" / "ncu_traffic.json"
+        tmap = json.loads(tfile.read_text()) if tfile.exists() else {}
+        tsuf = "" if MODE == (1, 0) else f":{mode_text()}"
         for j, ms in zip(jobs, res["kern_ms"]):
             dur = ms * 1e-3
             ach = j.algo_bytes / dur / 1e9
@@ -801,14 +804,14 @@ def main_ours(args) -> None:
                                                                             res["clocks"]),
                                 "binding": "logic" if logic_t > hbm_t else "hbm",
                                 "frac_of_binding": round(max(hbm_t, logic_t) / dur, 4)})
+            tr = tmap.get(f"{cfg}:{j.label}{tsuf}")
+            if tr is not None:
+                ent["traffic"] = tr
+                ent["traffic_over_algorithmic"] = round(tr / j.algo_bytes, 3)
             per_op[j.label] = ent
             roofs.append((ms, j, ach))
         ms_dom, jd, ach = max(roofs, key=lambda r: r[0])
-        traffic = None
-        tfile = ROOT / "profiles" / "ncu_traffic.json"
-        if tfile.exists():
-            key = f"{cfg}:{jd.label}" + ("" if MODE == (1, 0) else f":{mode_text()}")
-            traffic = json.loads(tfile.read_text()).get(key)
+        traffic = tmap.get(f"{cfg}:{jd.label}{tsuf}")
         roof = {"bound": "hbm", "kernel": f"{jd.label} (1/{jd.spec.exp_bits}/{jd.spec.sig_bits} {mode_text()})",
                 "achieved": round(ach, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": round(ach / peaks["hbm_gbs"], 4), "traffic": traffic,
