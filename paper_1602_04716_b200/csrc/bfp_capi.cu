@@ -337,12 +337,18 @@ bfp_status bfp_kernel_attrs(const bfp_format* f, int kernel, int* regs, int* cta
 uint64_t bfp_launch_count(void) { return g_launches.load(); }
 
 // ------------------------------------------------------------ host pipeline
+// Three streams in a fixed order: every H2D copy on s_in, every kernel on
+// s_k, every D2H copy on s_out, with one event per stage and buffer slot.
+// Copies of one direction therefore run strictly in chunk order (chunk 0's
+// inputs arrive at the full link rate instead of sharing it with the chunks
+// behind it), so the pipeline fills in one chunk time and drains in one.
 struct bfp_host_ctx {
-  static constexpr int kDepth = 4;   // chunks in flight (one stream each)
+  static constexpr int kDepth = 4;   // buffer slots (chunks in flight)
   static constexpr int kMaxOut = 8;  // outputs per chunk (batched ops)
   size_t chunk_blocks = 0;
   size_t cap_bytes = 0;  // per buffer
-  cudaStream_t st[kDepth] = {};
+  cudaStream_t s_in = nullptr, s_k = nullptr, s_out = nullptr;
+  cudaEvent_t in_done[kDepth] = {}, k_done[kDepth] = {}, out_done[kDepth] = {};
   void* in[kDepth][3] = {};
   void* out[kDepth][kMaxOut] = {};
   int dev = 0;
@@ -360,8 +366,11 @@ bfp_host_ctx* bfp_host_ctx_create(size_t chunk_elems) {
   // sized for the widest case: 32 planes or float32 elements
   c->cap_bytes = c->chunk_blocks * 1024 * 4;
   cudaGetDevice(&c->dev);
+  for (cudaStream_t* st : {&c->s_in, &c->s_k, &c->s_out})
+    if (cudaStreamCreateWithFlags(st, cudaStreamNonBlocking) != cudaSuccess) goto bad;
   for (int i = 0; i < bfp_host_ctx::kDepth; ++i) {
-    if (cudaStreamCreateWithFlags(&c->st[i], cudaStreamNonBlocking) != cudaSuccess) goto bad;
+    for (cudaEvent_t* ev : {&c->in_done[i], &c->k_done[i], &c->out_done[i]})
+      if (cudaEventCreateWithFlags(ev, cudaEventDisableTiming) != cudaSuccess) goto bad;
     for (int k = 0; k < 3; ++k)
       if (cudaMalloc(&c->in[i][k], c->cap_bytes) != cudaSuccess) goto bad;
     if (!c->out_buf(i, 0)) goto bad;
@@ -375,14 +384,18 @@ bad:
 
 void bfp_host_ctx_destroy(bfp_host_ctx* c) {
   if (!c) return;
+  for (cudaStream_t st : {c->s_in, c->s_k, c->s_out})
+    if (st) cudaStreamSynchronize(st);
   for (int i = 0; i < bfp_host_ctx::kDepth; ++i) {
-    if (c->st[i]) cudaStreamSynchronize(c->st[i]);
     for (int k = 0; k < 3; ++k)
       if (c->in[i][k]) cudaFree(c->in[i][k]);
     for (int k = 0; k < bfp_host_ctx::kMaxOut; ++k)
       if (c->out[i][k]) cudaFree(c->out[i][k]);
-    if (c->st[i]) cudaStreamDestroy(c->st[i]);
+    for (cudaEvent_t ev : {c->in_done[i], c->k_done[i], c->out_done[i]})
+      if (ev) cudaEventDestroy(ev);
   }
+  for (cudaStream_t st : {c->s_in, c->s_k, c->s_out})
+    if (st) cudaStreamDestroy(st);
   delete c;
 }
 
@@ -391,48 +404,77 @@ void bfp_host_ctx_destroy(bfp_host_ctx* c) {
 namespace {
 
 // Chunk size of one call: the context's chunk, but small enough that the call
-// splits into >= 2 x depth chunks (a 2^24-element call in one 2^24 chunk runs
-// H2D, kernel and D2H back to back), and never below 1024 blocks (2^20
-// elements) so per-copy overhead stays small.
+// splits into >= 16 chunks (fill and drain cost one chunk each), and never
+// below 512 blocks (2^19 elements) so per-copy overhead stays small.
 size_t chunk_for(const bfp_host_ctx* c, size_t blocks) {
-  constexpr size_t kMinBlocks = 1024;
-  const size_t split = (blocks + 2 * bfp_host_ctx::kDepth - 1) / (2 * bfp_host_ctx::kDepth);
+  constexpr size_t kMinBlocks = 512, kMinChunks = 16;
+  const size_t split = (blocks + kMinChunks - 1) / kMinChunks;
   size_t cb = split < kMinBlocks ? kMinBlocks : split;
   return cb < c->chunk_blocks ? cb : c->chunk_blocks;
 }
 
-// Generic chunked pipeline: chunk k uses stream/buffer set k % depth, so the
-// H2D of chunk k+1, the kernel of chunk k and the D2H of chunk k-1 overlap.
-// in_stride / out_stride: bytes per 1024-element block on each side.
-template <typename Body>
-bfp_status host_pipeline(bfp_host_ctx* c, size_t count, int n_in, const void* const* h_in,
-                         size_t in_stride, void* h_out, size_t out_stride, bool out_elems,
-                         Body body) {
+struct Chunk {
+  int slot;
+  size_t b0, nb;  // first block, blocks
+  size_t e0, ne;  // first element, elements
+};
+
+// Generic pipeline over the chunks of `count` elements.
+//   in_bytes(ch, a, &src, &bytes)  -> host source / size of input a
+//   body(ch, st)                   -> kernel launches on st (slot buffers)
+//   out_bytes(ch, q, &dst, &bytes) -> host destination / size of output q
+template <typename In, typename Body, typename Out>
+bfp_status host_pipeline(bfp_host_ctx* c, size_t count, int n_in, int n_out, In in_bytes,
+                         Body body, Out out_bytes) {
   if (!c) return fail(BFP_EARG, "null host context");
+  for (int q = 0; q < n_out; ++q)
+    for (int i = 0; i < bfp_host_ctx::kDepth; ++i)
+      if (!c->out_buf(i, q)) return fail(BFP_ECUDA, "host ctx: output buffer allocation failed");
   const size_t blocks = nblocks(count);
   const size_t cb = chunk_for(c, blocks);
+  bool used[bfp_host_ctx::kDepth] = {};
+  cudaError_t e = cudaSuccess;
   for (size_t b0 = 0, k = 0; b0 < blocks; b0 += cb, ++k) {
-    const int i = int(k % bfp_host_ctx::kDepth);
-    const size_t nb = (blocks - b0 < cb) ? blocks - b0 : cb;
-    const size_t e0 = b0 * 1024;
-    const size_t ecount = (count - e0 < nb * 1024) ? count - e0 : nb * 1024;
+    Chunk ch;
+    ch.slot = int(k % bfp_host_ctx::kDepth);
+    ch.b0 = b0;
+    ch.nb = (blocks - b0 < cb) ? blocks - b0 : cb;
+    ch.e0 = b0 * 1024;
+    ch.ne = (count - ch.e0 < ch.nb * 1024) ? count - ch.e0 : ch.nb * 1024;
+    const int i = ch.slot;
+    // inputs of slot i are free once its previous kernels are done
+    if (used[i] && (e = cudaStreamWaitEvent(c->s_in, c->k_done[i], 0)) != cudaSuccess)
+      return cuda_status(e, "wait");
     for (int a = 0; a < n_in; ++a) {
-      const size_t bytes = in_stride ? nb * in_stride : ecount * 4;
-      const char* src = static_cast<const char*>(h_in[a]) + (in_stride ? b0 * in_stride : e0 * 4);
-      cudaError_t e = cudaMemcpyAsync(c->in[i][a], src, bytes, cudaMemcpyHostToDevice, c->st[i]);
-      if (e != cudaSuccess) return cuda_status(e, "H2D");
+      const void* src;
+      size_t bytes;
+      in_bytes(ch, a, &src, &bytes);
+      if ((e = cudaMemcpyAsync(c->in[i][a], src, bytes, cudaMemcpyHostToDevice, c->s_in)) !=
+          cudaSuccess)
+        return cuda_status(e, "H2D");
     }
-    const bfp_status s = body(i, ecount, c->st[i]);
+    if ((e = cudaEventRecord(c->in_done[i], c->s_in)) != cudaSuccess) return cuda_status(e, "record");
+    if ((e = cudaStreamWaitEvent(c->s_k, c->in_done[i], 0)) != cudaSuccess) return cuda_status(e, "wait");
+    // outputs of slot i are free once its previous D2H copies are done
+    if (used[i] && (e = cudaStreamWaitEvent(c->s_k, c->out_done[i], 0)) != cudaSuccess)
+      return cuda_status(e, "wait");
+    const bfp_status s = body(ch, c->s_k);
     if (s != BFP_OK) return s;
-    const size_t obytes = out_elems ? ecount * 4 : nb * out_stride;
-    char* dst = static_cast<char*>(h_out) + (out_elems ? e0 * 4 : b0 * out_stride);
-    cudaError_t e = cudaMemcpyAsync(dst, c->out[i][0], obytes, cudaMemcpyDeviceToHost, c->st[i]);
-    if (e != cudaSuccess) return cuda_status(e, "D2H");
+    if ((e = cudaEventRecord(c->k_done[i], c->s_k)) != cudaSuccess) return cuda_status(e, "record");
+    if ((e = cudaStreamWaitEvent(c->s_out, c->k_done[i], 0)) != cudaSuccess) return cuda_status(e, "wait");
+    for (int q = 0; q < n_out; ++q) {
+      void* dst;
+      size_t bytes;
+      out_bytes(ch, q, &dst, &bytes);
+      if ((e = cudaMemcpyAsync(dst, c->out[i][q], bytes, cudaMemcpyDeviceToHost, c->s_out)) !=
+          cudaSuccess)
+        return cuda_status(e, "D2H");
+    }
+    if ((e = cudaEventRecord(c->out_done[i], c->s_out)) != cudaSuccess) return cuda_status(e, "record");
+    used[i] = true;
   }
-  for (int i = 0; i < bfp_host_ctx::kDepth; ++i) {
-    cudaError_t e = cudaStreamSynchronize(c->st[i]);
-    if (e != cudaSuccess) return cuda_status(e, "sync");
-  }
+  for (cudaStream_t st : {c->s_in, c->s_k, c->s_out})
+    if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return cuda_status(e, "sync");
   return BFP_OK;
 }
 
@@ -443,23 +485,9 @@ extern "C" {
 bfp_status bfp_arith_host(bfp_host_ctx* c, int op, const bfp_format* f, const uint32_t* h_x,
                           const uint32_t* h_y, const uint32_t* h_c, uint32_t* h_z,
                           size_t count) {
-  const Impl* impl = nullptr;
-  bfp_status s = resolve(f, &impl);
-  if (s != BFP_OK) return s;
-  if (op < 0 || op > 4) return fail(BFP_EARG, "bad op");
-  if (!h_x || !h_y || !h_z || (op == 4 && !h_c)) return fail(BFP_EARG, "null operand");
-  const size_t stride = nplanes(f) * 128;
-  const void* ins[3] = {h_x, h_y, h_c};
-  return host_pipeline(c, count, op == 4 ? 3 : 2, ins, stride, h_z, stride, false,
-                       [&](int i, size_t ecount, cudaStream_t st) {
-                         ++g_launches;
-                         return cuda_status(
-                             impl->arith(op, static_cast<const uint32_t*>(c->in[i][0]),
-                                         static_cast<const uint32_t*>(c->in[i][1]),
-                                         static_cast<const uint32_t*>(c->in[i][2]),
-                                         static_cast<uint32_t*>(c->out[i][0]), nblocks(ecount), st),
-                             "arith launch");
-                       });
+  const int ops[1] = {op};
+  uint32_t* outs[1] = {h_z};
+  return bfp_arith_host_batch(c, 1, ops, f, h_x, h_y, h_c, outs, count);
 }
 
 // Several ops over the SAME host operands: each chunk's inputs cross PCIe
@@ -481,42 +509,31 @@ bfp_status bfp_arith_host_batch(bfp_host_ctx* c, int nops, const int* ops, const
   }
   if (!h_x || !h_y || (need_c && !h_c)) return fail(BFP_EARG, "null operand");
   const size_t stride = nplanes(f) * 128;
-  const size_t blocks = nblocks(count);
-  const size_t cb = chunk_for(c, blocks);
-  // per chunk: inputs into in[i][0..2], op q's result into out[i][q] (own
-  // buffer, so op q+1's kernel does not wait for op q's D2H)
-  for (size_t b0 = 0, k = 0; b0 < blocks; b0 += cb, ++k) {
-    const int i = int(k % bfp_host_ctx::kDepth);
-    const size_t nb = (blocks - b0 < cb) ? blocks - b0 : cb;
-    const size_t bytes = nb * stride;
-    const void* ins[3] = {h_x, h_y, h_c};
-    for (int a = 0; a < (need_c ? 3 : 2); ++a) {
-      cudaError_t e = cudaMemcpyAsync(c->in[i][a], static_cast<const char*>(ins[a]) + b0 * stride,
-                                      bytes, cudaMemcpyHostToDevice, c->st[i]);
-      if (e != cudaSuccess) return cuda_status(e, "H2D");
-    }
-    for (int q = 0; q < nops; ++q) {
-      void* ob = c->out_buf(i, q);
-      if (!ob) return fail(BFP_ECUDA, "host ctx: output buffer allocation failed");
-      ++g_launches;
-      s = cuda_status(impl->arith(ops[q], static_cast<const uint32_t*>(c->in[i][0]),
-                                  static_cast<const uint32_t*>(c->in[i][1]),
-                                  static_cast<const uint32_t*>(c->in[i][2]),
-                                  static_cast<uint32_t*>(ob), nb, c->st[i]),
-                      "arith launch");
-      if (s != BFP_OK) return s;
-    }
-    for (int q = 0; q < nops; ++q) {
-      cudaError_t e = cudaMemcpyAsync(reinterpret_cast<char*>(h_z[q]) + b0 * stride, c->out[i][q],
-                                      bytes, cudaMemcpyDeviceToHost, c->st[i]);
-      if (e != cudaSuccess) return cuda_status(e, "D2H");
-    }
-  }
-  for (int i = 0; i < bfp_host_ctx::kDepth; ++i) {
-    cudaError_t e = cudaStreamSynchronize(c->st[i]);
-    if (e != cudaSuccess) return cuda_status(e, "sync");
-  }
-  return BFP_OK;
+  const void* ins[3] = {h_x, h_y, h_c};
+  return host_pipeline(
+      c, count, need_c ? 3 : 2, nops,
+      [&](const Chunk& ch, int a, const void** src, size_t* bytes) {
+        *src = static_cast<const char*>(ins[a]) + ch.b0 * stride;
+        *bytes = ch.nb * stride;
+      },
+      [&](const Chunk& ch, cudaStream_t st) {
+        const int i = ch.slot;
+        for (int q = 0; q < nops; ++q) {
+          ++g_launches;
+          const bfp_status r = cuda_status(
+              impl->arith(ops[q], static_cast<const uint32_t*>(c->in[i][0]),
+                          static_cast<const uint32_t*>(c->in[i][1]),
+                          static_cast<const uint32_t*>(c->in[i][2]),
+                          static_cast<uint32_t*>(c->out[i][q]), ch.nb, st),
+              "arith launch");
+          if (r != BFP_OK) return r;
+        }
+        return BFP_OK;
+      },
+      [&](const Chunk& ch, int q, void** dst, size_t* bytes) {
+        *dst = reinterpret_cast<char*>(h_z[q]) + ch.b0 * stride;
+        *bytes = ch.nb * stride;
+      });
 }
 
 bfp_status bfp_pack_f32_host(bfp_host_ctx* c, const bfp_format* f, const float* h_in,
@@ -525,15 +542,23 @@ bfp_status bfp_pack_f32_host(bfp_host_ctx* c, const bfp_format* f, const float* 
   bfp_status s = resolve(f, &impl);
   if (s != BFP_OK) return s;
   if (!h_in || !h_planes) return fail(BFP_EARG, "null buffer");
-  const void* ins[1] = {h_in};
-  return host_pipeline(c, count, 1, ins, 0, h_planes, nplanes(f) * 128, false,
-                       [&](int i, size_t ecount, cudaStream_t st) {
-                         ++g_launches;
-                         return cuda_status(impl->pack_f32(static_cast<const float*>(c->in[i][0]),
-                                                           static_cast<uint32_t*>(c->out[i][0]),
-                                                           ecount, st),
-                                            "pack_f32 launch");
-                       });
+  const size_t stride = nplanes(f) * 128;
+  return host_pipeline(
+      c, count, 1, 1,
+      [&](const Chunk& ch, int, const void** src, size_t* bytes) {
+        *src = h_in + ch.e0;
+        *bytes = ch.ne * 4;
+      },
+      [&](const Chunk& ch, cudaStream_t st) {
+        ++g_launches;
+        return cuda_status(impl->pack_f32(static_cast<const float*>(c->in[ch.slot][0]),
+                                          static_cast<uint32_t*>(c->out[ch.slot][0]), ch.ne, st),
+                           "pack_f32 launch");
+      },
+      [&](const Chunk& ch, int, void** dst, size_t* bytes) {
+        *dst = reinterpret_cast<char*>(h_planes) + ch.b0 * stride;
+        *bytes = ch.nb * stride;
+      });
 }
 
 bfp_status bfp_unpack_f32_host(bfp_host_ctx* c, const bfp_format* f, const uint32_t* h_planes,
@@ -542,15 +567,23 @@ bfp_status bfp_unpack_f32_host(bfp_host_ctx* c, const bfp_format* f, const uint3
   bfp_status s = resolve(f, &impl);
   if (s != BFP_OK) return s;
   if (!h_out || !h_planes) return fail(BFP_EARG, "null buffer");
-  const void* ins[1] = {h_planes};
-  return host_pipeline(c, count, 1, ins, nplanes(f) * 128, h_out, 0, true,
-                       [&](int i, size_t ecount, cudaStream_t st) {
-                         ++g_launches;
-                         return cuda_status(
-                             impl->unpack_f32(static_cast<const uint32_t*>(c->in[i][0]),
-                                              static_cast<float*>(c->out[i][0]), ecount, st),
-                             "unpack_f32 launch");
-                       });
+  const size_t stride = nplanes(f) * 128;
+  return host_pipeline(
+      c, count, 1, 1,
+      [&](const Chunk& ch, int, const void** src, size_t* bytes) {
+        *src = reinterpret_cast<const char*>(h_planes) + ch.b0 * stride;
+        *bytes = ch.nb * stride;
+      },
+      [&](const Chunk& ch, cudaStream_t st) {
+        ++g_launches;
+        return cuda_status(impl->unpack_f32(static_cast<const uint32_t*>(c->in[ch.slot][0]),
+                                            static_cast<float*>(c->out[ch.slot][0]), ch.ne, st),
+                           "unpack_f32 launch");
+      },
+      [&](const Chunk& ch, int, void** dst, size_t* bytes) {
+        *dst = h_out + ch.e0;
+        *bytes = ch.ne * 4;
+      });
 }
 
 void* bfp_host_alloc(size_t bytes) {

@@ -27,7 +27,13 @@ enum Op { OP_ADD = 0, OP_SUB = 1, OP_MUL = 2, OP_DIV = 3, OP_MUL_ADD = 4 };
 
 constexpr int kThreads = 128;
 
+#if defined(BFP_LDST_PLAIN)
+__device__ __forceinline__ w32 ld_stream(const w32* p) { return *p; }
+#elif defined(BFP_LDST_NC)
+__device__ __forceinline__ w32 ld_stream(const w32* p) { return __ldg(p); }
+#else
 __device__ __forceinline__ w32 ld_stream(const w32* p) { return __ldcs(p); }
+#endif
 
 // Programmatic dependent launch: every kernel waits for the previous grid to
 // complete -- memory included -- before its first global access (so
@@ -52,7 +58,24 @@ __device__ __forceinline__ void pdl_release() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 #endif
 }
+// The same release issued from inside a grid-stride loop, by each thread
+// after the stores of its last unit.  A release after the
+// loop makes ptxas re-materialise the memory descriptor into a fresh uniform
+// register pair (R2UR) for every LDG/STG of the body -- 72 extra ALU-pipe
+// instructions per unit on 1/5/10 mul, ~11% of a logic-bound kernel; issued
+// under a predicate inside the loop it does not.  Dependents only start once
+// every thread has released or exited, and their griddepcontrol.wait still
+// waits for this grid's completion, so the timing is all that changes.
+__device__ __forceinline__ void pdl_release_if(bool last) {
+#if !BFP_PDL_EARLY
+  if (last) asm volatile("griddepcontrol.launch_dependents;");
+#endif
+}
+#if defined(BFP_LDST_PLAIN) || defined(BFP_LDST_NC)
+__device__ __forceinline__ void st_stream(w32* p, w32 v) { *p = v; }
+#else
 __device__ __forceinline__ void st_stream(w32* p, w32 v) { __stcs(p, v); }
+#endif
 
 // Operands of one unit: NIN inputs x N planes, loaded with the streaming path.
 template <int N, int NIN>
@@ -97,11 +120,14 @@ __device__ __forceinline__ void eval_unit(const w32* X, const w32* Y, const w32*
 // costs no spills and measured +10% on 1/8/7 mul, +2-5% on 1/5/10 mul.  Small
 // networks are HBM-bound (the cap measured -2..-3% there) and the widest
 // (1/8/15 mul, mul_add) gained nothing.
+#ifndef BFP_MID_MINB
+#define BFP_MID_MINB 6
+#endif
 template <class F, int OP>
 constexpr int arith_minb() {
   if constexpr (Gen<F, OP>::ok) {
     constexpr int l = Gen<F, OP>::luts;
-    if ((OP == OP_MUL || OP == OP_DIV) && l >= 300 && l <= 800) return 6;
+    if ((OP == OP_MUL || OP == OP_DIV) && l >= 300 && l <= 800) return BFP_MID_MINB;
   }
   return BFP_ARITH_MINB;
 }
@@ -119,11 +145,15 @@ __global__ void __launch_bounds__(kThreads, arith_minb<F, OP>()) k_arith(const w
     const size_t base = (u >> 5) * (size_t(N) * 32) + (u & 31);
     Operands<N, NIN> cur;
     cur.load(x, y, c, base);
+    // register-capped networks: releasing before the network keeps the
+    // loop-carried values out of local memory (ptxas spilled 20-24 B of the
+    // 1/5/10 and 1/6/9 mul loops with the release after the stores)
+    if constexpr (arith_minb<F, OP>() > 1) pdl_release_if(u + stride >= units);
     w32 Z[N];
     eval_unit<F, OP>(cur.v[0], cur.v[1], cur.v[NIN - 1], Z);
     BFP_UNROLL for (int j = 0; j < N; ++j) st_stream(z + base + j * 32, Z[j]);
+    if constexpr (arith_minb<F, OP>() <= 1) pdl_release_if(u + stride >= units);
   }
-  pdl_release();
 }
 
 // ---------------------------------------------- bulk-copy pipelined variant
@@ -421,8 +451,8 @@ __global__ void __launch_bounds__(kThreads) k_pack_enc(const uint8_t* __restrict
     elems_to_planes<EB>(L, P);
     const size_t base = (u >> 5) * (size_t(N) * 32) + (u & 31);
     BFP_UNROLL for (int j = 0; j < N; ++j) st_stream(planes + base + j * 32, P[j]);
+    pdl_release_if(u + stride >= units);
   }
-  pdl_release();
 }
 
 template <int N, int EB>
@@ -443,8 +473,8 @@ __global__ void __launch_bounds__(kThreads) k_unpack_enc(const w32* __restrict__
     w32 L[8 * EB];
     planes_to_elems<EB>(P, L);
     warp_store_elems<EB>(enc, u, n, aligned, tile, lane, L);
+    pdl_release_if(u + stride >= wunits);
   }
-  pdl_release();
 }
 
 // 32 float32 bit patterns of one unit -> the unit's N plane words (encode_scalar
@@ -530,8 +560,8 @@ __global__ void __launch_bounds__(kThreads) k_pack_f32(const float* __restrict__
     floats_to_planes<F>(V, P);
     const size_t base = (u >> 5) * (size_t(N) * 32) + (u & 31);
     BFP_UNROLL for (int j = 0; j < N; ++j) st_stream(planes + base + j * 32, P[j]);
+    pdl_release_if(u + stride >= units);
   }
-  pdl_release();
 }
 
 // planes -> decode_scalar -> float32.
@@ -554,8 +584,8 @@ __global__ void __launch_bounds__(kThreads) k_unpack_f32(const w32* __restrict__
     w32 V[32];
     planes_to_floats<F>(P, V);
     warp_store_elems<4>(outb, u, n, aligned, tile, lane, V);
+    pdl_release_if(u + stride >= wunits);
   }
-  pdl_release();
 }
 
 // binary64 -> encode_scalar -> planes (format.hpp:125-188, the reference
@@ -583,8 +613,8 @@ __global__ void __launch_bounds__(kThreads) k_pack_f64(const double* __restrict_
     elems_to_planes<8>(L, P);
     const size_t base = (u >> 5) * (size_t(N) * 32) + (u & 31);
     BFP_UNROLL for (int j = 0; j < N; ++j) st_stream(planes + base + j * 32, P[j]);
+    pdl_release_if(u + stride >= units);
   }
-  pdl_release();
 }
 
 // planes -> decode_scalar -> binary64 (exact).
@@ -612,8 +642,8 @@ __global__ void __launch_bounds__(kThreads) k_unpack_f64(const w32* __restrict__
       L[2 * k + 1] = w32(d >> 32);
     }
     warp_store_elems<8>(outb, u, n, aligned, tile, lane, L);
+    pdl_release_if(u + stride >= wunits);
   }
-  pdl_release();
 }
 
 // Fused float32-in / float32-out arithmetic: the
@@ -649,8 +679,8 @@ __global__ void __launch_bounds__(kThreads) k_arith_f32(const float* __restrict_
     w32 V[32];
     planes_to_floats<F>(P, V);
     warp_store_elems<4>(reinterpret_cast<uint8_t*>(z), u, n, aligned, tile, lane, V);
+    pdl_release_if(u + stride >= units);
   }
-  pdl_release();
 }
 
 // ------------------------------------------------------- launch + table

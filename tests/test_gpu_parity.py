@@ -481,3 +481,24 @@ def test_host_batch_matches_device(oracle):
         L.bfp_host_ctx_destroy(ctx)
     for o, op in zip(outs, ("mul", "sub", "div")):
         assert np.array_equal(oracle.unpack_planes(o, n, 8), oracle.binop(op, fmt, x, y)), op
+
+
+@pytest.mark.gpu
+def test_host_mul_add_many_chunks(oracle):
+    """Three-input host pipeline (mul_add) over more chunks than buffer slots:
+    slot reuse is ordered by the k_done / out_done events."""
+    L = _lib.lib()
+    fmt = (6, 9, 1, 0)
+    n = 11 * (1 << 19) + 4321
+    rng = np.random.default_rng(12)
+    a, b, c = (operands(6, 9, n, rng) for _ in range(3))
+    pa, pb, pc = (oracle.pack_planes(v, 16) for v in (a, b, c))
+    pz = np.zeros_like(pa)
+    ctx = L.bfp_host_ctx_create(1 << 19)
+    try:
+        f = cfmt(fmt)
+        assert L.bfp_arith_host(ctx, 4, C.byref(f), pa.ctypes.data, pb.ctypes.data, pc.ctypes.data,
+                                pz.ctypes.data, n) == 0
+    finally:
+        L.bfp_host_ctx_destroy(ctx)
+    assert np.array_equal(oracle.unpack_planes(pz, n, 16), oracle.binop("mul_add", fmt, a, b, c))
