@@ -866,9 +866,10 @@ def main_ours(args) -> None:
                            "unit": UNIT, "h2d_bytes_per_step": int(e2e["h2d"]),
                            "d2h_bytes_per_step": int(e2e["d2h"]),
                            "path": "C ABI host entry points (bfp_arith_host_batch / "
-                                   "bfp_pack_f32_host / bfp_unpack_f32_host: pinned host buffers, "
-                                   "chunked H2D / kernel / D2H on 3 streams; ops sharing operands "
-                                   "copy them once)",
+                                   "bfp_pack_f32_host / bfp_unpack_f32_host: pinned host buffers; "
+                                   "inputs copied H2D in chunk order on one stream, kernels on a "
+                                   "second write each chunk's results in place into the pinned "
+                                   "host outputs over PCIe; ops sharing operands copy them once)",
                            "steps": e2e["steps"]}
         if rank == 0 and world == 1 and not args.no_cpu_baseline:
             log("cpu baseline")

@@ -346,6 +346,7 @@ struct bfp_host_ctx {
   static constexpr int kDepth = 4;   // buffer slots (chunks in flight)
   static constexpr int kMaxOut = 8;  // outputs per chunk (batched ops)
   size_t chunk_blocks = 0;
+  size_t min_chunks = 8;  // a call splits into at least this many chunks
   size_t cap_bytes = 0;  // per buffer
   cudaStream_t s_in = nullptr, s_k = nullptr, s_out = nullptr;
   cudaEvent_t in_done[kDepth] = {}, k_done[kDepth] = {}, out_done[kDepth] = {};
@@ -363,6 +364,10 @@ bfp_host_ctx* bfp_host_ctx_create(size_t chunk_elems) {
   if (!chunk_elems) chunk_elems = size_t(1) << 22;
   auto* c = new bfp_host_ctx;
   c->chunk_blocks = (chunk_elems + 1023) / 1024;
+  if (const char* v = getenv("BFP_HOST_MIN_CHUNKS")) {  // tuning knob
+    const long m = atol(v);
+    if (m >= 1) c->min_chunks = size_t(m);
+  }
   // sized for the widest case: 32 planes or float32 elements
   c->cap_bytes = c->chunk_blocks * 1024 * 4;
   cudaGetDevice(&c->dev);
@@ -404,11 +409,11 @@ void bfp_host_ctx_destroy(bfp_host_ctx* c) {
 namespace {
 
 // Chunk size of one call: the context's chunk, but small enough that the call
-// splits into >= 16 chunks (fill and drain cost one chunk each), and never
-// below 512 blocks (2^19 elements) so per-copy overhead stays small.
+// splits into >= min_chunks chunks (fill and drain cost one chunk each), and
+// never below 512 blocks (2^19 elements) so per-copy overhead stays small.
 size_t chunk_for(const bfp_host_ctx* c, size_t blocks) {
-  constexpr size_t kMinBlocks = 512, kMinChunks = 16;
-  const size_t split = (blocks + kMinChunks - 1) / kMinChunks;
+  constexpr size_t kMinBlocks = 512;
+  const size_t split = (blocks + c->min_chunks - 1) / c->min_chunks;
   size_t cb = split < kMinBlocks ? kMinBlocks : split;
   return cb < c->chunk_blocks ? cb : c->chunk_blocks;
 }
@@ -419,17 +424,58 @@ struct Chunk {
   size_t e0, ne;  // first element, elements
 };
 
+// Device-accessible alias of a host address when it lies in page-locked,
+// mapped memory (bfp_host_alloc / cudaMallocHost / cudaHostRegister), else null.
+void* mapped_alias(void* h) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, h) != cudaSuccess) {
+    cudaGetLastError();  // pageable memory on older runtimes reports an error
+    return nullptr;
+  }
+  if (a.type != cudaMemoryTypeHost || !a.devicePointer || !a.hostPointer) return nullptr;
+  return static_cast<char*>(a.devicePointer) + (static_cast<char*>(h) - static_cast<char*>(a.hostPointer));
+}
+
 // Generic pipeline over the chunks of `count` elements.
 //   in_bytes(ch, a, &src, &bytes)  -> host source / size of input a
-//   body(ch, st)                   -> kernel launches on st (slot buffers)
 //   out_bytes(ch, q, &dst, &bytes) -> host destination / size of output q
+//   body(ch, outs, st)             -> kernel launches on st, reading the slot's
+//                                     input buffers, writing outs[q]
+// Inputs are copied H2D in chunk order on s_in.  Outputs in page-locked
+// mapped host memory of calls up to kDirectMaxBytes are written by the
+// kernels in place (the stores cross PCIe as the kernel runs: no D2H copy
+// stage); otherwise they land in the slot's device buffers and are copied
+// D2H in chunk order on s_out.
 template <typename In, typename Body, typename Out>
 bfp_status host_pipeline(bfp_host_ctx* c, size_t count, int n_in, int n_out, In in_bytes,
                          Body body, Out out_bytes) {
   if (!c) return fail(BFP_EARG, "null host context");
-  for (int q = 0; q < n_out; ++q)
-    for (int i = 0; i < bfp_host_ctx::kDepth; ++i)
-      if (!c->out_buf(i, q)) return fail(BFP_ECUDA, "host ctx: output buffer allocation failed");
+  if (count == 0) return BFP_OK;
+  // In-place writes cross PCIe at ~52.6 GB/s against ~57 GB/s for a D2H copy
+  // (B200 box, tools/pcie_probe.py) but drop the copy stage's per-chunk
+  // event hops and its drain: they win on calls whose output is small next
+  // to that fixed cost (2^24 fp8 add +10%, 2^26 mul+sub +2.5%) and lose on
+  // large ones (2^28 float32 unpack -6%), hence the size cut-off.
+  constexpr size_t kDirectMaxBytes = size_t(256) << 20;
+  bool direct = true;
+  {
+    const Chunk ch0{0, 0, 1, 0, 1};
+    const Chunk all{0, 0, nblocks(count), 0, count};
+    size_t total = 0;
+    for (int q = 0; q < n_out && direct; ++q) {
+      void* dst;
+      size_t bytes;
+      out_bytes(ch0, q, &dst, &bytes);
+      direct = mapped_alias(dst) != nullptr;
+      out_bytes(all, q, &dst, &bytes);
+      total += bytes;
+    }
+    direct = direct && total <= kDirectMaxBytes;
+  }
+  if (!direct)
+    for (int q = 0; q < n_out; ++q)
+      for (int i = 0; i < bfp_host_ctx::kDepth; ++i)
+        if (!c->out_buf(i, q)) return fail(BFP_ECUDA, "host ctx: output buffer allocation failed");
   const size_t blocks = nblocks(count);
   const size_t cb = chunk_for(c, blocks);
   bool used[bfp_host_ctx::kDepth] = {};
@@ -455,22 +501,37 @@ bfp_status host_pipeline(bfp_host_ctx* c, size_t count, int n_in, int n_out, In 
     }
     if ((e = cudaEventRecord(c->in_done[i], c->s_in)) != cudaSuccess) return cuda_status(e, "record");
     if ((e = cudaStreamWaitEvent(c->s_k, c->in_done[i], 0)) != cudaSuccess) return cuda_status(e, "wait");
+    void* outs[bfp_host_ctx::kMaxOut];
+    for (int q = 0; q < n_out; ++q) {
+      if (direct) {
+        void* dst;
+        size_t bytes;
+        out_bytes(ch, q, &dst, &bytes);
+        outs[q] = mapped_alias(dst);
+      } else {
+        outs[q] = c->out[i][q];
+      }
+    }
     // outputs of slot i are free once its previous D2H copies are done
-    if (used[i] && (e = cudaStreamWaitEvent(c->s_k, c->out_done[i], 0)) != cudaSuccess)
+    if (!direct && used[i] && (e = cudaStreamWaitEvent(c->s_k, c->out_done[i], 0)) != cudaSuccess)
       return cuda_status(e, "wait");
-    const bfp_status s = body(ch, c->s_k);
+    const bfp_status s = body(ch, outs, c->s_k);
     if (s != BFP_OK) return s;
     if ((e = cudaEventRecord(c->k_done[i], c->s_k)) != cudaSuccess) return cuda_status(e, "record");
-    if ((e = cudaStreamWaitEvent(c->s_out, c->k_done[i], 0)) != cudaSuccess) return cuda_status(e, "wait");
-    for (int q = 0; q < n_out; ++q) {
-      void* dst;
-      size_t bytes;
-      out_bytes(ch, q, &dst, &bytes);
-      if ((e = cudaMemcpyAsync(dst, c->out[i][q], bytes, cudaMemcpyDeviceToHost, c->s_out)) !=
-          cudaSuccess)
-        return cuda_status(e, "D2H");
+    if (!direct) {
+      if ((e = cudaStreamWaitEvent(c->s_out, c->k_done[i], 0)) != cudaSuccess)
+        return cuda_status(e, "wait");
+      for (int q = 0; q < n_out; ++q) {
+        void* dst;
+        size_t bytes;
+        out_bytes(ch, q, &dst, &bytes);
+        if ((e = cudaMemcpyAsync(dst, c->out[i][q], bytes, cudaMemcpyDeviceToHost, c->s_out)) !=
+            cudaSuccess)
+          return cuda_status(e, "D2H");
+      }
+      if ((e = cudaEventRecord(c->out_done[i], c->s_out)) != cudaSuccess)
+        return cuda_status(e, "record");
     }
-    if ((e = cudaEventRecord(c->out_done[i], c->s_out)) != cudaSuccess) return cuda_status(e, "record");
     used[i] = true;
   }
   for (cudaStream_t st : {c->s_in, c->s_k, c->s_out})
@@ -516,7 +577,7 @@ bfp_status bfp_arith_host_batch(bfp_host_ctx* c, int nops, const int* ops, const
         *src = static_cast<const char*>(ins[a]) + ch.b0 * stride;
         *bytes = ch.nb * stride;
       },
-      [&](const Chunk& ch, cudaStream_t st) {
+      [&](const Chunk& ch, void* const* outs, cudaStream_t st) {
         const int i = ch.slot;
         for (int q = 0; q < nops; ++q) {
           ++g_launches;
@@ -524,7 +585,7 @@ bfp_status bfp_arith_host_batch(bfp_host_ctx* c, int nops, const int* ops, const
               impl->arith(ops[q], static_cast<const uint32_t*>(c->in[i][0]),
                           static_cast<const uint32_t*>(c->in[i][1]),
                           static_cast<const uint32_t*>(c->in[i][2]),
-                          static_cast<uint32_t*>(c->out[i][q]), ch.nb, st),
+                          static_cast<uint32_t*>(outs[q]), ch.nb, st),
               "arith launch");
           if (r != BFP_OK) return r;
         }
@@ -549,10 +610,10 @@ bfp_status bfp_pack_f32_host(bfp_host_ctx* c, const bfp_format* f, const float* 
         *src = h_in + ch.e0;
         *bytes = ch.ne * 4;
       },
-      [&](const Chunk& ch, cudaStream_t st) {
+      [&](const Chunk& ch, void* const* outs, cudaStream_t st) {
         ++g_launches;
         return cuda_status(impl->pack_f32(static_cast<const float*>(c->in[ch.slot][0]),
-                                          static_cast<uint32_t*>(c->out[ch.slot][0]), ch.ne, st),
+                                          static_cast<uint32_t*>(outs[0]), ch.ne, st),
                            "pack_f32 launch");
       },
       [&](const Chunk& ch, int, void** dst, size_t* bytes) {
@@ -574,10 +635,10 @@ bfp_status bfp_unpack_f32_host(bfp_host_ctx* c, const bfp_format* f, const uint3
         *src = reinterpret_cast<const char*>(h_planes) + ch.b0 * stride;
         *bytes = ch.nb * stride;
       },
-      [&](const Chunk& ch, cudaStream_t st) {
+      [&](const Chunk& ch, void* const* outs, cudaStream_t st) {
         ++g_launches;
         return cuda_status(impl->unpack_f32(static_cast<const uint32_t*>(c->in[ch.slot][0]),
-                                            static_cast<float*>(c->out[ch.slot][0]), ch.ne, st),
+                                            static_cast<float*>(outs[0]), ch.ne, st),
                            "unpack_f32 launch");
       },
       [&](const Chunk& ch, int, void** dst, size_t* bytes) {

@@ -502,3 +502,51 @@ def test_host_mul_add_many_chunks(oracle):
     finally:
         L.bfp_host_ctx_destroy(ctx)
     assert np.array_equal(oracle.unpack_planes(pz, n, 16), oracle.binop("mul_add", fmt, a, b, c))
+
+
+def _pinned_like(L, arr: np.ndarray):
+    """A page-locked (mapped) copy of arr from bfp_host_alloc, viewed as numpy."""
+    p = L.bfp_host_alloc(arr.nbytes)
+    assert p
+    view = np.ctypeslib.as_array((C.c_uint8 * arr.nbytes).from_address(p)).view(arr.dtype)
+    view[:] = arr.reshape(-1)
+    return p, view
+
+
+def test_host_pipeline_pinned_outputs_written_in_place(oracle):
+    """Outputs in mapped pinned memory are written by the kernels directly
+    (no D2H stage); results equal the pageable-buffer path and the oracle."""
+    L = _lib.lib()
+    fmt = (5, 10, 1, 0)
+    n = 7 * (1 << 19) + 999
+    rng = np.random.default_rng(21)
+    x, y = operands(5, 10, n, rng), operands(5, 10, n, rng)
+    px, py = oracle.pack_planes(x, 16), oracle.pack_planes(y, 16)
+    ptrs = []
+    try:
+        (hx, _), (hy, _) = _pinned_like(L, px), _pinned_like(L, py)
+        outs = [_pinned_like(L, np.zeros_like(px)) for _ in range(2)]
+        ptrs += [hx, hy] + [o[0] for o in outs]
+        ctx = L.bfp_host_ctx_create(1 << 20)
+        try:
+            f = cfmt(fmt)
+            arr = (C.c_int * 2)(2, 1)
+            zp = (C.c_void_p * 2)(*[o[0] for o in outs])
+            assert L.bfp_arith_host_batch(ctx, 2, arr, C.byref(f), hx, hy, None, zp, n) == 0
+            for (_, v), op in zip(outs, ("mul", "sub")):
+                assert np.array_equal(oracle.unpack_planes(v.copy(), n, 16), oracle.binop(op, fmt, x, y)), op
+            xs = (rng.standard_normal(n) * 100).astype(np.float32)
+            hxs, _ = _pinned_like(L, xs)
+            hpp, vpp = _pinned_like(L, np.zeros_like(px))
+            hback, vback = _pinned_like(L, np.zeros(n, dtype=np.float32))
+            ptrs += [hxs, hpp, hback]
+            assert L.bfp_pack_f32_host(ctx, C.byref(f), hxs, hpp, n) == 0
+            assert np.array_equal(vpp, oracle.pack_planes(oracle.encode_f32(fmt, xs), 16))
+            assert L.bfp_unpack_f32_host(ctx, C.byref(f), hpp, hback, n) == 0
+            assert np.array_equal(vback.view(np.uint32),
+                                  oracle.decode_f32(fmt, oracle.encode_f32(fmt, xs)).view(np.uint32))
+        finally:
+            L.bfp_host_ctx_destroy(ctx)
+    finally:
+        for p in ptrs:
+            L.bfp_host_free(p)
