@@ -119,15 +119,25 @@ __device__ __forceinline__ void eval_unit(const w32* X, const w32* Y, const w32*
 // at 90-100 registers unconstrained (5 CTAs/SM); capping them for 6 CTAs
 // costs no spills and measured +10% on 1/8/7 mul, +2-5% on 1/5/10 mul.  Small
 // networks are HBM-bound (the cap measured -2..-3% there) and the widest
-// (1/8/15 mul, mul_add) gained nothing.
+// (1/8/15 mul at 4 CTAs/SM, mul_add at 5 or 6) stayed within +-2% after the
+// Booth product (profiles/r01_ab_minb_wide.txt): they run at 0.90-0.95 of the
+// LOP3 rate of the clock they are power-capped to, so only fewer LOP3 helps.
 #ifndef BFP_MID_MINB
 #define BFP_MID_MINB 6
+#endif
+#ifndef BFP_WIDE_MINB
+#define BFP_WIDE_MINB 1
+#endif
+#ifndef BFP_MULADD_MINB
+#define BFP_MULADD_MINB 1
 #endif
 template <class F, int OP>
 constexpr int arith_minb() {
   if constexpr (Gen<F, OP>::ok) {
     constexpr int l = Gen<F, OP>::luts;
     if ((OP == OP_MUL || OP == OP_DIV) && l >= 300 && l <= 800) return BFP_MID_MINB;
+    if ((OP == OP_MUL || OP == OP_DIV) && l > 800 && l <= 1100) return BFP_WIDE_MINB;
+    if (OP == OP_MUL_ADD && l >= 300 && l <= 1000) return BFP_MULADD_MINB;
   }
   return BFP_ARITH_MINB;
 }

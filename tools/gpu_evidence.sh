@@ -9,6 +9,7 @@ timeout 1500 python -m pytest tests -q -x -m gpu > gpurun_out/pytest_gpu.log 2>&
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke_rc=$?; tail -1 gpurun_out/smoke.log
 fi
 if [ "${BENCH:-1}" = 1 ]; then
+timeout 600 python bench.py --impl reference > gpurun_out/bench_reference.jsonl 2> gpurun_out/bench_reference.err; echo bench_reference_rc=$?
 timeout 600 python bench.py > gpurun_out/bench_default.jsonl 2> gpurun_out/bench_default.err; echo bench_default_rc=$?
 timeout 900 python bench.py --config all --steps 50 --warmup 5 > gpurun_out/bench_all.jsonl 2> gpurun_out/bench_all.err; echo bench_all_rc=$?
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/ncu/launches_default.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu/launches_default.log 2>&1; echo launches_rc=$?
