@@ -6,6 +6,7 @@
 #include <cstddef>
 #include <cstdint>
 #include <cstring>
+#include <utility>
 
 #include "../../paper_1602_04716_b200/csrc/bfp_circuits.cuh"
 #include "../../paper_1602_04716_b200/csrc/bfp_formats.h"
@@ -186,4 +187,24 @@ extern "C" int host_codec64(int dir, unsigned e, unsigned s, int rn, int ftz, co
   if (e == 11 && s == 20) { with_fmt<11, 20>(rn, ftz, fn); return 0; }
   if (e == 2 && s == 1) { with_fmt<2, 1>(rn, ftz, fn); return 0; }
   return dispatch(e, s, rn, ftz, fn);
+}
+
+// Significand products (tests only): which = 0 array (sig_product), 1 Booth
+// (sig_product_booth).  a, b: S+1 words each, p: 2S+2 words.
+template <int S>
+static void product_t(int which, const uint32_t* a, const uint32_t* b, uint32_t* p) {
+  if (which == 0)
+    bfpg::sig_product<S>(a, b, p);
+  else
+    bfpg::sig_product_booth<S>(a, b, p);
+}
+template <int... Ks>
+static int product_dispatch(int s, int which, const uint32_t* a, const uint32_t* b, uint32_t* p,
+                            std::integer_sequence<int, Ks...>) {
+  int ok = -1;  // S = K + 2, 2..30
+  ((s == Ks + 2 ? (product_t<Ks + 2>(which, a, b, p), ok = 0) : 0), ...);
+  return ok;
+}
+extern "C" int host_product(int s, int which, const uint32_t* a, const uint32_t* b, uint32_t* p) {
+  return product_dispatch(s, which, a, b, p, std::make_integer_sequence<int, 29>{});
 }

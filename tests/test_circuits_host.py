@@ -169,3 +169,30 @@ def test_codec64_host(oracle, ref_oracle, host, fmt2):
     nan = np.isnan(want.view(np.float64))
     assert np.array_equal(got[~nan], want[~nan])
     assert np.all(got[nan] == np.uint64(0x7FF8000000000000))  # quiet_NaN()
+
+
+@pytest.mark.parametrize("s", list(range(2, 31)))
+def test_significand_products_exact(host, s):
+    """Array and radix-4 Booth (constexpr Dadda schedule) significand products
+    equal the exact integer product lane by lane, S = 2..30 (mul_w uses Booth
+    for S >= 9), with random significands and the all-ones top bits mul_w feeds."""
+    import ctypes as C
+    L = host.L
+    L.host_product.argtypes = [C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]
+    rng = np.random.default_rng(100 + s)
+    for trial in range(24):
+        a = rng.integers(0, 1 << 32, s + 1, dtype=np.uint64).astype(np.uint32)
+        b = rng.integers(0, 1 << 32, s + 1, dtype=np.uint64).astype(np.uint32)
+        if trial % 2:
+            a[s] = b[s] = 0xFFFFFFFF
+        if trial == 2:
+            a[:] = b[:] = 0xFFFFFFFF
+        # per-lane values (bit j of lane k = bit k of word j)
+        av = [sum(((int(a[j]) >> k) & 1) << j for j in range(s + 1)) for k in range(32)]
+        bv = [sum(((int(b[j]) >> k) & 1) << j for j in range(s + 1)) for k in range(32)]
+        want = [x * y for x, y in zip(av, bv)]
+        for which in (0, 1):
+            p = np.zeros(2 * s + 2, dtype=np.uint32)
+            assert L.host_product(s, which, a.ctypes.data, b.ctypes.data, p.ctypes.data) == 0
+            got = [sum(((int(p[j]) >> k) & 1) << j for j in range(2 * s + 2)) for k in range(32)]
+            assert got == want, (s, which, trial)
