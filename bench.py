@@ -220,6 +220,9 @@ def _arith_job(label, op, spec, n, sets, device):
                      "sets": len(sets)})
 
 
+X1_FMTS = [(3, 2), (4, 3), (5, 3), (5, 7), (5, 10), (8, 7), (8, 15)]
+
+
 def make_jobs(cfg: str, rank: int, world: int, device) -> list:
     """Per-rank resident operands and the timed kernels of config `cfg`."""
     import torch
@@ -299,6 +302,34 @@ def make_jobs(cfg: str, rank: int, world: int, device) -> list:
                for sd in (W.SEED_A, W.SEED_B, W.SEED_C)]
         torch.cuda.empty_cache()
         return [_arith_job("mul_add", "mul_add", spec, n, [tuple(ops)], device)]
+    if cfg == "X1":  # secondary: bfp_div over the C4 formats + 1/4/3, 1/5/10
+        n = 1 << 28
+        lo = rank * n
+        jobs = []
+        for (e, s) in X1_FMTS:
+            spec = spec_of(e, s)
+            a = bfp.pack(W.c4_encodings(e, s, lo, lo + n, W.SEED_A, device), spec)
+            b = bfp.pack(W.c4_encodings(e, s, lo, lo + n, W.SEED_B, device), spec)
+            torch.cuda.empty_cache()
+            jobs.append(_arith_job(f"div_1/{e}/{s}", "div", spec, n, [(a, b, None)], device))
+        return jobs
+    if cfg == "X2":  # secondary: fused float32-in/out ops, C3 operands
+        n = 1 << 28
+        spec = spec_of(5, 10)
+        lo = rank * n
+        xa = W.c3_floats(lo, lo + n, W.SEED_A, device)
+        xb = W.c3_floats(lo, lo + n, W.SEED_B, device)
+        outs = [torch.empty(n, dtype=torch.float32, device=device) for _ in range(2)]
+        jobs = []
+        for op in ("add", "mul"):
+            def launch(i, st, op=op):
+                rc = L.bfp_arith_f32(OPNAMES[op], spec.c, xa.data_ptr(), xb.data_ptr(), None,
+                                     outs[i & 1].data_ptr(), n, st)
+                if rc != 0:
+                    raise RuntimeError(L.bfp_last_error())
+            jobs.append(Job(f"{op}_f32", f"{op}_f32", spec, n, launch, 12 * n,
+                            host={"kind": "none"}))
+        return jobs
     raise ValueError(cfg)
 
 
@@ -464,6 +495,8 @@ def run_e2e(cfg: str, jobs, steps: int, world: int, rank: int, local: int) -> di
                 calls.append((lambda spec=spec, hp=hp, hz=hz, n=n:
                               L.bfp_unpack_f32_host(ctx, spec.c, hp, hz, n), pb, 4 * n, n))
         torch.cuda.empty_cache()
+        if not calls:  # no host-buffer entry point for these kernels (X2)
+            return None
 
         def step():
             for fn, _, _, _ in calls:
@@ -647,12 +680,37 @@ def ref_cpu_jobs(cfg: str, sample: int, threads: int):
         fmt = (6, 9) + MODE
         encs = [O.encode_f32(fmt, W.c5_floats(0, sample, sd, "cpu").numpy()) for sd in (1, 2, 3)]
         arith("mul_add", "mul_add", fmt, encs)
+    elif cfg == "X1":
+        for (e, s) in X1_FMTS:
+            fmt = (e, s) + MODE
+            encs = [W.c4_encodings(e, s, 0, sample, sd, "cpu").numpy().astype(np.uint64)
+                    for sd in (1, 2)]
+            arith(f"div_1/{e}/{s}", "div", fmt, encs)
+    elif cfg == "X2":
+        # the reference user's float32 path: encode_scalar + pack of both
+        # operands, the op, unpack + decode_scalar of the result
+        fmt = (5, 10) + MODE
+        xs = [np.ascontiguousarray(W.c3_floats(0, sample, sd, "cpu").numpy()) for sd in (1, 2)]
+        pl = [np.zeros(O.nblocks(sample) * 16 * 32, dtype=np.uint32) for _ in range(2)]
+        fl_out = np.zeros(sample, dtype=np.float32)
+        encs = [O.encode_f32(fmt, x) for x in xs]
+        planes = [O.pack_planes(v, 16) for v in encs]
+        for op in ("add", "mul"):
+            def chain(op=op):
+                for x, p in zip(xs, pl):
+                    R.ref_pack_f32_path(x.ctypes.data_as(O._f32p), sample, p.ctypes.data_as(O._u32p),
+                                        5, 10, MODE[0], MODE[1], threads)
+                z = O.ref_binop_planes(op, fmt, planes[0], planes[1], None, threads=threads)
+                R.ref_unpack_f32_path(np.ascontiguousarray(z).ctypes.data_as(O._u32p), sample,
+                                      fl_out.ctypes.data_as(O._f32p), 5, 10, threads)
+            jobs.append((f"{op}_f32", chain))
     else:
         raise ValueError(cfg)
     return jobs, O.ref_lib_path().name
 
 
-REF_SAMPLE = {"C1": 1 << 22, "C2": 1 << 22, "C3": 1 << 20, "C4": 1 << 20, "C5": 1 << 20}
+REF_SAMPLE = {"C1": 1 << 22, "C2": 1 << 22, "C3": 1 << 20, "C4": 1 << 20, "C5": 1 << 20,
+              "X1": 1 << 20, "X2": 1 << 20}
 
 
 def ref_cpu_run(cfg: str, sample: int, reps: int | None = None, seconds: float = 10.0,
@@ -702,6 +760,11 @@ CONFIG_TEXT = {
            "format; uniform finite bit patterns", "sweep", 1 << 28),
     "C5": ("C5: 1/6/9 z=round(round(a*b)+c) fused, N=2^32 total split evenly over the GPUs; "
            "float32 sign x 2^U[-10,9] x U[1,2) -> encode_scalar", "1/6/9", None),
+    "X1": ("X1 (secondary, not a BASELINE config): div sweep over 1/3/2, 1/4/3, 1/5/3, 1/5/7, 1/5/10, "
+           "1/8/7, 1/8/15, N=2^28 per GPU per format; C4 operand distribution", "sweep", 1 << 28),
+    "X2": ("X2 (secondary, not a BASELINE config): 1/5/10 add and mul with float32 in / float32 out "
+           "in one kernel each (pack -> op -> unpack in registers), N=2^28 per GPU; C3 operands",
+           "1/5/10", 1 << 28),
 }
 
 

@@ -32,7 +32,12 @@
  * default stream) on the current device; no device memory is allocated by
  * the d_* entry points; errors are returned, never thrown.  Calls are
  * re-entrant.  The h_* entry points take host buffers (pinned for full
- * speed, see bfp_host_alloc) and run a chunked H2D / kernel / D2H pipeline.
+ * speed, see bfp_host_alloc) and run a chunked pipeline: inputs are copied
+ * H2D in chunk order on one stream, kernels run on a second; outputs in
+ * page-locked mapped memory (bfp_host_alloc) of calls up to 256 MiB are
+ * written in place by the kernels over PCIe, others are staged in device
+ * buffers and copied D2H in chunk order on a third stream.  The calls block
+ * until the results are in host memory.
  */
 #ifndef BFPGPU_H_
 #define BFPGPU_H_
@@ -128,7 +133,7 @@ bfp_status bfp_arith(int op, const bfp_format* f, const uint32_t* d_x, const uin
 bfp_status bfp_arith_f32(int op, const bfp_format* f, const float* d_x, const float* d_y,
                          const float* d_c, float* d_z, size_t count, void* stream);
 
-/* ---- host-buffer entry points (pipelined H2D / kernel / D2H) ------------- */
+/* ---- host-buffer entry points (pipelined H2D / kernel [/ D2H]) ---------- */
 typedef struct bfp_host_ctx bfp_host_ctx;
 bfp_host_ctx* bfp_host_ctx_create(size_t chunk_elems); /* 0 = default (2^22) */
 void bfp_host_ctx_destroy(bfp_host_ctx* ctx);

@@ -19,9 +19,11 @@
 //     exponent-range test), and exponent/fraction are rounded as one packed
 //     integer so the significand carry, subnormal->normal and overflow->Inf
 //     transitions fall out of one increment chain;
-//   * mul: an exact (S+1)x(S+1) array product, full normalise, a narrow
-//     (S+3)-bit subnormal shifter driven by a (E+2)-bit exponent, packed
-//     rounding as above;
+//   * mul: at most one operand normalised before the product (two subnormal
+//     operands underflow to zero), an exact (S+1)x(S+1) product -- array cells
+//     for S < 9, radix-4 Booth rows with a compile-time Dadda reduction for
+//     S >= 9 -- a 1-bit product normalise, a narrow (S+3)-bit subnormal
+//     shifter driven by a (E+2)-bit exponent, packed rounding as above;
 //   * special values come from the larger-magnitude operand (add) or four
 //     class masks (mul) and are applied with one LOP3 per output plane.
 // Bit-exactness against the reference is established by tests, not by
