@@ -501,6 +501,11 @@ __device__ __forceinline__ void floats_to_planes(w32* V, w32* P) {
       L[q] = hw_cvt2<HW, F::RN>(__uint_as_float(V[2 * q]), __uint_as_float(V[2 * q + 1]));
     enc16_to_planes(L, P);
     canon_nan_planes<F>(P);
+    if constexpr (F::FTZ) {  // subnormal results -> signed zero: clear their fraction planes
+      w32 h = 0;
+      BFP_UNROLL for (int i = 0; i < F::E; ++i) h |= P[F::S + i];
+      BFP_UNROLL for (int j = 0; j < F::S; ++j) P[j] &= h;
+    }
   } else {
     BFP_UNROLL for (int k = 0; k < 32; ++k) V[k] = encode_f32_fast<F>(V[k]);
     if constexpr (N <= 8) {

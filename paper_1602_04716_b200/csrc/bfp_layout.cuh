@@ -505,7 +505,10 @@ BFP_HD void canon_nan_planes(w32* P) {
 // planes fix above canonicalises.  0 = generic, 1 = binary16, 2 = bfloat16.
 template <class F>
 struct HwCodec {
-  static constexpr int kind = F::FTZ ? 0 : (F::E == 5 && F::S == 10) ? 1 : (F::E == 8 && F::S == 7) ? 2 : 0;
+  // FTZ formats too: encode_scalar flushes AFTER rounding (format.hpp:173-177),
+  // so the hardware conversion followed by a flush of subnormal results is
+  // exact (floats_to_planes), and decode_scalar has no DAZ (format.hpp:114-116).
+  static constexpr int kind = (F::E == 5 && F::S == 10) ? 1 : (F::E == 8 && F::S == 7) ? 2 : 0;
 };
 
 #if defined(__CUDACC__)

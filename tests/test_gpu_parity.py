@@ -550,3 +550,26 @@ def test_host_pipeline_pinned_outputs_written_in_place(oracle):
     finally:
         for p in ptrs:
             L.bfp_host_free(p)
+
+
+@pytest.mark.parametrize("fmt2", [(5, 10), (8, 7)])
+@pytest.mark.parametrize("mode", MODES)
+def test_pack_f32_hw_path_underflow_boundary(oracle, fmt2, mode):
+    """The hardware-cvt encoders (binary16 / bfloat16 layouts, every mode incl.
+    FTZ = convert then flush subnormal results) around the subnormal range and
+    the normal boundary: every 7th float32 of both signs over the exponents
+    from 12 below the smallest subnormal to 2 above the smallest normal."""
+    e, s = fmt2
+    spec = bfp.make_spec(e, s, mode[0], mode[1])
+    fmt = fmt2 + mode
+    emin = 2 - (1 << (e - 1))  # unbiased exponent of the smallest normal
+    lo_exp, hi_exp = max(0, 127 + emin - s - 12), 127 + emin + 2  # bfloat16: float32 subnormals
+    man = np.arange(0, 1 << 23, 7, dtype=np.uint32)
+    exps = np.arange(lo_exp, hi_exp + 1, dtype=np.uint32)
+    bits = (exps[:, None] << 23 | man[None, :]).reshape(-1)
+    bits = np.concatenate([bits, bits | np.uint32(0x80000000)])
+    xs = bits.view(np.float32)
+    v = bfp.pack_f32(torch.from_numpy(xs).cuda(), spec)
+    want = oracle.encode_f32(fmt, xs)
+    got = bfp.to_u64(bfp.unpack(v), spec).cpu().numpy().astype(np.uint64)
+    assert np.array_equal(got, want), int((got != want).sum())
