@@ -868,6 +868,9 @@ def main_ours(args) -> None:
                                 "binding": "logic" if logic_t > hbm_t else "hbm",
                                 "frac_of_binding": round(max(hbm_t, logic_t) / dur, 4)})
             tr = tmap.get(f"{cfg}:{j.label}{tsuf}")
+            if isinstance(tr, dict):
+                ent["ncu"] = {k: v for k, v in tr.items() if k != "bytes"}
+                tr = tr.get("bytes")
             if tr is not None:
                 ent["traffic"] = tr
                 ent["traffic_over_algorithmic"] = round(tr / j.algo_bytes, 3)
@@ -875,6 +878,8 @@ def main_ours(args) -> None:
             roofs.append((ms, j, ach))
         ms_dom, jd, ach = max(roofs, key=lambda r: r[0])
         traffic = tmap.get(f"{cfg}:{jd.label}{tsuf}")
+        if isinstance(traffic, dict):
+            traffic = traffic.get("bytes")
         roof = {"bound": "hbm", "kernel": f"{jd.label} (1/{jd.spec.exp_bits}/{jd.spec.sig_bits} {mode_text()})",
                 "achieved": round(ach, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": round(ach / peaks["hbm_gbs"], 4), "traffic": traffic,

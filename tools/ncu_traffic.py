@@ -1,5 +1,6 @@
 """Per-launch DRAM traffic of every timed kernel, from `ncu --set full` captures,
-into profiles/ncu_traffic.json (the `roofline.traffic` source of bench.py).
+into profiles/ncu_traffic.json (the `roofline.traffic` source of bench.py), with
+the same capture's ALU-pipe utilisation and DRAM throughput (% of peak).
 
     python tools/ncu_traffic.py OUT.json CFG=report.ncu-rep [CFG=report ...]
 
@@ -33,7 +34,10 @@ def rows(rep: str) -> list[dict]:
         scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
         rd = float(d["dram__bytes_read.sum"]) * scale[units[hdr.index("dram__bytes_read.sum")]]
         wr = float(d["dram__bytes_write.sum"]) * scale[units[hdr.index("dram__bytes_write.sum")]]
+        pct = lambda k: round(float(d[k]), 2) if k in d and d[k] not in ("", "n/a") else None
         out.append({"kernel": d["Kernel Name"], "read": rd, "write": wr,
+                    "alu": pct("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"),
+                    "dram": pct("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
                     "us": float(d["gpu__time_duration.sum"]) *
                     {"ns": 1e-3, "us": 1.0, "usecond": 1.0, "nsecond": 1e-3, "msecond": 1e3, "ms": 1e3}
                     [units[hdr.index("gpu__time_duration.sum")]]})
@@ -67,7 +71,8 @@ def main() -> None:
         base, _, mode = cfg.partition(":")
         for lb, r in last.items():
             key = f"{base}:{lb}" + (f":{mode}" if mode else "")
-            res[key] = int(r["read"] + r["write"])
+            res[key] = {"bytes": int(r["read"] + r["write"]), "ncu_us": round(r["us"], 2),
+                        "alu_pipe_pct": r["alu"], "dram_throughput_pct": r["dram"]}
             print(f"{key:24s} read {r['read'] / 1e6:10.2f} MB  write {r['write'] / 1e6:10.2f} MB  "
                   f"{r['us']:9.1f} us")
     with open(out, "w") as f:
