@@ -42,6 +42,7 @@ namespace bfp::gpu {
 
 enum class rounding_mode { rz, rn };           // format.hpp:16
 enum class subnormal_policy { gradual, ftz };  // format.hpp:17
+enum class value_class { zero, subnormal, normal, infinity, nan };  // format.hpp:19
 using encoding = std::uint64_t;                // format.hpp:21
 
 struct format_spec {  // format.hpp:23-55
@@ -70,6 +71,27 @@ struct format_spec {  // format.hpp:23-55
                       subnormals == subnormal_policy::ftz ? 1u : 0u, name.c_str()};
   }
 };
+
+// Value-level view of one element (format.hpp:75-99): host helpers.
+struct scalar_custom {
+  unsigned sign = 0;
+  std::uint64_t biased_exp = 0;
+  std::uint64_t fraction = 0;
+  value_class cls = value_class::zero;
+};
+
+inline scalar_custom split(encoding enc, const format_spec& f) {
+  scalar_custom r;
+  r.sign = static_cast<unsigned>((enc >> (f.exp_bits + f.sig_bits)) & 1u);
+  r.biased_exp = (enc >> f.sig_bits) & f.exp_field_max();
+  r.fraction = enc & f.frac_mask();
+  const bool top = r.biased_exp == f.exp_field_max(), low = r.biased_exp == 0;
+  r.cls = top ? (r.fraction ? value_class::nan : value_class::infinity)
+              : low ? (r.fraction ? value_class::subnormal : value_class::zero) : value_class::normal;
+  return r;
+}
+
+inline value_class classify(encoding enc, const format_spec& f) { return split(enc, f).cls; }
 
 inline void validate(const format_spec& f) {  // format.hpp:57-64
   if (f.exp_bits < 2 || f.exp_bits > 11) throw std::invalid_argument("exp_bits must be in [2, 11]");

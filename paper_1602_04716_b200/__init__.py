@@ -18,6 +18,10 @@ from .bfp import (  # noqa: F401
     bfp_sub,
     bfp_vector,
     bfpraw_stride,
+    classify,
+    scalar_custom,
+    split,
+    value_class,
     pack_bfpraw,
     unpack_bfpraw,
     decode_scalar,

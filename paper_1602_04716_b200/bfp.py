@@ -108,6 +108,41 @@ class format_spec:
         return 1 if n <= 8 else 2 if n <= 16 else 4 if n <= 32 else 8
 
 
+class value_class(enum.IntEnum):  # format.hpp:19
+    zero = 0
+    subnormal = 1
+    normal = 2
+    infinity = 3
+    nan = 4
+
+
+@dataclass
+class scalar_custom:  # format.hpp:75-81
+    sign: int = 0
+    biased_exp: int = 0
+    fraction: int = 0
+    cls: value_class = value_class.zero
+
+
+def split(enc: int, f: format_spec) -> scalar_custom:
+    """format.hpp:83-95: sign / biased exponent / fraction / class of one encoding."""
+    sign = (enc >> (f.exp_bits + f.sig_bits)) & 1
+    be = (enc >> f.sig_bits) & f.exp_field_max()
+    fr = enc & f.frac_mask()
+    if be == f.exp_field_max():
+        cls = value_class.nan if fr else value_class.infinity
+    elif be == 0:
+        cls = value_class.subnormal if fr else value_class.zero
+    else:
+        cls = value_class.normal
+    return scalar_custom(sign, be, fr, cls)
+
+
+def classify(enc: int, f: format_spec) -> value_class:
+    """format.hpp:97-99."""
+    return split(enc, f).cls
+
+
 def validate(f: format_spec) -> None:
     """format.hpp:57-64 (raises ValueError where the reference throws invalid_argument)."""
     if f.exp_bits < 2 or f.exp_bits > 11:

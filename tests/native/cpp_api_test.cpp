@@ -14,6 +14,22 @@ extern "C" uint64_t orc_encode(double x, unsigned e, unsigned s, int rn, int ftz
 int main() {
   namespace g = bfp::gpu;
   int fails = 0;
+  {  // split / classify (format.hpp:83-99)
+    const auto f = g::make_spec(5, 10);
+    const g::encoding cases[] = {0x0000, 0x8001, 0x3c00, 0x7c00, 0xfe00, 0x03ff};
+    const g::value_class want[] = {g::value_class::zero, g::value_class::subnormal, g::value_class::normal,
+                                   g::value_class::infinity, g::value_class::nan, g::value_class::subnormal};
+    for (int k = 0; k < 6; ++k)
+      if (g::classify(cases[k], f) != want[k]) {
+        std::printf("classify mismatch %d\n", k);
+        ++fails;
+      }
+    const auto sc = g::split(0xbc01, f);
+    if (sc.sign != 1 || sc.biased_exp != 15 || sc.fraction != 1) {
+      std::printf("split mismatch\n");
+      ++fails;
+    }
+  }
   std::mt19937_64 rng(42);
   for (auto [e, s] : {std::pair{4u, 3u}, std::pair{5u, 10u}, std::pair{8u, 15u}}) {
     for (int rn = 0; rn < 2; ++rn) {

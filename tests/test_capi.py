@@ -106,3 +106,22 @@ def test_host_scalar_codec_matches_oracle(oracle):
             a = bfp.decode_scalar(int(enc), f)
             b = oracle.orc().orc_decode(int(enc), e, s)
             assert (math.isnan(a) and math.isnan(b)) or a == b
+
+
+def test_split_classify_mirror(oracle):
+    """split / classify (format.hpp:83-99) agree with the oracle's exact decode
+    on every encoding of the <= 9-bit formats and sampled wider ones."""
+    rng = np.random.default_rng(7)
+    for (e, s) in FORMATS:
+        f = bfp.make_spec(e, s)
+        nb = 1 + e + s
+        encs = range(1 << nb) if nb <= 9 else [int(x) for x in rng.integers(0, 1 << nb, size=2000)]
+        for enc in encs:
+            sc = bfp.split(enc, f)
+            assert sc.sign == enc >> (e + s) and sc.fraction == enc & ((1 << s) - 1)
+            assert sc.biased_exp == (enc >> s) & ((1 << e) - 1)
+            x = oracle.orc().orc_decode(enc, e, s)
+            want = (bfp.value_class.nan if math.isnan(x) else bfp.value_class.infinity if math.isinf(x)
+                    else bfp.value_class.zero if x == 0 else bfp.value_class.subnormal
+                    if abs(x) < 2.0 ** f.emin() else bfp.value_class.normal)
+            assert bfp.classify(enc, f) == want, (e, s, enc)
