@@ -27,13 +27,7 @@ enum Op { OP_ADD = 0, OP_SUB = 1, OP_MUL = 2, OP_DIV = 3, OP_MUL_ADD = 4 };
 
 constexpr int kThreads = 128;
 
-#if defined(BFP_LDST_PLAIN)
-__device__ __forceinline__ w32 ld_stream(const w32* p) { return *p; }
-#elif defined(BFP_LDST_NC)
-__device__ __forceinline__ w32 ld_stream(const w32* p) { return __ldg(p); }
-#else
 __device__ __forceinline__ w32 ld_stream(const w32* p) { return __ldcs(p); }
-#endif
 
 // Programmatic dependent launch: every kernel waits for the previous grid to
 // complete -- memory included -- before its first global access (so
@@ -71,11 +65,7 @@ __device__ __forceinline__ void pdl_release_if(bool last) {
   if (last) asm volatile("griddepcontrol.launch_dependents;");
 #endif
 }
-#if defined(BFP_LDST_PLAIN) || defined(BFP_LDST_NC)
-__device__ __forceinline__ void st_stream(w32* p, w32 v) { *p = v; }
-#else
 __device__ __forceinline__ void st_stream(w32* p, w32 v) { __stcs(p, v); }
-#endif
 
 // Operands of one unit: NIN inputs x N planes, loaded with the streaming path.
 template <int N, int NIN>
