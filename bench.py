@@ -330,6 +330,35 @@ def make_jobs(cfg: str, rank: int, world: int, device) -> list:
             jobs.append(Job(f"{op}_f32", f"{op}_f32", spec, n, launch, 12 * n,
                             host={"kind": "none"}))
         return jobs
+    if cfg in ("X3", "X3u"):  # secondary: z = a*b + c*d, fused (bfp_chain) or as 3 kernels
+        n = 1 << 28
+        spec = spec_of(5, 10)
+        lo = rank * n
+        vs = [bfp.pack(W.c4_encodings(5, 10, lo, lo + n, sd, device), spec)
+              for sd in (W.SEED_A, W.SEED_B, W.SEED_C, W.SEED_C + 1)]
+        torch.cuda.empty_cache()
+        outs = [bfp.empty(spec, n, device) for _ in range(2)]
+        nb = spec.total_bits()
+        if cfg == "X3":
+            ptrs = (C.c_void_p * 4)(*[v.planes.data_ptr() for v in vs])
+
+            def launch(i, st):
+                rc = L.bfp_chain(spec.c, b"ab*cd*+", 4, ptrs, outs[i & 1].planes.data_ptr(), n, st)
+                if rc != 0:
+                    raise RuntimeError(L.bfp_last_error())
+            return [Job("a*b+c*d", "chain:ab*cd*+", spec, n, launch, 5 * nb / 8 * n, host={"kind": "none"})]
+        t = [bfp.empty(spec, n, device) for _ in range(2)]
+
+        def op(code, x, y, z):
+            def launch(i, st):
+                rc = L.bfp_arith(code, spec.c, x.planes.data_ptr(), y.planes.data_ptr(), None,
+                                 z.planes.data_ptr(), n, st)
+                if rc != 0:
+                    raise RuntimeError(L.bfp_last_error())
+            return launch
+        return [Job("mul a*b", "mul", spec, n, op(2, vs[0], vs[1], t[0]), 3 * nb / 8 * n, host={"kind": "none"}),
+                Job("mul c*d", "mul", spec, n, op(2, vs[2], vs[3], t[1]), 3 * nb / 8 * n, host={"kind": "none"}),
+                Job("add", "add", spec, n, op(0, t[0], t[1], outs[0]), 3 * nb / 8 * n, host={"kind": "none"})]
     raise ValueError(cfg)
 
 
@@ -686,6 +715,21 @@ def ref_cpu_jobs(cfg: str, sample: int, threads: int):
             encs = [W.c4_encodings(e, s, 0, sample, sd, "cpu").numpy().astype(np.uint64)
                     for sd in (1, 2)]
             arith(f"div_1/{e}/{s}", "div", fmt, encs)
+    elif cfg in ("X3", "X3u"):
+        fmt = (5, 10) + MODE
+        planes = [O.pack_planes(W.c4_encodings(5, 10, 0, sample, sd, "cpu").numpy().astype(np.uint64), 16)
+                  for sd in (1, 2, 3, 4)]
+
+        def expr():
+            p = O.ref_binop_planes("mul", fmt, planes[0], planes[1], threads=threads)
+            q = O.ref_binop_planes("mul", fmt, planes[2], planes[3], threads=threads)
+            O.ref_binop_planes("add", fmt, p, q, threads=threads)
+        if cfg == "X3":
+            jobs.append(("a*b+c*d", expr))
+        else:  # three op results per expression, as the X3u line counts them
+            jobs += [("mul a*b", lambda: O.ref_binop_planes("mul", fmt, planes[0], planes[1], threads=threads)),
+                     ("mul c*d", lambda: O.ref_binop_planes("mul", fmt, planes[2], planes[3], threads=threads)),
+                     ("add", lambda: O.ref_binop_planes("add", fmt, planes[0], planes[1], threads=threads))]
     elif cfg == "X2":
         # the reference user's float32 path: encode_scalar + pack of both
         # operands, the op, unpack + decode_scalar of the result
@@ -710,7 +754,7 @@ def ref_cpu_jobs(cfg: str, sample: int, threads: int):
 
 
 REF_SAMPLE = {"C1": 1 << 22, "C2": 1 << 22, "C3": 1 << 20, "C4": 1 << 20, "C5": 1 << 20,
-              "X1": 1 << 20, "X2": 1 << 20}
+              "X1": 1 << 20, "X2": 1 << 20, "X3": 1 << 20, "X3u": 1 << 20}
 
 
 def ref_cpu_run(cfg: str, sample: int, reps: int | None = None, seconds: float = 10.0,
@@ -765,6 +809,10 @@ CONFIG_TEXT = {
     "X2": ("X2 (secondary, not a BASELINE config): 1/5/10 add and mul with float32 in / float32 out "
            "in one kernel each (pack -> op -> unpack in registers), N=2^28 per GPU; C3 operands",
            "1/5/10", 1 << 28),
+    "X3": ("X3 (secondary, not a BASELINE config): z = a*b + c*d in 1/5/10 as ONE bfp_chain kernel "
+           "(intermediates in registers), N=2^28 per GPU; uniform finite operands", "1/5/10", 1 << 28),
+    "X3u": ("X3u (secondary, not a BASELINE config): z = a*b + c*d in 1/5/10 as three kernels "
+            "(mul, mul, add through HBM), N=2^28 per GPU; uniform finite operands", "1/5/10", 1 << 28),
 }
 
 
@@ -855,8 +903,16 @@ def main_ours(args) -> None:
             e, s = j.spec.exp_bits, j.spec.sig_bits
             ent = {"ms": round(ms, 4), "gelem_s": round(j.n / dur / 1e9, 2),
                    "hbm_gbs": round(ach, 1), "hbm_frac": round(ach / peaks["hbm_gbs"], 4)}
-            if j.op in OPNAMES:
-                lop3 = sass_lop3((e, s), int(j.spec.rounding), int(j.spec.subnormals), OPNAMES[j.op])
+            chain_ops = ([{"+": "add", "-": "sub", "*": "mul", "/": "div"}[ch]
+                          for ch in j.op.split(":", 1)[1] if ch in "+-*/"]
+                         if j.op.startswith("chain:") else None)
+            if j.op in OPNAMES or chain_ops:
+                if chain_ops:
+                    parts = [sass_lop3((e, s), int(j.spec.rounding), int(j.spec.subnormals), OPNAMES[o])
+                             for o in chain_ops]
+                    lop3 = None if None in parts else sum(parts)
+                else:
+                    lop3 = sass_lop3((e, s), int(j.spec.rounding), int(j.spec.subnormals), OPNAMES[j.op])
                 if lop3 is not None and peak_lop3:
                     pe = lop3 / 32.0
                     hbm_t = j.algo_bytes / (peaks["hbm_gbs"] * 1e9)

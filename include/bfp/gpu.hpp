@@ -29,6 +29,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <initializer_list>
 #include <limits>
 #include <span>
 #include <stdexcept>
@@ -329,6 +330,24 @@ inline bfp_vector bfp_div(const bfp_vector& x, const bfp_vector& y, cudaStream_t
 inline bfp_vector bfp_mul_add(const bfp_vector& a, const bfp_vector& b, const bfp_vector& c,
                               cudaStream_t st = nullptr) {
   return detail::arith(4, a, b, &c, st, "bfp_mul_add");
+}
+// Fused expression (bfp_chain): postfix program over inputs 'a', 'b', ...
+// (ins[0], ins[1], ...) and + - * /; e.g. chain("ab*cd*+", {&a, &b, &c, &d})
+// equals bfp_add(bfp_mul(a, b), bfp_mul(c, d)) bit for bit, in one kernel.
+inline bfp_vector chain(const char* program, std::initializer_list<const bfp_vector*> ins,
+                        cudaStream_t st = nullptr) {
+  if (ins.size() == 0 || ins.size() > 8) throw std::invalid_argument("chain: 1..8 inputs");
+  const bfp_vector& x = **ins.begin();
+  std::vector<const std::uint32_t*> ptrs;
+  for (const bfp_vector* v : ins) {
+    detail::require_same_shape(x.spec, v->spec);
+    if (v->size() != x.size()) throw std::invalid_argument("chain: operand sizes differ");
+    ptrs.push_back(v->planes());
+  }
+  bfp_vector z(x.spec, x.size());
+  const bfp_format f = x.spec.c();
+  detail::check(bfp_chain(&f, program, int(ptrs.size()), ptrs.data(), z.planes(), x.size(), st), "chain");
+  return z;
 }
 
 // Host scalar codec (format.hpp:101-188).

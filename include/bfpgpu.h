@@ -133,6 +133,19 @@ bfp_status bfp_arith(int op, const bfp_format* f, const uint32_t* d_x, const uin
 bfp_status bfp_arith_f32(int op, const bfp_format* f, const float* d_x, const float* d_y,
                          const float* d_c, float* d_z, size_t count, void* stream);
 
+/* Fused expression: z = program(d_in[0], d_in[1], ...) over plane buffers
+ * of one format, `count` elements each.  program is postfix over inputs
+ * 'a', 'b', ... (d_in[0], d_in[1], ..., at most 8) and the ops + - * /, e.g.
+ * "ab*c+" = (a*b)+c, "ab*cd*+" = a*b + c*d, "ab+c/" = (a+b)/c.  Every op
+ * rounds to the format exactly as bfp_add / bfp_sub / bfp_mul / bfp_div do
+ * (arith.hpp:235-444), so the result equals that sequence of calls; the
+ * intermediates stay in registers (one kernel, HBM traffic = the inputs
+ * once + the output).  Compiled for the format and program by NVRTC on first
+ * use and cached (BFP_EUNSUPPORTED without NVRTC).  Replaces chains of the
+ * reference's bfp_* calls ("longer chains"). */
+bfp_status bfp_chain(const bfp_format* f, const char* program, int n_inputs,
+                     const uint32_t* const* d_in, uint32_t* d_z, size_t count, void* stream);
+
 /* ---- host-buffer entry points (pipelined H2D / kernel [/ D2H]) ---------- */
 typedef struct bfp_host_ctx bfp_host_ctx;
 bfp_host_ctx* bfp_host_ctx_create(size_t chunk_elems); /* 0 = default (2^22) */

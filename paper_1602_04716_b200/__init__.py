@@ -18,6 +18,7 @@ from .bfp import (  # noqa: F401
     bfp_sub,
     bfp_vector,
     bfpraw_stride,
+    chain,
     classify,
     scalar_custom,
     split,

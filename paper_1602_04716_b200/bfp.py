@@ -359,6 +359,24 @@ def arith_f32(op: int, spec: format_spec, x: torch.Tensor, y: torch.Tensor,
     return z
 
 
+def chain(program: str, *vs: bfp_vector, out: bfp_vector | None = None) -> bfp_vector:
+    """Fused expression over bitslice vectors of one format (bfp_chain): postfix
+    `program` over inputs 'a', 'b', ... (vs[0], vs[1], ...) and + - * /, e.g.
+    chain("ab*cd*+", a, b, c, d) == bfp_add(bfp_mul(a, b), bfp_mul(c, d)) bit for
+    bit, in one kernel with the intermediates in registers."""
+    if not vs or len(vs) > 8:
+        raise ValueError("between 1 and 8 input vectors")
+    for v in vs[1:]:
+        require_same_shape(vs[0].spec, v.spec)
+        if v.count != vs[0].count:
+            raise ValueError("operands must have the same element count")
+    z = out if out is not None else empty(vs[0].spec, vs[0].count, vs[0].planes.device)
+    ptrs = (C.c_void_p * len(vs))(*[v.planes.data_ptr() for v in vs])
+    check(lib().bfp_chain(vs[0].spec.c, program.encode(), len(vs), ptrs, z.planes.data_ptr(), vs[0].count,
+                          _stream()), "chain")
+    return z
+
+
 # --------------------------------------------------------------------- host codec
 def encode_scalar(x: float, f: format_spec) -> int:
     """format.hpp:125-188: correctly rounded binary64 -> format (host, scalar)."""

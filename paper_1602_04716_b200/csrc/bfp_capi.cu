@@ -18,6 +18,8 @@ BFP_FORMAT_LIST(DECLARE_IMPL)
 #undef DECLARE_IMPL
 const Impl* jit_impl(unsigned e, unsigned s, int rn, int ftz);  // bfp_jit.cu
 bool jit_available();
+cudaError_t chain_launch(unsigned e, unsigned s, int rn, int ftz, const char* prog, const w32* const* in,
+                         int n_in, w32* z, size_t nblocks, cudaStream_t st);  // bfp_jit.cu
 }  // namespace bfpg
 
 using bfpg::Impl;
@@ -171,6 +173,45 @@ bfp_status bfp_arith(int op, const bfp_format* f, const uint32_t* d_x, const uin
   return cuda_status(impl->arith(op, d_x, d_y, d_c, d_z, nblocks(count),
                                  static_cast<cudaStream_t>(stream)),
                      "arith launch");
+}
+
+bfp_status bfp_chain(const bfp_format* f, const char* program, int n_inputs,
+                     const uint32_t* const* d_in, uint32_t* d_z, size_t count, void* stream) {
+  bfp_status s = validate(f);
+  if (s != BFP_OK) return s;
+  if (!program) return fail(BFP_EARG, "null program");
+  if (n_inputs < 1 || n_inputs > 8) return fail(BFP_EARG, "n_inputs must be in [1, 8]");
+  // canonical postfix: inputs 'a'.. (< n_inputs), ops + - * /, blanks ignored
+  std::string prog;
+  int depth = 0, ops = 0;
+  bool used[8] = {};
+  for (const char* c = program; *c; ++c) {
+    const char ch = *c;
+    if (ch == ' ' || ch == '\t') continue;
+    if (ch >= 'a' && ch < 'a' + n_inputs) {
+      used[ch - 'a'] = true;
+      ++depth;
+    } else if (ch == '+' || ch == '-' || ch == '*' || ch == '/') {
+      if (depth < 2) return fail(BFP_EARG, "program: operator without two operands");
+      --depth;
+      ++ops;
+    } else {
+      return fail(BFP_EARG, "program: unexpected character (inputs a.. and + - * / only)");
+    }
+    prog += ch;
+  }
+  if (depth != 1) return fail(BFP_EARG, "program must leave exactly one value");
+  if (ops > 64) return fail(BFP_EARG, "program: more than 64 operations");
+  if (count == 0) return BFP_OK;
+  if (!d_z || !d_in) return fail(BFP_EARG, "null operand");
+  for (int i = 0; i < n_inputs; ++i)
+    if (used[i] && !d_in[i]) return fail(BFP_EARG, "null operand");
+  if (!bfpg::jit_available()) return fail(BFP_EUNSUPPORTED, "bfp_chain needs NVRTC");
+  ++g_launches;
+  return cuda_status(bfpg::chain_launch(f->exp_bits, f->sig_bits, f->rounding == 1, f->subnormals == 1,
+                                        prog.c_str(), d_in, n_inputs, d_z, nblocks(count),
+                                        static_cast<cudaStream_t>(stream)),
+                     "chain launch");
 }
 
 bfp_status bfp_add(const bfp_format* f, const uint32_t* x, const uint32_t* y, uint32_t* z,

@@ -281,7 +281,151 @@ class JitFormat final : public Impl {
   mutable std::map<std::string, JitKernel> cache_;
 };
 
+// ---- fused expression programs (bfp_chain) --------------------------------
+// A postfix program over inputs 'a'..'h' and the ops + - * / becomes ONE
+// kernel: per unit the used inputs are loaded once, every op runs the same
+// network as the single-op kernels (eval_unit: the LOP3-mapped cover where
+// the format has one, else the template) with its result kept in registers,
+// and only the final value is stored.  Each op still rounds to the format,
+// so the result is bit-identical to the sequence of bfp_add/sub/mul/div calls;
+// the intermediates just never reach HBM.
+struct ChainKernel {
+  cudaKernel_t k = nullptr;
+  int wave = 0;
+};
+
+std::string chain_source(unsigned e, unsigned s, int rn, int ftz, const std::string& prog,
+                         bool with_gen) {
+  std::string src = "#include \"bfp_kernels.cuh\"\n";
+  if (with_gen) src += "#include \"gen/gen_" + std::to_string(e) + "_" + std::to_string(s) + ".cuh\"\n";
+  src += "struct BfpChainIn { const bfpg::w32* p[8]; };\n"
+         "extern \"C\" __global__ void __launch_bounds__(bfpg::kThreads)\n"
+         "bfp_chain_k(BfpChainIn in, bfpg::w32* __restrict__ z, size_t units) {\n"
+         "  using namespace bfpg;\n";
+  char buf[256];
+  std::snprintf(buf, sizeof buf, "  using F = Format<%u, %u, %s, %s>;\n", e, s, rn ? "true" : "false",
+                ftz ? "true" : "false");
+  src += buf;
+  src += "  constexpr int N = F::N;\n"
+         "  pdl_enter();\n"
+         "  const size_t stride = size_t(gridDim.x) * kThreads;\n"
+         "  for (size_t u = size_t(blockIdx.x) * kThreads + threadIdx.x; u < units; u += stride) {\n"
+         "    const size_t base = (u >> 5) * (size_t(N) * 32) + (u & 31);\n";
+  bool used[8] = {};
+  for (char ch : prog)
+    if (ch >= 'a' && ch <= 'h') used[ch - 'a'] = true;
+  for (int i = 0; i < 8; ++i)
+    if (used[i]) {
+      std::snprintf(buf, sizeof buf,
+                    "    w32 in%d[N];\n    BFP_UNROLL for (int j = 0; j < N; ++j) in%d[j] = "
+                    "ld_stream(in.p[%d] + base + j * 32);\n", i, i, i);
+      src += buf;
+    }
+  src += "    pdl_release_if(u + stride >= units);\n";
+  std::vector<std::string> stack;
+  int t = 0;
+  for (char ch : prog) {
+    if (ch >= 'a' && ch <= 'h') {
+      stack.push_back("in" + std::to_string(ch - 'a'));
+      continue;
+    }
+    const char* op = ch == '+' ? "OP_ADD" : ch == '-' ? "OP_SUB" : ch == '*' ? "OP_MUL" : "OP_DIV";
+    const std::string y = stack.back();
+    stack.pop_back();
+    const std::string x = stack.back();
+    stack.pop_back();
+    std::snprintf(buf, sizeof buf, "    w32 t%d[N];\n    eval_unit<F, %s>(%s, %s, %s, t%d);\n", t, op,
+                  x.c_str(), y.c_str(), x.c_str(), t);
+    src += buf;
+    stack.push_back("t" + std::to_string(t++));
+  }
+  src += "    BFP_UNROLL for (int j = 0; j < N; ++j) st_stream(z + base + j * 32, " + stack.back() +
+         "[j]);\n  }\n}\n";
+  return src;
+}
+
+cudaError_t chain_kernel(unsigned e, unsigned s, int rn, int ftz, const std::string& prog,
+                         ChainKernel* out) {
+  static std::mutex mu;
+  static std::map<std::string, ChainKernel> cache;
+  char key[64];
+  std::snprintf(key, sizeof key, "%u/%u/%d/%d:", e, s, rn, ftz);
+  const std::string k = key + prog;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find(k);
+  if (it != cache.end()) {
+    *out = it->second;
+    return cudaSuccess;
+  }
+  const Nvrtc& nv = nvrtc();
+  if (!nv.ok) return cudaErrorNotSupported;
+  // the format's LOP3-mapped covers when it has them (csrc/gen), else templates
+  const std::string gen = csrc_dir() + "/gen/gen_" + std::to_string(e) + "_" + std::to_string(s) + ".cuh";
+  FILE* fg = std::getenv("BFP_CHAIN_NOGEN") ? nullptr : std::fopen(gen.c_str(), "r");
+  if (fg) std::fclose(fg);
+  const std::string src = chain_source(e, s, rn, ftz, prog, fg != nullptr);
+  const std::string inc = "--include-path=" + csrc_dir();
+  const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", inc.c_str(), "-default-device",
+                        "-lineinfo"};
+  nvrtcProgram_t p = nullptr;
+  if (nv.create(&p, src.c_str(), "bfp_chain.cu", 0, nullptr, nullptr)) return cudaErrorNotSupported;
+  if (nv.compile(p, 5, opts) != 0) {
+    size_t ls = 0;
+    nv.log_size(p, &ls);
+    std::string log(ls, '\0');
+    nv.log(p, log.data());
+    std::fprintf(stderr, "[bfp jit] NVRTC failed for chain %s:\n%s\n", k.c_str(), log.c_str());
+    nv.destroy(&p);
+    return cudaErrorNotSupported;
+  }
+  size_t n = 0;
+  nv.cubin_size(p, &n);
+  std::vector<char> cubin(n);
+  nv.cubin(p, cubin.data());
+  nv.destroy(&p);
+  cudaLibrary_t lib = nullptr;
+  cudaError_t err = cudaLibraryLoadData(&lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
+  if (err != cudaSuccess) return err;
+  ChainKernel ck;
+  if ((err = cudaLibraryGetKernel(&ck.k, lib, "bfp_chain_k")) != cudaSuccess) return err;
+  int dev = 0, sms = 0, occ = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, reinterpret_cast<const void*>(ck.k), kThreads,
+                                                    0) != cudaSuccess || occ <= 0) {
+    cudaGetLastError();
+    occ = 2;
+  }
+  ck.wave = (sms > 0 ? sms : 148) * occ;
+  cache[k] = ck;
+  *out = ck;
+  return cudaSuccess;
+}
+
 }  // namespace
+
+cudaError_t chain_launch(unsigned e, unsigned s, int rn, int ftz, const char* prog, const w32* const* in,
+                         int n_in, w32* z, size_t nblocks, cudaStream_t st) {
+  ChainKernel k;
+  cudaError_t err = chain_kernel(e, s, rn, ftz, prog, &k);
+  if (err != cudaSuccess) return err;
+  struct {
+    const w32* p[8];
+  } ptrs = {};
+  for (int i = 0; i < n_in && i < 8; ++i) ptrs.p[i] = in[i];
+  size_t units = nblocks * 32;
+  void* argv[] = {&ptrs, &z, &units};
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid_for(k.wave, units));
+  cfg.blockDim = dim3(kThreads);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(k.k), argv);
+}
 
 bool jit_available() { return nvrtc().ok; }
 

@@ -50,6 +50,13 @@ int main() {
       }
       for (double v : {1.5, -3.25, 1e-6, 65504.0, 7e5})
         if (g::encode_scalar(v, spec) != orc_encode(v, e, s, rn, 0)) ++fails;
+      // fused expression == the same ops one call at a time
+      const auto ch = g::unpack(g::chain("ab*ab-/", {&x, &y}), n);
+      const auto seq = g::unpack(g::bfp_div(g::bfp_mul(x, y), g::bfp_sub(x, y)), n);
+      if (ch != seq) {
+        std::printf("chain mismatch 1/%u/%u\n", e, s);
+        ++fails;
+      }
     }
   }
   // .bfpraw round trip through the device, a 51-bit format (runtime backend)

@@ -125,3 +125,18 @@ def test_split_classify_mirror(oracle):
                     else bfp.value_class.zero if x == 0 else bfp.value_class.subnormal
                     if abs(x) < 2.0 ** f.emin() else bfp.value_class.normal)
             assert bfp.classify(enc, f) == want, (e, s, enc)
+
+
+def test_chain_program_validation(L):
+    """bfp_chain rejects malformed programs before touching the device."""
+    import ctypes as C
+    from paper_1602_04716_b200 import _lib
+    f = _lib.BfpFormat(4, 3, 1, 0, b"")
+    ptrs = (C.c_void_p * 2)(None, None)
+    for prog in (b"a+", b"ab", b"abc+", b"ax+", b"ab%", b"", b"ac+"):
+        assert L.bfp_chain(C.byref(f), prog, 2, ptrs, None, 1024, None) == _lib.BFP_EARG, prog
+    assert L.bfp_chain(C.byref(f), b"ab+", 9, ptrs, None, 1024, None) == _lib.BFP_EARG
+    assert L.bfp_chain(C.byref(f), None, 2, ptrs, None, 1024, None) == _lib.BFP_EARG
+    bad = _lib.BfpFormat(1, 3, 1, 0, b"")
+    assert L.bfp_chain(C.byref(bad), b"ab+", 2, ptrs, None, 1024, None) == _lib.BFP_EFORMAT
+    assert L.bfp_chain(C.byref(f), b" a b + ", 2, ptrs, None, 0, None) == _lib.BFP_OK  # count 0

@@ -1,0 +1,78 @@
+"""bfp_chain (fused expression programs, NVRTC-compiled): bit-identical to the
+same sequence of single-op calls, and to the oracle's composition."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import operands
+
+import paper_1602_04716_b200 as bfp
+
+pytestmark = pytest.mark.gpu
+
+OPS = {"+": bfp.bfp_add, "-": bfp.bfp_sub, "*": bfp.bfp_mul, "/": bfp.bfp_div}
+ONAME = {"+": "add", "-": "sub", "*": "mul", "/": "div"}
+
+
+def _eval_seq(prog, vs):
+    st = []
+    for ch in prog:
+        if ch.isalpha():
+            st.append(vs[ord(ch) - 97])
+        else:
+            y, x = st.pop(), st.pop()
+            st.append(OPS[ch](x, y))
+    return st[0]
+
+
+def _eval_oracle(oracle, prog, fmt, encs):
+    st = []
+    for ch in prog:
+        if ch.isalpha():
+            st.append(encs[ord(ch) - 97])
+        else:
+            y, x = st.pop(), st.pop()
+            st.append(oracle.binop(ONAME[ch], fmt, x, y))
+    return st[0]
+
+
+PROGRAMS = ["ab*c+", "ab*cd*+", "ab+c/", "ab-ab+*", "abc**d-", "ab/ba/-", "aa*a*a*", "ab*c+d*e-"]
+
+
+@pytest.mark.parametrize("fmt", [(4, 3, 1, 0), (5, 10, 1, 0), (6, 9, 0, 1), (8, 15, 1, 0), (7, 20, 1, 0)])
+@pytest.mark.parametrize("prog", PROGRAMS)
+def test_chain_matches_sequence_and_oracle(oracle, fmt, prog):
+    e, s, rn, ftz = fmt
+    spec = bfp.make_spec(e, s, rn, ftz)
+    k = max(ord(c) - 96 for c in prog if c.isalpha())
+    rng = np.random.default_rng(hash((fmt, prog)) & 0xFFFF)
+    n = 3 * 1024 + 77
+    encs = [operands(e, s, n, rng) for _ in range(k)]
+    vs = [bfp.pack(torch.from_numpy(x.astype(np.int64)).cuda(), spec) for x in encs]
+    z = bfp.chain(prog, *vs)
+    seq = _eval_seq(prog, vs)
+    assert torch.equal(z.planes, seq.planes), "chain != sequence of single-op calls"
+    got = bfp.to_u64(bfp.unpack(z), spec).cpu().numpy().astype(np.uint64)
+    assert np.array_equal(got, _eval_oracle(oracle, prog, fmt, encs))
+
+
+def test_chain_mul_add_equals_fused_kernel():
+    spec = bfp.make_spec(6, 9)
+    rng = np.random.default_rng(5)
+    n = 1 << 20
+    vs = [bfp.pack(torch.from_numpy(operands(6, 9, n, rng).astype(np.int64)).cuda(), spec) for _ in range(3)]
+    assert torch.equal(bfp.chain("ab*c+", *vs).planes, bfp.bfp_mul_add(*vs).planes)
+
+
+def test_chain_errors():
+    spec = bfp.make_spec(4, 3)
+    other = bfp.make_spec(4, 3, name="other")
+    a = bfp.empty(spec, 100)
+    with pytest.raises(ValueError):
+        bfp.chain("ab+", a, bfp.empty(other, 100))  # require_same_shape, name included
+    with pytest.raises(ValueError):
+        bfp.chain("ab+", a, bfp.empty(spec, 99))
+    with pytest.raises(ValueError):
+        bfp.chain("a+", a, a)
