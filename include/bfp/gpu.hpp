@@ -349,6 +349,14 @@ inline bfp_vector chain(const char* program, std::initializer_list<const bfp_vec
   detail::check(bfp_chain(&f, program, int(ptrs.size()), ptrs.data(), z.planes(), x.size(), st), "chain");
   return z;
 }
+// bfp_chain_f32: float32 device arrays in and out (count elements each).
+inline void chain_f32(const char* program, const format_spec& spec, std::initializer_list<const float*> d_in,
+                      float* d_out, std::size_t count, cudaStream_t st = nullptr) {
+  validate(spec);
+  const std::vector<const float*> ptrs(d_in);
+  const bfp_format f = spec.c();
+  detail::check(bfp_chain_f32(&f, program, int(ptrs.size()), ptrs.data(), d_out, count, st), "chain_f32");
+}
 
 // Host scalar codec (format.hpp:101-188).
 inline double decode_scalar(encoding enc, const format_spec& f) {

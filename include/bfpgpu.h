@@ -145,6 +145,12 @@ bfp_status bfp_arith_f32(int op, const bfp_format* f, const float* d_x, const fl
  * reference's bfp_* calls ("longer chains"). */
 bfp_status bfp_chain(const bfp_format* f, const char* program, int n_inputs,
                      const uint32_t* const* d_in, uint32_t* d_z, size_t count, void* stream);
+/* The same over float32 arrays: every input through encode_scalar, the
+ * program in the format, the result through decode_scalar -- one kernel,
+ * 4 B/elem per input + 4 B/elem out (E <= 8, S <= 23).  Equals
+ * unpack_f32(bfp_chain(program, pack_f32(x0), pack_f32(x1), ...)). */
+bfp_status bfp_chain_f32(const bfp_format* f, const char* program, int n_inputs,
+                         const float* const* d_in, float* d_z, size_t count, void* stream);
 
 /* ---- host-buffer entry points (pipelined H2D / kernel [/ D2H]) ---------- */
 typedef struct bfp_host_ctx bfp_host_ctx;

@@ -19,6 +19,7 @@ from .bfp import (  # noqa: F401
     bfp_vector,
     bfpraw_stride,
     chain,
+    chain_f32,
     classify,
     scalar_custom,
     split,

@@ -58,6 +58,7 @@ SIGNATURES = {
     "bfp_arith_f32": (C.c_int, [C.c_int, _F, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                 C.c_size_t, C.c_void_p]),
     "bfp_chain": (C.c_int, [_F, C.c_char_p, C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
+    "bfp_chain_f32": (C.c_int, [_F, C.c_char_p, C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
     "bfp_host_ctx_create": (C.c_void_p, [C.c_size_t]),
     "bfp_host_ctx_destroy": (None, [C.c_void_p]),
     "bfp_arith_host": (C.c_int, [C.c_void_p, C.c_int, _F, C.c_void_p, C.c_void_p, C.c_void_p,

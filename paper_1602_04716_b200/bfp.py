@@ -377,6 +377,23 @@ def chain(program: str, *vs: bfp_vector, out: bfp_vector | None = None) -> bfp_v
     return z
 
 
+def chain_f32(program: str, spec: format_spec, *xs: torch.Tensor) -> torch.Tensor:
+    """bfp_chain_f32: the program over float32 tensors in `spec` (each input
+    through encode_scalar, the result through decode_scalar), one kernel;
+    == unpack_f32(chain(program, pack_f32(x0, spec), pack_f32(x1, spec), ...))."""
+    validate(spec)
+    if not xs or len(xs) > 8:
+        raise ValueError("between 1 and 8 inputs")
+    xs = tuple(x.to(torch.float32).contiguous() for x in xs)
+    if any(x.numel() != xs[0].numel() for x in xs):
+        raise ValueError("operands must have the same element count")
+    z = torch.empty_like(xs[0])
+    ptrs = (C.c_void_p * len(xs))(*[x.data_ptr() for x in xs])
+    check(lib().bfp_chain_f32(spec.c, program.encode(), len(xs), ptrs, z.data_ptr(), xs[0].numel(), _stream()),
+          "chain_f32")
+    return z
+
+
 # --------------------------------------------------------------------- host codec
 def encode_scalar(x: float, f: format_spec) -> int:
     """format.hpp:125-188: correctly rounded binary64 -> format (host, scalar)."""

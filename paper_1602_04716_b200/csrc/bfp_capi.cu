@@ -18,8 +18,8 @@ BFP_FORMAT_LIST(DECLARE_IMPL)
 #undef DECLARE_IMPL
 const Impl* jit_impl(unsigned e, unsigned s, int rn, int ftz);  // bfp_jit.cu
 bool jit_available();
-cudaError_t chain_launch(unsigned e, unsigned s, int rn, int ftz, const char* prog, const w32* const* in,
-                         int n_in, w32* z, size_t nblocks, cudaStream_t st);  // bfp_jit.cu
+cudaError_t chain_launch(unsigned e, unsigned s, int rn, int ftz, const char* prog, bool f32,
+                         const void* const* in, int n_in, void* z, size_t count, cudaStream_t st);  // bfp_jit.cu
 }  // namespace bfpg
 
 using bfpg::Impl;
@@ -175,10 +175,13 @@ bfp_status bfp_arith(int op, const bfp_format* f, const uint32_t* d_x, const uin
                      "arith launch");
 }
 
-bfp_status bfp_chain(const bfp_format* f, const char* program, int n_inputs,
-                     const uint32_t* const* d_in, uint32_t* d_z, size_t count, void* stream) {
+namespace {
+bfp_status chain_common(const bfp_format* f, const char* program, int n_inputs, const void* const* d_in,
+                        void* d_z, size_t count, void* stream, bool f32) {
   bfp_status s = validate(f);
   if (s != BFP_OK) return s;
+  if (f32 && (f->exp_bits > 8 || f->sig_bits > 23))
+    return fail(BFP_EUNSUPPORTED, "float32 codec needs exp_bits <= 8 and sig_bits <= 23");
   if (!program) return fail(BFP_EARG, "null program");
   if (n_inputs < 1 || n_inputs > 8) return fail(BFP_EARG, "n_inputs must be in [1, 8]");
   // canonical postfix: inputs 'a'.. (< n_inputs), ops + - * /, blanks ignored
@@ -209,9 +212,22 @@ bfp_status bfp_chain(const bfp_format* f, const char* program, int n_inputs,
   if (!bfpg::jit_available()) return fail(BFP_EUNSUPPORTED, "bfp_chain needs NVRTC");
   ++g_launches;
   return cuda_status(bfpg::chain_launch(f->exp_bits, f->sig_bits, f->rounding == 1, f->subnormals == 1,
-                                        prog.c_str(), d_in, n_inputs, d_z, nblocks(count),
+                                        prog.c_str(), f32, d_in, n_inputs, d_z, count,
                                         static_cast<cudaStream_t>(stream)),
                      "chain launch");
+}
+}  // namespace
+
+bfp_status bfp_chain(const bfp_format* f, const char* program, int n_inputs,
+                     const uint32_t* const* d_in, uint32_t* d_z, size_t count, void* stream) {
+  return chain_common(f, program, n_inputs, reinterpret_cast<const void* const*>(d_in), d_z, count, stream,
+                      false);
+}
+
+bfp_status bfp_chain_f32(const bfp_format* f, const char* program, int n_inputs, const float* const* d_in,
+                         float* d_z, size_t count, void* stream) {
+  return chain_common(f, program, n_inputs, reinterpret_cast<const void* const*>(d_in), d_z, count, stream,
+                      true);
 }
 
 bfp_status bfp_add(const bfp_format* f, const uint32_t* x, const uint32_t* y, uint32_t* z,

@@ -294,34 +294,53 @@ struct ChainKernel {
   int wave = 0;
 };
 
+// f32: float32 inputs / output (encode_scalar / decode_scalar in registers, the
+// k_arith_f32 structure: per-warp smem tiles for the element-side accesses).
 std::string chain_source(unsigned e, unsigned s, int rn, int ftz, const std::string& prog,
-                         bool with_gen) {
+                         bool with_gen, bool f32) {
   std::string src = "#include \"bfp_kernels.cuh\"\n";
   if (with_gen) src += "#include \"gen/gen_" + std::to_string(e) + "_" + std::to_string(s) + ".cuh\"\n";
-  src += "struct BfpChainIn { const bfpg::w32* p[8]; };\n"
-         "extern \"C\" __global__ void __launch_bounds__(bfpg::kThreads)\n"
-         "bfp_chain_k(BfpChainIn in, bfpg::w32* __restrict__ z, size_t units) {\n"
-         "  using namespace bfpg;\n";
-  char buf[256];
+  if (f32)
+    src += "struct BfpChainIn { const float* p[8]; };\n"
+           "extern \"C\" __global__ void __launch_bounds__(bfpg::kThreads)\n"
+           "bfp_chain_k(BfpChainIn in, float* __restrict__ z, size_t n, size_t units, bool aligned) {\n"
+           "  using namespace bfpg;\n";
+  else
+    src += "struct BfpChainIn { const bfpg::w32* p[8]; };\n"
+           "extern \"C\" __global__ void __launch_bounds__(bfpg::kThreads)\n"
+           "bfp_chain_k(BfpChainIn in, bfpg::w32* __restrict__ z, size_t units) {\n"
+           "  using namespace bfpg;\n";
+  char buf[512];
   std::snprintf(buf, sizeof buf, "  using F = Format<%u, %u, %s, %s>;\n", e, s, rn ? "true" : "false",
                 ftz ? "true" : "false");
   src += buf;
   src += "  constexpr int N = F::N;\n"
          "  pdl_enter();\n"
-         "  const size_t stride = size_t(gridDim.x) * kThreads;\n"
-         "  for (size_t u = size_t(blockIdx.x) * kThreads + threadIdx.x; u < units; u += stride) {\n"
+         "  const size_t stride = size_t(gridDim.x) * kThreads;\n";
+  if (f32)
+    src += "  __shared__ __align__(16) w32 tiles[kThreads / 32][1024];\n"
+           "  const int lane = threadIdx.x & 31;\n"
+           "  w32* tile = tiles[threadIdx.x >> 5];\n";
+  src += "  for (size_t u = size_t(blockIdx.x) * kThreads + threadIdx.x; u < units; u += stride) {\n"
          "    const size_t base = (u >> 5) * (size_t(N) * 32) + (u & 31);\n";
   bool used[8] = {};
   for (char ch : prog)
     if (ch >= 'a' && ch <= 'h') used[ch - 'a'] = true;
   for (int i = 0; i < 8; ++i)
     if (used[i]) {
-      std::snprintf(buf, sizeof buf,
-                    "    w32 in%d[N];\n    BFP_UNROLL for (int j = 0; j < N; ++j) in%d[j] = "
-                    "ld_stream(in.p[%d] + base + j * 32);\n", i, i, i);
+      if (f32)
+        std::snprintf(buf, sizeof buf,
+                      "    w32 in%d[N];\n    {\n      w32 V[32], P[32];\n"
+                      "      warp_load_elems<4>(reinterpret_cast<const uint8_t*>(in.p[%d]), u, n, aligned, "
+                      "tile, lane, V);\n      floats_to_planes<F>(V, P);\n"
+                      "      BFP_UNROLL for (int j = 0; j < N; ++j) in%d[j] = P[j];\n    }\n", i, i, i);
+      else
+        std::snprintf(buf, sizeof buf,
+                      "    w32 in%d[N];\n    BFP_UNROLL for (int j = 0; j < N; ++j) in%d[j] = "
+                      "ld_stream(in.p[%d] + base + j * 32);\n", i, i, i);
       src += buf;
     }
-  src += "    pdl_release_if(u + stride >= units);\n";
+  if (!f32) src += "    pdl_release_if(u + stride >= units);\n";
   std::vector<std::string> stack;
   int t = 0;
   for (char ch : prog) {
@@ -339,17 +358,24 @@ std::string chain_source(unsigned e, unsigned s, int rn, int ftz, const std::str
     src += buf;
     stack.push_back("t" + std::to_string(t++));
   }
-  src += "    BFP_UNROLL for (int j = 0; j < N; ++j) st_stream(z + base + j * 32, " + stack.back() +
-         "[j]);\n  }\n}\n";
+  if (f32)
+    src += "    w32 P[32];\n    BFP_UNROLL for (int j = 0; j < 32; ++j) P[j] = j < N ? " + stack.back() +
+           "[j] : 0u;\n    w32 V[32];\n    planes_to_floats<F>(P, V);\n"
+           "    warp_store_elems<4>(reinterpret_cast<uint8_t*>(z), u, n, aligned, tile, lane, V);\n"
+           "    pdl_release_if(u + stride >= units);\n  }\n}\n";
+  else
+    src += "    BFP_UNROLL for (int j = 0; j < N; ++j) st_stream(z + base + j * 32, " + stack.back() +
+           "[j]);\n  }\n}\n";
+  (void)used;
   return src;
 }
 
-cudaError_t chain_kernel(unsigned e, unsigned s, int rn, int ftz, const std::string& prog,
+cudaError_t chain_kernel(unsigned e, unsigned s, int rn, int ftz, const std::string& prog, bool f32,
                          ChainKernel* out) {
   static std::mutex mu;
   static std::map<std::string, ChainKernel> cache;
   char key[64];
-  std::snprintf(key, sizeof key, "%u/%u/%d/%d:", e, s, rn, ftz);
+  std::snprintf(key, sizeof key, "%u/%u/%d/%d/%s:", e, s, rn, ftz, f32 ? "f32" : "planes");
   const std::string k = key + prog;
   std::lock_guard<std::mutex> lock(mu);
   auto it = cache.find(k);
@@ -363,7 +389,7 @@ cudaError_t chain_kernel(unsigned e, unsigned s, int rn, int ftz, const std::str
   const std::string gen = csrc_dir() + "/gen/gen_" + std::to_string(e) + "_" + std::to_string(s) + ".cuh";
   FILE* fg = std::getenv("BFP_CHAIN_NOGEN") ? nullptr : std::fopen(gen.c_str(), "r");
   if (fg) std::fclose(fg);
-  const std::string src = chain_source(e, s, rn, ftz, prog, fg != nullptr);
+  const std::string src = chain_source(e, s, rn, ftz, prog, fg != nullptr, f32);
   const std::string inc = "--include-path=" + csrc_dir();
   const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", inc.c_str(), "-default-device",
                         "-lineinfo"};
@@ -404,17 +430,26 @@ cudaError_t chain_kernel(unsigned e, unsigned s, int rn, int ftz, const std::str
 
 }  // namespace
 
-cudaError_t chain_launch(unsigned e, unsigned s, int rn, int ftz, const char* prog, const w32* const* in,
-                         int n_in, w32* z, size_t nblocks, cudaStream_t st) {
+// in / z: plane buffers (f32 = false) or float32 arrays of count elements.
+cudaError_t chain_launch(unsigned e, unsigned s, int rn, int ftz, const char* prog, bool f32,
+                         const void* const* in, int n_in, void* z, size_t count, cudaStream_t st) {
   ChainKernel k;
-  cudaError_t err = chain_kernel(e, s, rn, ftz, prog, &k);
+  cudaError_t err = chain_kernel(e, s, rn, ftz, prog, f32, &k);
   if (err != cudaSuccess) return err;
   struct {
-    const w32* p[8];
+    const void* p[8];
   } ptrs = {};
-  for (int i = 0; i < n_in && i < 8; ++i) ptrs.p[i] = in[i];
-  size_t units = nblocks * 32;
-  void* argv[] = {&ptrs, &z, &units};
+  uintptr_t bits = reinterpret_cast<uintptr_t>(z);
+  for (int i = 0; i < n_in && i < 8; ++i) {
+    ptrs.p[i] = in[i];
+    bits |= reinterpret_cast<uintptr_t>(in[i]);
+  }
+  size_t n = count;
+  size_t units = ((count + 1023) / 1024) * 32;
+  bool aligned = (bits & 15) == 0;
+  void* argv_planes[] = {&ptrs, &z, &units};
+  void* argv_f32[] = {&ptrs, &z, &n, &units, &aligned};
+  void** argv = f32 ? argv_f32 : argv_planes;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid_for(k.wave, units));
   cfg.blockDim = dim3(kThreads);

@@ -140,3 +140,13 @@ def test_chain_program_validation(L):
     bad = _lib.BfpFormat(1, 3, 1, 0, b"")
     assert L.bfp_chain(C.byref(bad), b"ab+", 2, ptrs, None, 1024, None) == _lib.BFP_EFORMAT
     assert L.bfp_chain(C.byref(f), b" a b + ", 2, ptrs, None, 0, None) == _lib.BFP_OK  # count 0
+
+
+def test_chain_f32_validation(L):
+    import ctypes as C
+    from paper_1602_04716_b200 import _lib
+    ptrs = (C.c_void_p * 2)(None, None)
+    wide = _lib.BfpFormat(8, 23 + 1, 1, 0, b"")  # no float32 codec beyond s = 23
+    assert L.bfp_chain_f32(C.byref(wide), b"ab+", 2, ptrs, None, 1024, None) == _lib.BFP_EUNSUPPORTED
+    f = _lib.BfpFormat(5, 10, 1, 0, b"")
+    assert L.bfp_chain_f32(C.byref(f), b"ab", 2, ptrs, None, 1024, None) == _lib.BFP_EARG

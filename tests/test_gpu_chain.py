@@ -76,3 +76,18 @@ def test_chain_errors():
         bfp.chain("ab+", a, bfp.empty(spec, 99))
     with pytest.raises(ValueError):
         bfp.chain("a+", a, a)
+
+
+@pytest.mark.parametrize("fmt", [(4, 3, 1, 0), (5, 10, 1, 1), (8, 7, 0, 0), (6, 9, 1, 0), (7, 20, 1, 0)])
+@pytest.mark.parametrize("prog", ["ab*c+", "ab+ab-*", "ab/"])
+def test_chain_f32_matches_planes_chain(fmt, prog):
+    e, s, rn, ftz = fmt
+    spec = bfp.make_spec(e, s, rn, ftz)
+    g = torch.Generator(device="cuda").manual_seed(e * 100 + s)
+    n = 5 * 1024 + 333  # ragged tail
+    k = max(ord(c) - 96 for c in prog if c.isalpha())
+    xs = [(torch.randn(n, device="cuda", generator=g) * 50).float() for _ in range(k)]
+    xs[0][:7] = torch.tensor([0.0, -0.0, float("inf"), float("nan"), 1e-30, -3e38, 65504.0], device="cuda")
+    got = bfp.chain_f32(prog, spec, *xs)
+    want = bfp.unpack_f32(bfp.chain(prog, *[bfp.pack_f32(x, spec) for x in xs]))
+    assert torch.equal(got.view(torch.int32), want.view(torch.int32))
