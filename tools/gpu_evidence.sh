@@ -16,7 +16,7 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 fi
 ARGS=""
 for cfg in ${CFGS:-C1 C2 C3 C4 C5}; do
-  case $cfg in C3) K='regex:k_(arith|pack_f32|unpack_f32)';; *) K='regex:k_arith';; esac
+  case $cfg in C3) K='regex:k_(arith|pack_f32|unpack_f32)';; X3) K='regex:bfp_chain_k';; *) K='regex:k_arith';; esac
   timeout 900 ncu --set full --clock-control none --import-source on -k "$K" \
     -o /tmp/ncu/$cfg -f python tools/profile_kernels.py --config $cfg --iters 1 > gpurun_out/ncu/$cfg.log 2>&1; echo prof_${cfg}_rc=$?
   ARGS="$ARGS $cfg=/tmp/ncu/$cfg.ncu-rep"

@@ -45,14 +45,19 @@ def rows(rep: str) -> list[dict]:
 
 
 def label(cfg: str, kernel: str) -> str | None:
-    m = re.search(r"k_(arith|pack_f32|unpack_f32)<\S*Format<(\d+), (\d+)[^>]*>(?:, (\d+))?", kernel)
+    if kernel.startswith("bfp_chain_k"):
+        return "a*b+c*d" if cfg.startswith("X3") else None
+    m = re.search(r"k_(arith_f32|arith|pack_f32|unpack_f32)<\S*Format<(\d+), (\d+)[^>]*>(?:, (\d+))?",
+                  kernel)
     if not m:
         return None
     kind, e, s = m.group(1), int(m.group(2)), int(m.group(3))
+    if kind == "arith_f32":
+        return f"{OPS[int(m.group(4))]}_f32"
     if kind != "arith":
         return kind
     op = OPS[int(m.group(4))]
-    return f"{op}_1/{e}/{s}" if cfg.startswith("C4") else op
+    return f"{op}_1/{e}/{s}" if cfg.startswith(("C4", "X1")) else op
 
 
 def main() -> None:
