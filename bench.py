@@ -65,7 +65,8 @@ class ClockSampler:
 
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,"
+              "power.limit")
 
     def __init__(self, device_index: int):
         self.dev = device_index
@@ -107,9 +108,14 @@ class ClockSampler:
             for nm, v in zip(names, r[4:8]):
                 if v.lower() == "active":
                     reasons.add(nm)
+        num = lambda v: float(v) if v.replace(".", "", 1).isdigit() else None
+        pw = [num(r[2]) for r in self.rows if len(r) >= 8 and num(r[2]) is not None]
+        lim = [num(r[8]) for r in self.rows if len(r) >= 9 and num(r[8]) is not None]
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None,
-                "samples": len(sm), "reasons": sorted(reasons)}
+                "samples": len(sm), "reasons": sorted(reasons),
+                "power_w": round(statistics.median(pw), 1) if pw else None,
+                "power_limit_w": max(lim) if lim else None}
 
 
 def clocks_rejected(c: dict) -> bool:
@@ -964,6 +970,9 @@ def main_ours(args) -> None:
                                 "programmatic dependent launch); per-kernel figures above come "
                                 "from one graph per kernel holding its K launches",
                         "ms_per_step_eager": round(res["ms_total_eager"] / args.steps, 5)}
+        pw = res["clocks"].get("power_w")
+        if pw:  # board energy per result element at the sampled draw (the logic kernels run power-capped)
+            roof["step"]["pj_per_elem"] = round(pw * ms_step * 1e-3 / (total_elems / world) * 1e12, 1)
         dd = per_op[jd.label]
         if "binding" in dd:
             roof["binding_leg"] = dd["binding"]
