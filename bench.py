@@ -146,7 +146,7 @@ def sass_lop3(fmt, rn, ftz, op: int) -> int | None:
         for name, r in _SASS.items():
             if key in name:
                 return r["LOP3"]
-    except Exception:
+    except (OSError, subprocess.SubprocessError, ValueError, KeyError):  # no cuobjdump / odd SASS
         return None
     return None
 
