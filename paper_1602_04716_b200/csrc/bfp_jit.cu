@@ -2,14 +2,19 @@
 // format_spec (format.hpp:57-64: e in [2,11], s in [1,52], n <= 64) is
 // accepted.  Formats without a compiled network get the SAME templates
 // (bfp_kernels.cuh) compiled on first use by NVRTC for sm_100a, per kernel,
-// cached for the life of the process -- the role of the paper's library
-// generator (exponent/mantissa/rounding in, library out).
+// cached for the life of the process and as CUBIN files on disk (see
+// nvrtc_compile) -- the role of the paper's library generator (PAPER.md:296:
+// exponent/mantissa/rounding in, library out).  Fused expression programs
+// (bfp_chain, bfp_chain_f32) are compiled the same way.
 //
 // libnvrtc is dlopen'ed (no link-time dependency); the CUBIN is loaded with
 // cudaLibraryLoadData and launched with cudaLaunchKernelExC (PDL attribute as
 // for the compiled kernels).  Disabled with BFP_JIT=0.
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
 
 #include <cstdio>
 #include <cstdlib>
@@ -81,6 +86,107 @@ std::string csrc_dir() {
     return (slash == std::string::npos ? std::string(".") : p.substr(0, slash)) + "/csrc";
   }
   return "csrc";
+}
+
+// ---- NVRTC compile with an on-disk CUBIN cache --------------------------
+// Key: FNV-1a over this library's path, size and mtime (a rebuilt library --
+// new headers, new networks -- invalidates every entry), the source, the name
+// expression and the options.  Directory: $BFP_JIT_CACHE, else
+// $HOME/.cache/bfpgpu; BFP_JIT_CACHE=0 disables it.  Entries are written to a
+// temporary file and renamed, so concurrent processes never see a torn file.
+std::string library_identity() {
+  Dl_info info;
+  if (!dladdr(reinterpret_cast<void*>(&library_identity), &info) || !info.dli_fname) return "?";
+  struct stat st {};
+  if (stat(info.dli_fname, &st) != 0) return info.dli_fname;
+  return std::string(info.dli_fname) + ":" + std::to_string(st.st_size) + ":" + std::to_string(st.st_mtime);
+}
+
+std::string cache_dir() {
+  const char* env = std::getenv("BFP_JIT_CACHE");
+  if (env && std::strcmp(env, "0") == 0) return "";
+  if (env && *env) return env;
+  const char* home = std::getenv("HOME");
+  return home ? std::string(home) + "/.cache/bfpgpu" : "";
+}
+
+uint64_t fnv1a(const std::string& s, uint64_t h = 1469598103934665603ull) {
+  for (unsigned char c : s) h = (h ^ c) * 1099511628211ull;
+  return h;
+}
+
+// Compiles `src` (one translation unit including bfp_kernels.cuh) for sm_100a;
+// returns the CUBIN and the lowered name of `expr` (or `expr` itself when it
+// names an extern "C" kernel: lower = false).
+bool nvrtc_compile(const std::string& src, const std::string& expr, bool lower, std::vector<char>* cubin,
+                   std::string* name) {
+  const Nvrtc& nv = nvrtc();
+  if (!nv.ok) return false;
+  const std::string inc = "--include-path=" + csrc_dir();
+  const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", inc.c_str(), "-default-device",
+                        "-lineinfo"};
+  const std::string dir = cache_dir();
+  std::string path;
+  if (!dir.empty()) {
+    std::string key = library_identity() + "\n" + src + "\n" + expr;
+    for (const char* o : opts) key += std::string("\n") + o;
+    char hex[24];
+    std::snprintf(hex, sizeof hex, "%016llx", static_cast<unsigned long long>(fnv1a(key)));
+    path = dir + "/" + hex + ".cubin";
+    if (FILE* f = std::fopen(path.c_str(), "rb")) {  // [u32 name length][name][cubin]
+      uint32_t nl = 0;
+      bool ok = std::fread(&nl, 4, 1, f) == 1 && nl < 4096;
+      std::string nm(ok ? nl : 0, '\0');
+      ok = ok && std::fread(nm.data(), 1, nl, f) == nl;
+      std::vector<char> bin;
+      char buf[65536];
+      size_t r;
+      while (ok && (r = std::fread(buf, 1, sizeof buf, f)) > 0) bin.insert(bin.end(), buf, buf + r);
+      std::fclose(f);
+      if (ok && !bin.empty()) {
+        *cubin = std::move(bin);
+        *name = nm;
+        return true;
+      }
+    }
+  }
+  nvrtcProgram_t prog = nullptr;
+  if (nv.create(&prog, src.c_str(), "bfp_jit.cu", 0, nullptr, nullptr)) return false;
+  if (lower) nv.add_name(prog, expr.c_str());
+  if (nv.compile(prog, 5, opts) != 0) {
+    size_t ls = 0;
+    nv.log_size(prog, &ls);
+    std::string log(ls, '\0');
+    nv.log(prog, log.data());
+    std::fprintf(stderr, "[bfp jit] NVRTC failed for %s:\n%s\n", expr.c_str(), log.c_str());
+    nv.destroy(&prog);
+    return false;
+  }
+  if (lower) {
+    const char* lowered = nullptr;
+    nv.lowered(prog, expr.c_str(), &lowered);
+    *name = lowered ? lowered : "";
+  } else {
+    *name = expr;
+  }
+  size_t n = 0;
+  nv.cubin_size(prog, &n);
+  cubin->assign(n, 0);
+  nv.cubin(prog, cubin->data());
+  nv.destroy(&prog);
+  if (!path.empty()) {
+    for (size_t i = 1; i <= dir.size(); ++i)  // mkdir -p
+      if (i == dir.size() || dir[i] == '/') mkdir(dir.substr(0, i).c_str(), 0755);
+    const std::string tmp = path + ".tmp" + std::to_string(getpid());
+    if (FILE* f = std::fopen(tmp.c_str(), "wb")) {
+      const uint32_t nl = uint32_t(name->size());
+      const bool ok = std::fwrite(&nl, 4, 1, f) == 1 && std::fwrite(name->data(), 1, nl, f) == nl &&
+                      std::fwrite(cubin->data(), 1, cubin->size(), f) == cubin->size();
+      std::fclose(f);
+      if (!ok || std::rename(tmp.c_str(), path.c_str()) != 0) std::remove(tmp.c_str());
+    }
+  }
+  return true;
 }
 
 struct JitKernel {
@@ -210,32 +316,10 @@ class JitFormat final : public Impl {
       *out = it->second;
       return cudaSuccess;
     }
-    const Nvrtc& nv = nvrtc();
-    if (!nv.ok) return cudaErrorNotSupported;
-    const std::string inc = "--include-path=" + csrc_dir();
-    const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", inc.c_str(),
-                          "-default-device", "-lineinfo"};
-    nvrtcProgram_t prog = nullptr;
-    if (nv.create(&prog, "#include \"bfp_kernels.cuh\"\n", "bfp_jit.cu", 0, nullptr, nullptr))
+    std::vector<char> cubin;
+    std::string name;
+    if (!nvrtc_compile("#include \"bfp_kernels.cuh\"\n", expr, true, &cubin, &name))
       return cudaErrorNotSupported;
-    nv.add_name(prog, expr.c_str());
-    if (nv.compile(prog, 5, opts) != 0) {
-      size_t ls = 0;
-      nv.log_size(prog, &ls);
-      std::string log(ls, '\0');
-      nv.log(prog, log.data());
-      std::fprintf(stderr, "[bfp jit] NVRTC failed for %s:\n%s\n", expr.c_str(), log.c_str());
-      nv.destroy(&prog);
-      return cudaErrorNotSupported;
-    }
-    const char* lowered = nullptr;
-    nv.lowered(prog, expr.c_str(), &lowered);
-    const std::string name = lowered ? lowered : "";
-    size_t n = 0;
-    nv.cubin_size(prog, &n);
-    std::vector<char> cubin(n);
-    nv.cubin(prog, cubin.data());
-    nv.destroy(&prog);
     cudaLibrary_t lib = nullptr;
     cudaError_t e = cudaLibraryLoadData(&lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
     if (e != cudaSuccess) return e;
@@ -383,32 +467,15 @@ cudaError_t chain_kernel(unsigned e, unsigned s, int rn, int ftz, const std::str
     *out = it->second;
     return cudaSuccess;
   }
-  const Nvrtc& nv = nvrtc();
-  if (!nv.ok) return cudaErrorNotSupported;
+  if (!nvrtc().ok) return cudaErrorNotSupported;
   // the format's LOP3-mapped covers when it has them (csrc/gen), else templates
   const std::string gen = csrc_dir() + "/gen/gen_" + std::to_string(e) + "_" + std::to_string(s) + ".cuh";
   FILE* fg = std::getenv("BFP_CHAIN_NOGEN") ? nullptr : std::fopen(gen.c_str(), "r");
   if (fg) std::fclose(fg);
   const std::string src = chain_source(e, s, rn, ftz, prog, fg != nullptr, f32);
-  const std::string inc = "--include-path=" + csrc_dir();
-  const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", inc.c_str(), "-default-device",
-                        "-lineinfo"};
-  nvrtcProgram_t p = nullptr;
-  if (nv.create(&p, src.c_str(), "bfp_chain.cu", 0, nullptr, nullptr)) return cudaErrorNotSupported;
-  if (nv.compile(p, 5, opts) != 0) {
-    size_t ls = 0;
-    nv.log_size(p, &ls);
-    std::string log(ls, '\0');
-    nv.log(p, log.data());
-    std::fprintf(stderr, "[bfp jit] NVRTC failed for chain %s:\n%s\n", k.c_str(), log.c_str());
-    nv.destroy(&p);
-    return cudaErrorNotSupported;
-  }
-  size_t n = 0;
-  nv.cubin_size(p, &n);
-  std::vector<char> cubin(n);
-  nv.cubin(p, cubin.data());
-  nv.destroy(&p);
+  std::vector<char> cubin;
+  std::string name;
+  if (!nvrtc_compile(src, "bfp_chain_k", false, &cubin, &name)) return cudaErrorNotSupported;
   cudaLibrary_t lib = nullptr;
   cudaError_t err = cudaLibraryLoadData(&lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
   if (err != cudaSuccess) return err;

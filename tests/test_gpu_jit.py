@@ -142,3 +142,28 @@ def test_pack_unpack_f64(oracle, fmt2, mode):
     nan = np.isnan(ref)
     assert np.array_equal(back.view(np.uint64)[~nan], ref.view(np.uint64)[~nan])
     assert np.all(back.view(np.uint64)[nan] == np.uint64(0x7FF8000000000000))
+
+
+def test_jit_disk_cache(tmp_path):
+    """NVRTC kernels are cached as CUBIN files: a second process loads them
+    instead of compiling, with the same results."""
+    import os
+    import subprocess
+    import sys
+    from conftest import ROOT
+    code = ("import torch, numpy as np, paper_1602_04716_b200 as bfp\n"
+            "spec = bfp.make_spec(7, 20)\n"
+            "v = [bfp.pack(torch.arange(5000, dtype=torch.int64, device='cuda') * k + 12345, spec) for k in (3, 7)]\n"
+            "z = bfp.chain('ab*ab+-', *v)\n"
+            "print(int(z.planes.to(torch.int64).sum()))\n")
+    env = dict(os.environ, BFP_JIT_CACHE=str(tmp_path), PYTHONPATH=str(ROOT))
+    out = [subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+           for _ in range(2)]
+    assert all(o.returncode == 0 for o in out), out[0].stderr + out[1].stderr
+    assert out[0].stdout == out[1].stdout
+    files = list(tmp_path.glob("*.cubin"))
+    assert len(files) >= 2  # the pack kernel and the chain program
+    mtimes = {f: f.stat().st_mtime_ns for f in files}
+    out3 = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+    assert out3.returncode == 0 and out3.stdout == out[0].stdout
+    assert {f: f.stat().st_mtime_ns for f in tmp_path.glob("*.cubin")} == mtimes  # loaded, not rewritten
