@@ -50,13 +50,16 @@ def test_all_pairs_16bit(oracle, op, fmt):
 
     t0 = time.time()
     bad = 0
-    workers = max(1, (os.cpu_count() or 2) - 1)
+    # bounded: <= 16 oracle threads (~256 MB of operands each while running)
+    # and a window of workers + 2 chunks of results in flight
+    workers = max(1, min(16, (os.cpu_count() or 2) - 1))
+    win = workers + 2
     starts = list(range(0, 1 << 16, XB))
     with ThreadPoolExecutor(max_workers=workers) as ex:
-        futs = {x0: ex.submit(want, x0) for x0 in starts[:2 * workers]}  # bounded window
+        futs = {x0: ex.submit(want, x0) for x0 in starts[:win]}
         for k, x0 in enumerate(starts):
-            if k + 2 * workers < len(starts):
-                futs[starts[k + 2 * workers]] = ex.submit(want, starts[k + 2 * workers])
+            if k + win < len(starts):
+                futs[starts[k + win]] = ex.submit(want, starts[k + win])
             fut = futs.pop(x0)
             xd = torch.arange(x0, x0 + XB, dtype=torch.int64, device="cuda").repeat_interleave(1 << 16)
             got = bfp.unpack(fn(bfp.pack(xd, spec), vy)).cpu().numpy().view(np.uint16)
