@@ -211,10 +211,12 @@ def _arith_job(label, op, spec, n, sets, device):
     outs = [bfp.empty(spec, n, device) for _ in range(2)]  # rotating outputs
 
     def launch(i, st):
+        # resident operands that nothing in the step writes: BFP_INPUTS_READY
+        # lets each kernel's first loads overlap its predecessor's tail
         a, b, c = sets[i % len(sets)]
-        rc = L.bfp_arith(OPNAMES[op], spec.c, a.planes.data_ptr(), b.planes.data_ptr(),
-                         c.planes.data_ptr() if c is not None else None,
-                         outs[i & 1].planes.data_ptr(), n, st)
+        rc = L.bfp_arith_ex(OPNAMES[op], spec.c, a.planes.data_ptr(), b.planes.data_ptr(),
+                            c.planes.data_ptr() if c is not None else None,
+                            outs[i & 1].planes.data_ptr(), n, st, 1)
         if rc != 0:
             raise RuntimeError(L.bfp_last_error())
 

@@ -126,6 +126,18 @@ bfp_status bfp_mul_add(const bfp_format* f, const uint32_t* d_a, const uint32_t*
 /* op: 0 add, 1 sub, 2 mul, 3 div, 4 mul_add (d_c only for 4). */
 bfp_status bfp_arith(int op, const bfp_format* f, const uint32_t* d_x, const uint32_t* d_y,
                      const uint32_t* d_c, uint32_t* d_z, size_t count, void* stream);
+/* bfp_arith with flags.  BFP_INPUTS_READY: the caller guarantees that no work
+ * still running on `stream` writes d_x / d_y / d_c (they are resident, or
+ * produced by work that has completed).  The kernel then issues its first
+ * loads before waiting for the previous kernel on the stream (programmatic
+ * dependent launch) and waits before its first store, so short kernels
+ * overlap their load ramp with the predecessor's tail.  Results are
+ * identical; only a violated guarantee (inputs written by the immediately
+ * preceding kernel) could observe stale data. */
+#define BFP_INPUTS_READY 1u
+bfp_status bfp_arith_ex(int op, const bfp_format* f, const uint32_t* d_x, const uint32_t* d_y,
+                        const uint32_t* d_c, uint32_t* d_z, size_t count, void* stream,
+                        unsigned flags);
 
 /* Fused float32-in / float32-out: z = (float)decode(op(encode(x), encode(y)
  * [, encode(c)])) in one kernel -- the same result as pack_f32 / op /

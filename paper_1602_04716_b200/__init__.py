@@ -10,6 +10,7 @@ from .bfp import (  # noqa: F401
     OP_MUL,
     OP_MUL_ADD,
     OP_SUB,
+    arith,
     arith_f32,
     bfp_add,
     bfp_div,

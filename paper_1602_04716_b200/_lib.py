@@ -13,6 +13,7 @@ LIB_PATH = Path(__file__).resolve().parent / "libbfpgpu.so"
 
 # bfp_status
 BFP_OK, BFP_EFORMAT, BFP_EMISMATCH, BFP_ESIZE, BFP_EUNSUPPORTED, BFP_ECUDA, BFP_EARG = range(7)
+BFP_INPUTS_READY = 1  # bfp_arith_ex flag (include/bfpgpu.h)
 
 
 class BfpFormat(C.Structure):
@@ -55,6 +56,8 @@ SIGNATURES = {
                               C.c_void_p]),
     "bfp_arith": (C.c_int, [C.c_int, _F, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                             C.c_size_t, C.c_void_p]),
+    "bfp_arith_ex": (C.c_int, [C.c_int, _F, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t,
+                               C.c_void_p, C.c_uint]),
     "bfp_arith_f32": (C.c_int, [C.c_int, _F, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                 C.c_size_t, C.c_void_p]),
     "bfp_chain": (C.c_int, [_F, C.c_char_p, C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),

@@ -302,17 +302,27 @@ def unpack_f64(v: bfp_vector, count: int | None = None) -> torch.Tensor:
 
 
 def _binop(op: int, x: bfp_vector, y: bfp_vector, c: bfp_vector | None = None,
-           out: bfp_vector | None = None) -> bfp_vector:
+           out: bfp_vector | None = None, inputs_ready: bool = False) -> bfp_vector:
     require_same_shape(x.spec, y.spec)
     if c is not None:
         require_same_shape(x.spec, c.spec)
     if x.count != y.count or (c is not None and c.count != x.count):
         raise ValueError("operands must have the same element count")
     z = out if out is not None else empty(x.spec, x.count, x.planes.device)
-    check(lib().bfp_arith(op, x.spec.c, x.planes.data_ptr(), y.planes.data_ptr(),
-                          c.planes.data_ptr() if c is not None else None, z.planes.data_ptr(),
-                          x.count, _stream()), ("add", "sub", "mul", "div", "mul_add")[op])
+    check(lib().bfp_arith_ex(op, x.spec.c, x.planes.data_ptr(), y.planes.data_ptr(),
+                             c.planes.data_ptr() if c is not None else None, z.planes.data_ptr(),
+                             x.count, _stream(), 1 if inputs_ready else 0),
+          ("add", "sub", "mul", "div", "mul_add")[op])
     return z
+
+
+def arith(op: int, x: bfp_vector, y: bfp_vector, c: bfp_vector | None = None,
+          out: bfp_vector | None = None, inputs_ready: bool = False) -> bfp_vector:
+    """bfp_arith_ex: op 0 add, 1 sub, 2 mul, 3 div, 4 mul_add.  inputs_ready
+    (BFP_INPUTS_READY) asserts that no work still running on the stream
+    writes x / y / c, letting the kernel's first loads overlap the previous
+    kernel's tail."""
+    return _binop(op, x, y, c, out, inputs_ready)
 
 
 def bfp_add(x: bfp_vector, y: bfp_vector, out: bfp_vector | None = None) -> bfp_vector:

@@ -161,18 +161,24 @@ size_t bfp_enc_bytes(const bfp_format* f) {
   return n <= 8 ? 1 : (n <= 16 ? 2 : (n <= 32 ? 4 : 8));
 }
 
-bfp_status bfp_arith(int op, const bfp_format* f, const uint32_t* d_x, const uint32_t* d_y,
-                     const uint32_t* d_c, uint32_t* d_z, size_t count, void* stream) {
+bfp_status bfp_arith_ex(int op, const bfp_format* f, const uint32_t* d_x, const uint32_t* d_y,
+                        const uint32_t* d_c, uint32_t* d_z, size_t count, void* stream, unsigned flags) {
   const Impl* impl = nullptr;
   const bfp_status s = resolve(f, &impl);
   if (s != BFP_OK) return s;
   if (op < 0 || op > 4) return fail(BFP_EARG, "bad op");
+  if (flags & ~unsigned(BFP_INPUTS_READY)) return fail(BFP_EARG, "unknown flags");
   if (count == 0) return BFP_OK;
   if (!d_x || !d_y || !d_z || (op == 4 && !d_c)) return fail(BFP_EARG, "null operand");
   ++g_launches;
   return cuda_status(impl->arith(op, d_x, d_y, d_c, d_z, nblocks(count),
-                                 static_cast<cudaStream_t>(stream)),
+                                 static_cast<cudaStream_t>(stream), flags),
                      "arith launch");
+}
+
+bfp_status bfp_arith(int op, const bfp_format* f, const uint32_t* d_x, const uint32_t* d_y,
+                     const uint32_t* d_c, uint32_t* d_z, size_t count, void* stream) {
+  return bfp_arith_ex(op, f, d_x, d_y, d_c, d_z, count, stream, 0);
 }
 
 namespace {

@@ -201,11 +201,11 @@ class JitFormat final : public Impl {
   bool compiled() const override { return false; }
 
   cudaError_t arith(int op, const w32* x, const w32* y, const w32* c, w32* z, size_t nblocks,
-                    cudaStream_t st) const override {
+                    cudaStream_t st, unsigned flags) const override {
     if (op < 0 || op > 4) return cudaErrorInvalidValue;
     const size_t units = nblocks * 32;
     if (!units) return cudaSuccess;
-    return run(fmt_expr("bfpg::k_arith<%s, %d>", op), units, st, {&x, &y, &c, &z, &units});
+    return run(fmt_expr("bfpg::k_arith<%s, %d>", op), units, st, {&x, &y, &c, &z, &units, &flags});
   }
   cudaError_t pack_enc(const void* enc, w32* planes, size_t n, cudaStream_t st) const override {
     const int eb = enc_bytes();

@@ -136,8 +136,14 @@ template <class F, int OP>
 __global__ void __launch_bounds__(kThreads, arith_minb<F, OP>()) k_arith(const w32* __restrict__ x,
                                                     const w32* __restrict__ y,
                                                     const w32* __restrict__ c,
-                                                    w32* __restrict__ z, size_t units) {
-  pdl_enter();
+                                                    w32* __restrict__ z, size_t units,
+                                                    unsigned flags) {
+  // BFP_INPUTS_READY (flags bit 0): the caller guarantees that no work still
+  // running on the stream writes x / y / c, so each thread issues its first
+  // unit's loads before griddepcontrol.wait -- they overlap the previous
+  // kernel's tail -- and waits before its first store (no WAR / WAW hazard).
+  bool waited = !(flags & 1u);
+  if (waited) pdl_enter();
   constexpr int N = F::N;
   constexpr int NIN = OP == OP_MUL_ADD ? 3 : 2;
   const size_t stride = size_t(gridDim.x) * kThreads;
@@ -145,6 +151,10 @@ __global__ void __launch_bounds__(kThreads, arith_minb<F, OP>()) k_arith(const w
     const size_t base = (u >> 5) * (size_t(N) * 32) + (u & 31);
     Operands<N, NIN> cur;
     cur.load(x, y, c, base);
+    if (!waited) {
+      asm volatile("griddepcontrol.wait;" ::: "memory");
+      waited = true;
+    }
     // register-capped networks: releasing before the network keeps the
     // loop-carried values out of local memory (ptxas spilled 20-24 B of the
     // 1/5/10 and 1/6/9 mul loops with the release after the stores)
@@ -757,7 +767,7 @@ inline int grid_for(int wave, size_t units) {
 struct Impl {
   virtual ~Impl() = default;
   virtual cudaError_t arith(int op, const w32* x, const w32* y, const w32* c, w32* z,
-                            size_t nblocks, cudaStream_t st) const = 0;
+                            size_t nblocks, cudaStream_t st, unsigned flags = 0) const = 0;
   virtual cudaError_t pack_enc(const void* enc, w32* planes, size_t n, cudaStream_t st) const = 0;
   virtual cudaError_t unpack_enc(const w32* planes, void* enc, size_t n, cudaStream_t st) const = 0;
   virtual cudaError_t pack_f32(const float* in, w32* planes, size_t n, cudaStream_t st) const = 0;
@@ -784,7 +794,7 @@ struct FormatImpl {
 
   template <int OP>
   static cudaError_t launch_arith(const w32* x, const w32* y, const w32* c, w32* z, size_t units,
-                                  cudaStream_t st) {
+                                  cudaStream_t st, unsigned flags) {
     const int bulk = bulk_mode();  // 0 off, 1 auto (prefer_bulk), 2 force
     if (bulk == 2 || (bulk == 1 && prefer_bulk<F, OP>())) {
       auto kb = k_arith_bulk<F, OP>;
@@ -800,18 +810,18 @@ struct FormatImpl {
     }
     auto k = k_arith<F, OP>;
     static const int wave = wave_ctas(k);
-    return launch(k, grid_for(wave, units), st, x, y, c, z, units);
+    return launch(k, grid_for(wave, units), st, x, y, c, z, units, flags);
   }
   static cudaError_t arith(int op, const w32* x, const w32* y, const w32* c, w32* z,
-                           size_t nblocks, cudaStream_t st) {
+                           size_t nblocks, cudaStream_t st, unsigned flags) {
     const size_t units = nblocks * 32;
     if (!units) return cudaSuccess;
     switch (op) {
-      case OP_ADD: return launch_arith<OP_ADD>(x, y, c, z, units, st);
-      case OP_SUB: return launch_arith<OP_SUB>(x, y, c, z, units, st);
-      case OP_MUL: return launch_arith<OP_MUL>(x, y, c, z, units, st);
-      case OP_DIV: return launch_arith<OP_DIV>(x, y, c, z, units, st);
-      case OP_MUL_ADD: return launch_arith<OP_MUL_ADD>(x, y, c, z, units, st);
+      case OP_ADD: return launch_arith<OP_ADD>(x, y, c, z, units, st, flags);
+      case OP_SUB: return launch_arith<OP_SUB>(x, y, c, z, units, st, flags);
+      case OP_MUL: return launch_arith<OP_MUL>(x, y, c, z, units, st, flags);
+      case OP_DIV: return launch_arith<OP_DIV>(x, y, c, z, units, st, flags);
+      case OP_MUL_ADD: return launch_arith<OP_MUL_ADD>(x, y, c, z, units, st, flags);
       default: return cudaErrorInvalidValue;
     }
   }
@@ -945,8 +955,8 @@ struct FormatImpl {
   }
   struct Backend final : Impl {
     cudaError_t arith(int op, const w32* x, const w32* y, const w32* c, w32* z, size_t nb,
-                      cudaStream_t st) const override {
-      return FormatImpl::arith(op, x, y, c, z, nb, st);
+                      cudaStream_t st, unsigned flags) const override {
+      return FormatImpl::arith(op, x, y, c, z, nb, st, flags);
     }
     cudaError_t pack_enc(const void* e, w32* p, size_t n, cudaStream_t st) const override {
       return FormatImpl::pack_enc(e, p, n, st);

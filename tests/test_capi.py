@@ -150,3 +150,11 @@ def test_chain_f32_validation(L):
     assert L.bfp_chain_f32(C.byref(wide), b"ab+", 2, ptrs, None, 1024, None) == _lib.BFP_EUNSUPPORTED
     f = _lib.BfpFormat(5, 10, 1, 0, b"")
     assert L.bfp_chain_f32(C.byref(f), b"ab", 2, ptrs, None, 1024, None) == _lib.BFP_EARG
+
+
+def test_arith_ex_flags_validated(L):
+    import ctypes as C
+    from paper_1602_04716_b200 import _lib
+    f = _lib.BfpFormat(4, 3, 1, 0, b"")
+    assert L.bfp_arith_ex(0, C.byref(f), None, None, None, None, 0, None, 2) == _lib.BFP_EARG
+    assert L.bfp_arith_ex(0, C.byref(f), None, None, None, None, 0, None, _lib.BFP_INPUTS_READY) == _lib.BFP_OK

@@ -573,3 +573,26 @@ def test_pack_f32_hw_path_underflow_boundary(oracle, fmt2, mode):
     want = oracle.encode_f32(fmt, xs)
     got = bfp.to_u64(bfp.unpack(v), spec).cpu().numpy().astype(np.uint64)
     assert np.array_equal(got, want), int((got != want).sum())
+
+
+@pytest.mark.parametrize("fmt2", [(4, 3), (5, 10), (6, 9)])
+def test_inputs_ready_flag_back_to_back(oracle, fmt2):
+    """BFP_INPUTS_READY (loads before the PDL wait): back-to-back launches on
+    one stream over resident operands give the same bits as the oracle."""
+    e, s = fmt2
+    nb = 1 + e + s
+    fmt = fmt2 + (1, 0)
+    spec = bfp.make_spec(e, s)
+    rng = np.random.default_rng(31 + nb)
+    n = (1 << 20) + 333
+    xs = [operands(e, s, n, rng) for _ in range(3)]
+    vs = [bfp.pack(torch.from_numpy(x.astype(np.int64)).cuda(), spec) for x in xs]
+    outs = [bfp.empty(spec, n) for _ in range(6)]
+    ops = [(0, "add"), (2, "mul"), (4, "mul_add"), (1, "sub"), (2, "mul"), (0, "add")]
+    for k, (code, _) in enumerate(ops):  # no sync in between: PDL chains the kernels
+        bfp.arith(code, vs[k % 3], vs[(k + 1) % 3], vs[(k + 2) % 3], out=outs[k], inputs_ready=True)
+    torch.cuda.synchronize()
+    for k, (code, name) in enumerate(ops):
+        got = bfp.to_u64(bfp.unpack(outs[k]), spec).cpu().numpy().astype(np.uint64)
+        want = oracle.binop(name, fmt, xs[k % 3], xs[(k + 1) % 3], xs[(k + 2) % 3])
+        assert np.array_equal(got, want), name
