@@ -19,6 +19,9 @@
  *   unpack + decode_scalar format.hpp:101-123           bfp_unpack_f32
  *   bfpraw_stride / to_bfpraw / from_bfpraw             bfp_bfpraw_stride, bfp_pack_bfpraw,
  *     pack.hpp:78-109                                     bfp_unpack_bfpraw
+ *   encode_scalar(double) / decode_scalar -> double     bfp_pack_f64 / bfp_unpack_f64
+ *   chains of bfp_add / sub / mul / div calls           bfp_chain (planes), bfp_chain_f32
+ *                                                         (float32), one kernel per program
  *
  * Storage ("planes"): the memory image of an array of bitfield<lane<1024>>
  * (bitfield.hpp:10-28): element i, plane j (0 = fraction LSB, n-1 = sign) is
