@@ -2,9 +2,9 @@
 the C ABI, against the oracle (the C restatement, itself pinned to the
 reference in tests/test_oracle.py).
 
-About 20 s per case on a 16-core GPU host.  The RN + gradual cases run by
-default (BFP_EXHAUSTIVE16=0 skips them); BFP_EXHAUSTIVE16=all adds the other
-rounding / subnormal modes.  Log of a run: profiles/r01_exhaustive16.log.
+About 16 s per case on a 16-core GPU host.  Five RN + gradual cases run by
+default (BFP_EXHAUSTIVE16=0 skips them); BFP_EXHAUSTIVE16=all runs every
+16-bit format x add/sub/mul/div x rounding x subnormal mode (48 cases).  Log of a run: profiles/r01_exhaustive16.log.
 The device side generates the pairs in place (x = block of 256 values, y =
 all 65536) and compares the result planes' encodings against oracle chunks
 computed on a thread pool (ctypes releases the GIL).
@@ -27,9 +27,9 @@ pytestmark = [pytest.mark.gpu, pytest.mark.slow,
 
 CASES = [("mul", (5, 10, 1, 0)), ("add", (5, 10, 1, 0)), ("mul", (6, 9, 1, 0)),
          ("mul", (8, 7, 1, 0)), ("div", (5, 10, 1, 0))]
-if MODE == "all":
-    CASES += [(op, (5, 10, rn, ftz)) for op in ("mul", "add") for (rn, ftz) in ((0, 0), (1, 1), (0, 1))]
-    CASES += [("mul", (8, 7, 0, 1)), ("sub", (6, 9, 1, 0))]
+if MODE == "all":  # every 16-bit format x add/sub/mul/div x RN/RZ x gradual/FTZ (48 cases)
+    CASES = [(op, (e, s, rn, ftz)) for (e, s) in ((5, 10), (6, 9), (8, 7)) for op in ("add", "sub", "mul", "div")
+             for (rn, ftz) in ((1, 0), (0, 0), (1, 1), (0, 1))]
 XB = 256  # x values per chunk -> 2^24 pairs
 
 
