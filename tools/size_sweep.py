@@ -28,8 +28,8 @@ def main() -> None:
     e, s = map(int, a.fmt.split(","))
     spec = bfp.make_spec(e, s)
     op = {"add": 0, "sub": 1, "mul": 2, "div": 3}[a.op]
-    peak = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()).get("hbm_copy_gbs", 6459.6) \
-        if (ROOT / "MEASURED_PEAKS.json").exists() else 6459.6
+    peak = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()).get("hbm_gbs", 6551.4) \
+        if (ROOT / "MEASURED_PEAKS.json").exists() else 6551.4
     l2 = 126 << 20
     rows = []
     for lg in range(14, 29, 2):
