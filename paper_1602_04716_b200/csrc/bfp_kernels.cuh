@@ -273,8 +273,8 @@ __global__ void __launch_bounds__(kThreads) k_arith_bulk(const w32* __restrict__
     eval_unit<F, OP>(ops[0], ops[1], ops[NIN - 1], Z);
     w32* zb = z + b * size_t(TW) + lane;
     BFP_UNROLL for (int j = 0; j < N; ++j) st_stream(zb + j * 32, Z[j]);
+    pdl_release_if(b + tw >= nblocks);  // in-loop: see pdl_release_if (no per-access R2UR)
   }
-  pdl_release();
 }
 
 // Logic-bound networks (LOP3 per byte of HBM traffic above the B200's
