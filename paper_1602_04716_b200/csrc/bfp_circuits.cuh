@@ -415,17 +415,17 @@ BFP_HD void add_w(const w32* X, const w32* Y, w32* Z) {
 
 // ====================================================== shared final stage
 // Rounds and packs a significand field R = [jam, guard, sig(S+1)] whose
-// biased exponent minus one is ez (EW = E+2 bit two's complement):
+// biased exponent minus one is ez (EW-bit two's complement, EW >= E+2):
 //   ez >= 0: normal, exponent field ez + hidden (+ rounding carry);
 //   ez <  0: subnormal range, R shifts right by -ez first (jam collects);
 // then overflow (Inf under RN, max-finite under RZ), FTZ after rounding
 // (still below the smallest normal) and the special-value overrides:
 // zero_res / inf_res force a signed zero / Inf, use_nan the canonical NaN.
-template <class F>
+template <class F, int EW>
 BFP_HD void finish_round(w32* R, const w32* ez, w32 sign, w32 zero_res, w32 inf_res, w32 use_nan,
                          w32* Z) {
   constexpr int E = F::E, S = F::S, M = E + S;
-  constexpr int EW = E + 2;
+  static_assert(EW >= E + 2, "finish_round: working exponent narrower than E + 2");
   constexpr int WR = S + 3;
   const w32 sub = ez[EW - 1];
   {
@@ -458,7 +458,10 @@ BFP_HD void finish_round(w32* R, const w32* ez, w32 sign, w32 zero_res, w32 inf_
   pack_round<E + 1, S, E + 1>(em, sig, rnd, fr, ex);
   w32 eall = ONES;
   BFP_UNROLL for (int i = 0; i < E; ++i) eall &= ex[i];
-  const w32 ovf = ex[E] | ex[E + 1] | eall;
+  // ez bits above E (only when EW > E + 2): a positive ez >= 2^(E+1) overflows
+  w32 high = 0;
+  BFP_UNROLL for (int i = E + 1; i < EW - 1; ++i) high |= ez[i];
+  const w32 ovf = ex[E] | ex[E + 1] | eall | (high & ~sub);
 
   w32 flush = 0;
   if constexpr (F::FTZ) flush = sub & ~ex[0];  // still below the smallest normal
@@ -484,6 +487,31 @@ BFP_HD void finish_round(w32* R, const w32* ez, w32 sign, w32 zero_res, w32 inf_
     Z[S + j] = (ex[j] & quiet) | hset;
   }
   Z[M] = sign & ~use_nan;
+}
+
+// Signed working-exponent widths.  E + 2 bits hold every intermediate of the
+// named formats; a format with a wide significand and a narrow exponent range
+// (e.g. 1/3/11, 1/2/5: normalisation counts up to S or 2S+1 against a bias of
+// 3 or 1) needs more, so the width is the larger of E + 2 and the bits of the
+// exact range of the exponent expression (plus one of margin).
+constexpr int signed_bits(long lo, long hi) {
+  int w = 2;
+  while (lo < -(1L << (w - 1)) || hi >= (1L << (w - 1))) ++w;
+  return w;
+}
+// mul: ez = ex_eff + ey_eff - bias - lz - borrow, finite ex_eff in [1, 2^E - 2],
+// lz <= S (one normalised operand) or 2S + 1 (full product normaliser).
+template <class F>
+constexpr int mul_ew() {
+  constexpr long bias = F::BIAS;
+  constexpr long lzmax = ((1 - F::BIAS) <= -F::S - 1) ? F::S : 2L * F::S + 1;
+  return imax(F::E + 2, signed_bits(-bias - lzmax - 2, 2 * ((1L << F::E) - 2) - bias + 1));
+}
+// div: ez = (ex_eff - lzx) - (ey_eff - lzy) - scale + bias - 1, lz <= S.
+template <class F>
+constexpr int div_ew() {
+  constexpr long bias = F::BIAS, top = (1L << F::E) - 2;
+  return imax(F::E + 2, signed_bits(1 - top - F::S - 1 + bias - 1 - 1, top - 1 + F::S + bias - 1 + 1));
 }
 
 // Operand classes shared by mul / div.
@@ -690,7 +718,7 @@ BFP_HD void sig_product_best(const w32* a, const w32* b, w32* P) {
 template <class F>
 BFP_HD void mul_w(const w32* X, const w32* Y, w32* Z) {
   constexpr int E = F::E, S = F::S, M = E + S;
-  constexpr int EW = E + 2;  // signed working exponent
+  constexpr int EW = mul_ew<F>();  // signed working exponent
   constexpr bool BOTH_SUB_ZERO = (1 - F::BIAS) <= -S - 1;
   const w32 sign = X[M] ^ Y[M];
   const Classes cx = classify<F>(X), cy = classify<F>(Y);
@@ -772,7 +800,7 @@ BFP_HD void mul_w(const w32* X, const w32* Y, w32* Z) {
   if constexpr (BOTH_SUB_ZERO) zero_src |= ~cx.h & ~cy.h;  // underflows to a signed zero
   const w32 zero_res = zero_src & ~use_nan;
   const w32 inf_res = (cx.inf | cy.inf) & ~use_nan;
-  finish_round<F>(R, ez, sign, zero_res, inf_res, use_nan, Z);
+  finish_round<F, EW>(R, ez, sign, zero_res, inf_res, use_nan, Z);
 }
 
 // ================================================================= DIV
@@ -784,7 +812,7 @@ BFP_HD void mul_w(const w32* X, const w32* Y, w32* Z) {
 template <class F>
 BFP_HD void div_w(const w32* X, const w32* Y, w32* Z) {
   constexpr int E = F::E, S = F::S, M = E + S;
-  constexpr int EW = E + 2;
+  constexpr int EW = div_ew<F>();
   constexpr int W1 = S + 1;
   const w32 sign = X[M] ^ Y[M];
   const Classes cx = classify<F>(X), cy = classify<F>(Y);
@@ -878,7 +906,7 @@ BFP_HD void div_w(const w32* X, const w32* Y, w32* Z) {
   const w32 use_nan = cx.nan | cy.nan | (cx.z & cy.z) | (cx.inf & cy.inf);
   const w32 zero_res = (cx.z | cy.inf) & ~use_nan;
   const w32 inf_res = (cx.inf | cy.z) & ~use_nan;
-  finish_round<F>(Rf, ez, sign, zero_res, inf_res, use_nan, Z);
+  finish_round<F, EW>(Rf, ez, sign, zero_res, inf_res, use_nan, Z);
 }
 
 // z = round(round(a * b) + c) -- the reference chain bfp_add(bfp_mul(a,b),c),

@@ -196,3 +196,18 @@ def test_significand_products_exact(host, s):
             assert L.host_product(s, which, a.ctypes.data, b.ctypes.data, p.ctypes.data) == 0
             got = [sum(((int(p[j]) >> k) & 1) << j for j in range(2 * s + 2)) for k in range(32)]
             assert got == want, (s, which, trial)
+
+
+def test_template_format_sweep(tmp_path, oracle):
+    """The template networks (what the NVRTC backend compiles) over ~60
+    formats incl. 1/2/5, 1/3/11, 1/2/24 (working exponent wider than E + 2)
+    and both RN + gradual and RZ + FTZ, against the oracle."""
+    import subprocess
+    from conftest import ROOT
+    exe = tmp_path / "format_sweep"
+    subprocess.run(["g++", "-O1", "-std=c++17", str(ROOT / "tests" / "native" / "format_sweep.cpp"),
+                    f"-L{ROOT / 'oracle'}", "-loracle", f"-Wl,-rpath,{ROOT / 'oracle'}", "-o", str(exe)],
+                   check=True)
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr
+    assert r.stdout.strip().endswith("total bad 0"), r.stdout

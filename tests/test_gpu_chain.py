@@ -91,3 +91,43 @@ def test_chain_f32_matches_planes_chain(fmt, prog):
     got = bfp.chain_f32(prog, spec, *xs)
     want = bfp.unpack_f32(bfp.chain(prog, *[bfp.pack_f32(x, spec) for x in xs]))
     assert torch.equal(got.view(torch.int32), want.view(torch.int32))
+
+
+def _random_program(rng, k: int, nops: int) -> str:
+    """A random well-formed postfix program over inputs a.. (k of them)."""
+    out, depth = [], 0
+    while nops > 0 or depth != 1:
+        if depth >= 2 and (nops > 0 and rng.random() < 0.45 or depth > nops + 1):
+            out.append("+-*/"[int(rng.integers(4))])
+            depth -= 1
+            nops -= 1
+        elif nops > 0 or depth < 1:
+            out.append(chr(97 + int(rng.integers(k))))
+            depth += 1
+        else:
+            out.append("+-*/"[int(rng.integers(4))])
+            depth -= 1
+    return "".join(out)
+
+
+@pytest.mark.slow
+@pytest.mark.skipif(not __import__("os").environ.get("BFP_FUZZ_CHAIN"), reason="set BFP_FUZZ_CHAIN=<count>")
+def test_chain_fuzz(oracle):
+    """Random programs x random legal formats (compiled and NVRTC-only) x modes
+    against the oracle's composition of single ops."""
+    import os
+    rng = np.random.default_rng(2024)
+    for t in range(int(os.environ["BFP_FUZZ_CHAIN"])):
+        e = int(rng.integers(2, 9))
+        s = int(rng.integers(1, 24))
+        rn, ftz = int(rng.integers(2)), int(rng.integers(2))
+        k = int(rng.integers(1, 6))
+        prog = _random_program(rng, k, int(rng.integers(1, 7)))
+        fmt = (e, s, rn, ftz)
+        spec = bfp.make_spec(e, s, rn, ftz)
+        n = int(rng.integers(1, 5000))
+        encs = [operands(e, s, n, rng) for _ in range(k)]
+        vs = [bfp.pack(torch.from_numpy(x.astype(np.int64)).cuda(), spec) for x in encs]
+        got = bfp.to_u64(bfp.unpack(bfp.chain(prog, *vs)), spec).cpu().numpy().astype(np.uint64)
+        want = _eval_oracle(oracle, prog, fmt, encs)
+        assert np.array_equal(got, want), (t, fmt, prog)

@@ -17,7 +17,7 @@ from paper_1602_04716_b200 import _lib
 
 pytestmark = pytest.mark.gpu
 
-JIT_FORMATS = [(2, 1), (6, 3), (7, 20), (11, 20), (10, 40)]
+JIT_FORMATS = [(2, 1), (6, 3), (7, 20), (11, 20), (10, 40), (2, 5), (3, 11), (2, 30)]  # last three: working exponent wider than E + 2
 OPS = {"add": 0, "sub": 1, "mul": 2, "div": 3, "mul_add": 4}
 
 
