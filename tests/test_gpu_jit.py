@@ -60,7 +60,7 @@ def test_jit_arith_vs_reference(ref_oracle, fmt2, mode):
         assert np.array_equal(got, want), (op, fmt)
 
 
-@pytest.mark.parametrize("fmt2", [(2, 1), (6, 3), (7, 16)])
+@pytest.mark.parametrize("fmt2", [(2, 1), (6, 3), (7, 16), (2, 5), (3, 11), (2, 20), (4, 22)])
 def test_jit_codec(oracle, fmt2):
     e, s = fmt2
     nb = 1 + e + s
@@ -118,7 +118,7 @@ def test_wide_layout_and_bfpraw(ref_oracle, fmt2):
     assert np.array_equal(bfp.unpack_bfpraw(vr).cpu().numpy(), raw)
 
 
-@pytest.mark.parametrize("fmt2", [(4, 3), (5, 10), (8, 23), (7, 30), (11, 52), (2, 1)])
+@pytest.mark.parametrize("fmt2", [(4, 3), (5, 10), (8, 23), (7, 30), (11, 52), (2, 1), (2, 5), (3, 11), (2, 40)])
 @pytest.mark.parametrize("mode", [(1, 0), (0, 1)])
 def test_pack_unpack_f64(oracle, fmt2, mode):
     """binary64 -> encode_scalar -> planes and planes -> decode_scalar (exact
