@@ -131,3 +131,9 @@ def test_chain_fuzz(oracle):
         got = bfp.to_u64(bfp.unpack(bfp.chain(prog, *vs)), spec).cpu().numpy().astype(np.uint64)
         want = _eval_oracle(oracle, prog, fmt, encs)
         assert np.array_equal(got, want), (t, fmt, prog)
+        if e <= 8 and s <= 23:  # the float32 form: == decode(chain(encode(x), ...))
+            scale = float(2.0 ** float(rng.integers(-8, 9)))
+            xs = [torch.from_numpy((rng.standard_normal(n) * scale).astype(np.float32)).cuda() for _ in range(k)]
+            zf = bfp.chain_f32(prog, spec, *xs)
+            zp = bfp.unpack_f32(bfp.chain(prog, *[bfp.pack_f32(x, spec) for x in xs]))
+            assert torch.equal(zf.view(torch.int32), zp.view(torch.int32)), (t, fmt, prog, "f32")
