@@ -596,3 +596,47 @@ def test_inputs_ready_flag_back_to_back(oracle, fmt2):
         got = bfp.to_u64(bfp.unpack(outs[k]), spec).cpu().numpy().astype(np.uint64)
         want = oracle.binop(name, fmt, xs[k % 3], xs[(k + 1) % 3], xs[(k + 2) % 3])
         assert np.array_equal(got, want), name
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_host_pipeline_random_shapes(oracle, seed):
+    """Host-buffer entry points over random counts, context chunk sizes, op
+    batches and pageable / pinned buffers == the device-buffer calls."""
+    L = _lib.lib()
+    rng = np.random.default_rng(1000 + seed)
+    (e, s) = [(4, 3), (5, 10), (6, 9), (3, 2)][seed % 4]
+    nb = 1 + e + s
+    fmt = (e, s, 1, 0)
+    spec = bfp.make_spec(e, s)
+    n = int(rng.integers(1, 3 << 20))
+    chunk = int(1 << int(rng.integers(19, 23)))
+    ops = [int(o) for o in rng.choice([0, 1, 2, 3], size=int(rng.integers(1, 4)), replace=False)]
+    pinned = bool(seed % 2)
+    x, y = operands(e, s, n, rng), operands(e, s, n, rng)
+    px, py = oracle.pack_planes(x, nb), oracle.pack_planes(y, nb)
+    ptrs = []
+    try:
+        if pinned:
+            (hx, _), (hy, _) = _pinned_like(L, px), _pinned_like(L, py)
+            outs = [_pinned_like(L, np.zeros_like(px)) for _ in ops]
+            ptrs += [hx, hy] + [o[0] for o in outs]
+            zp = [o[0] for o in outs]
+            views = [o[1] for o in outs]
+        else:
+            hx, hy = px.ctypes.data, py.ctypes.data
+            views = [np.zeros_like(px) for _ in ops]
+            zp = [v.ctypes.data for v in views]
+        ctx = L.bfp_host_ctx_create(chunk)
+        try:
+            arr = (C.c_int * len(ops))(*ops)
+            outp = (C.c_void_p * len(ops))(*zp)
+            assert L.bfp_arith_host_batch(ctx, len(ops), arr, C.byref(cfmt(fmt)), hx, hy, None, outp, n) == 0
+        finally:
+            L.bfp_host_ctx_destroy(ctx)
+        vx, vy = (bfp.pack(torch.from_numpy(v.astype(np.int64)).cuda(), spec) for v in (x, y))
+        for op, v in zip(ops, views):
+            want = bfp.arith(op, vx, vy).planes.cpu().numpy().view(np.uint32)
+            assert np.array_equal(np.asarray(v).view(np.uint32).reshape(-1), want.reshape(-1)), (op, n, chunk, pinned)
+    finally:
+        for p in ptrs:
+            L.bfp_host_free(p)
