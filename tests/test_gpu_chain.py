@@ -137,3 +137,8 @@ def test_chain_fuzz(oracle):
             zf = bfp.chain_f32(prog, spec, *xs)
             zp = bfp.unpack_f32(bfp.chain(prog, *[bfp.pack_f32(x, spec) for x in xs]))
             assert torch.equal(zf.view(torch.int32), zp.view(torch.int32)), (t, fmt, prog, "f32")
+            if k >= 2:  # the fused single-op float32 kernel (bfp_arith_f32) of the same format
+                op = int(rng.integers(4))
+                za = bfp.arith_f32(op, spec, xs[0], xs[1])
+                zr = bfp.unpack_f32(bfp.arith(op, bfp.pack_f32(xs[0], spec), bfp.pack_f32(xs[1], spec)))
+                assert torch.equal(za.view(torch.int32), zr.view(torch.int32)), (t, fmt, op, "arith_f32")
