@@ -167,3 +167,26 @@ def test_jit_disk_cache(tmp_path):
     out3 = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
     assert out3.returncode == 0 and out3.stdout == out[0].stdout
     assert {f: f.stat().st_mtime_ns for f in tmp_path.glob("*.cubin")} == mtimes  # loaded, not rewritten
+
+
+@pytest.mark.slow
+@pytest.mark.skipif(not __import__("os").environ.get("BFP_FUZZ_WIDE"), reason="set BFP_FUZZ_WIDE=<count>")
+def test_jit_wide_format_fuzz(ref_oracle):
+    """Random legal formats with wide significands (s in [20, 52], n <= 64),
+    random modes, every op, against the reference templates themselves."""
+    import os
+    O = ref_oracle
+    rng = np.random.default_rng(77)
+    for t in range(int(os.environ["BFP_FUZZ_WIDE"])):
+        e = int(rng.integers(2, 12))
+        s = int(rng.integers(20, min(52, 63 - e) + 1))
+        fmt = (e, s, int(rng.integers(2)), int(rng.integers(2)))
+        nb = 1 + e + s
+        n = 2048
+        x, y, c = (operands(e, s, n, rng) for _ in range(3))
+        y[: n // 8] = related(x[: n // 8], e, s, rng)
+        px, py, pc = (O.pack_planes(v, nb) for v in (x, y, c))
+        for op in OPS:
+            got = _arith(op, fmt, px, py, pc)
+            want = O.ref_binop_planes(op, fmt, px, py, pc if op == "mul_add" else None)
+            assert np.array_equal(got, want), (t, op, fmt)
