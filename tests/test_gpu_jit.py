@@ -190,3 +190,46 @@ def test_jit_wide_format_fuzz(ref_oracle):
             got = _arith(op, fmt, px, py, pc)
             want = O.ref_binop_planes(op, fmt, px, py, pc if op == "mul_add" else None)
             assert np.array_equal(got, want), (t, op, fmt)
+
+
+@pytest.mark.slow
+@pytest.mark.skipif(not __import__("os").environ.get("BFP_FUZZ_LAYOUT"), reason="set BFP_FUZZ_LAYOUT=<count>")
+def test_layout_fuzz(oracle):
+    """Random legal formats (n <= 64), counts and buffer offsets through the
+    layout paths: encodings -> planes (oracle pack_planes), planes ->
+    encodings, .bfpraw bytes round trip, binary64 codec (oracle encode_f64 /
+    decode_f64) and, where e <= 8 and s <= 23, the float32 codec."""
+    import os
+    rng = np.random.default_rng(99)
+    for t in range(int(os.environ["BFP_FUZZ_LAYOUT"])):
+        e = int(rng.integers(2, 12))
+        s = int(rng.integers(1, min(52, 63 - e) + 1))
+        mode = (int(rng.integers(2)), int(rng.integers(2)))
+        fmt = (e, s) + mode
+        nb = 1 + e + s
+        spec = bfp.make_spec(e, s, *mode)
+        n = int(rng.integers(1, 6000))
+        enc = operands(e, s, n, rng)
+        v = bfp.pack(torch.from_numpy(enc.astype(np.int64)).cuda(), spec)
+        assert np.array_equal(v.planes.cpu().numpy().view(np.uint32), oracle.pack_planes(enc, nb)), (t, fmt)
+        assert np.array_equal(bfp.to_u64(bfp.unpack(v), spec).cpu().numpy().astype(np.uint64), enc), (t, fmt)
+        stride = bfp.bfpraw_stride(spec)
+        off = int(rng.integers(0, 16))  # unaligned byte view
+        raw_buf = torch.zeros(n * stride + 16, dtype=torch.uint8, device="cuda")
+        raw = raw_buf[off: off + n * stride]
+        raw.copy_(bfp.unpack_bfpraw(v))
+        assert torch.equal(bfp.pack_bfpraw(raw, spec).planes, v.planes), (t, fmt, "bfpraw")
+        xs = (rng.standard_normal(n) * float(2.0 ** float(rng.integers(-40, 41)))).astype(np.float64)
+        xs[: n // 10] = rng.choice([0.0, -0.0, np.inf, -np.inf, np.nan, 1e-300, -5e-324], size=n // 10)
+        v64 = bfp.pack_f64(torch.from_numpy(xs).cuda(), spec)
+        want = oracle.encode_f64(fmt, xs)
+        assert np.array_equal(bfp.to_u64(bfp.unpack(v64), spec).cpu().numpy().astype(np.uint64), want), (t, fmt, "f64")
+        back = bfp.unpack_f64(v64).cpu().numpy().view(np.uint64)
+        assert np.array_equal(back, oracle.decode_f64(fmt, want).view(np.uint64)), (t, fmt, "f64 back")
+        if e <= 8 and s <= 23:
+            xf = xs.astype(np.float32)
+            vf = bfp.pack_f32(torch.from_numpy(xf).cuda(), spec)
+            wf = oracle.encode_f32(fmt, xf)
+            assert np.array_equal(bfp.to_u64(bfp.unpack(vf), spec).cpu().numpy().astype(np.uint64), wf), (t, fmt, "f32")
+            bf = bfp.unpack_f32(vf).cpu().numpy().view(np.uint32)
+            assert np.array_equal(bf, oracle.decode_f32(fmt, wf).view(np.uint32)), (t, fmt, "f32 back")
