@@ -92,8 +92,15 @@ const Impl* lookup_compiled(const bfp_format* f) {
 
 // Compiled network when the format is instantiated, else the NVRTC
 // runtime-format backend (same templates, compiled on first use).
+// BFP_FORCE_JIT=1 routes compiled formats through the runtime backend too
+// (measurement / testing of the template path).
 const Impl* lookup(const bfp_format* f) {
-  if (const Impl* c = lookup_compiled(f)) return c;
+  static const bool force_jit = [] {
+    const char* v = std::getenv("BFP_FORCE_JIT");
+    return v && v[0] == '1';
+  }();
+  if (!force_jit)
+    if (const Impl* c = lookup_compiled(f)) return c;
   return bfpg::jit_impl(f->exp_bits, f->sig_bits, f->rounding == 1, f->subnormals == 1);
 }
 
