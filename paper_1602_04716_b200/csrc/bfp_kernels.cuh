@@ -108,15 +108,15 @@ __device__ __forceinline__ void eval_unit(const w32* X, const w32* Y, const w32*
 // (mul / div of 300-800 LOP3 per word: 1/5/7, 1/5/10, 1/6/9, 1/8/7) come out
 // at 90-100 registers unconstrained (5 CTAs/SM); capping them for 6 CTAs
 // costs no spills and measured +10% on 1/8/7 mul, +2-5% on 1/5/10 mul.  Small
-// networks are HBM-bound (the cap measured -2..-3% there) and the widest
-// (1/8/15 mul at 4 CTAs/SM, mul_add at 5 or 6) stayed within +-2% after the
-// Booth product (profiles/r01_ab_minb_wide.txt): they run at 0.90-0.95 of the
-// LOP3 rate of the clock they are power-capped to, so only fewer LOP3 helps.
+// networks are HBM-bound (the cap measured -2..-3% there).  The 1/8/15 mul
+// (~1000 LOP3 per word, 137 registers uncapped = 3 CTAs/SM) capped for 4
+// CTAs/SM (115 registers, no spills) measured +4% in two repeated A/Bs
+// (profiles/r01_ab_minb_wide.txt); mul_add at 5 or 6 stayed within +-2%.
 #ifndef BFP_MID_MINB
 #define BFP_MID_MINB 6
 #endif
 #ifndef BFP_WIDE_MINB
-#define BFP_WIDE_MINB 1
+#define BFP_WIDE_MINB 4
 #endif
 #ifndef BFP_MULADD_MINB
 #define BFP_MULADD_MINB 1
