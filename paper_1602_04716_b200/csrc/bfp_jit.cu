@@ -119,12 +119,14 @@ uint64_t fnv1a(const std::string& s, uint64_t h = 1469598103934665603ull) {
 // returns the CUBIN and the lowered name of `expr` (or `expr` itself when it
 // names an extern "C" kernel: lower = false).
 bool nvrtc_compile(const std::string& src, const std::string& expr, bool lower, std::vector<char>* cubin,
-                   std::string* name) {
+                   std::string* name, const std::string& extra_inc = "") {
   const Nvrtc& nv = nvrtc();
   if (!nv.ok) return false;
   const std::string inc = "--include-path=" + csrc_dir();
-  const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", inc.c_str(), "-default-device",
-                        "-lineinfo"};
+  const std::string inc2 = "--include-path=" + (extra_inc.empty() ? csrc_dir() : extra_inc);
+  const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", inc.c_str(), inc2.c_str(),
+                        "-default-device", "-lineinfo"};
+  constexpr int kOpts = 6;
   const std::string dir = cache_dir();
   std::string path;
   if (!dir.empty()) {
@@ -153,7 +155,7 @@ bool nvrtc_compile(const std::string& src, const std::string& expr, bool lower, 
   nvrtcProgram_t prog = nullptr;
   if (nv.create(&prog, src.c_str(), "bfp_jit.cu", 0, nullptr, nullptr)) return false;
   if (lower) nv.add_name(prog, expr.c_str());
-  if (nv.compile(prog, 5, opts) != 0) {
+  if (nv.compile(prog, kOpts, opts) != 0) {
     size_t ls = 0;
     nv.log_size(prog, &ls);
     std::string log(ls, '\0');
@@ -187,6 +189,52 @@ bool nvrtc_compile(const std::string& src, const std::string& expr, bool lower, 
     }
   }
   return true;
+}
+
+// ---- runtime LOP3 covers (BFP_JIT_MAP=1) ---------------------------------
+// Formats without a build-time cover normally run the templates as ptxas maps
+// them (6-12% slower on logic-bound networks than the LOP3-mapped covers,
+// DESIGN.md §10).  With BFP_JIT_MAP=1 the build-time mapper (tools/lutmap/
+// gen.cpp, GEN_ONE mode) is compiled with g++ for the format and run once; its
+// header lands in <cache>/gen and every kernel of the format includes it.  Any
+// failure (no g++, no tools tree, no cache directory) falls back to templates.
+// Returns the directory holding gen_E_S_RN_FTZ.cuh, or "" when not mapped.
+std::string runtime_cover_dir(unsigned e, unsigned s, int rn, int ftz) {
+  const char* env = std::getenv("BFP_JIT_MAP");
+  if (!env || env[0] != '1') return "";
+  const std::string cache = cache_dir();
+  if (cache.empty()) return "";
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  const std::string dir = cache + "/gen";
+  const std::string stem = "gen_" + std::to_string(e) + "_" + std::to_string(s) + "_" + std::to_string(rn) +
+                           "_" + std::to_string(ftz);
+  const std::string hdr = dir + "/" + stem + ".cuh";
+  struct stat st {};
+  if (stat(hdr.c_str(), &st) == 0) return dir;
+  const std::string tools = csrc_dir() + "/../../tools/lutmap";
+  if (stat((tools + "/gen.cpp").c_str(), &st) != 0) return "";
+  for (size_t i = 1; i <= dir.size(); ++i)
+    if (i == dir.size() || dir[i] == '/') mkdir(dir.substr(0, i).c_str(), 0755);
+  const std::string exe = dir + "/" + stem + ".gen." + std::to_string(getpid());
+  char defs[160];
+  std::snprintf(defs, sizeof defs, "-DGEN_ONE_E=%u -DGEN_ONE_S=%u -DGEN_ONE_RN=%d -DGEN_ONE_FTZ=%d", e, s, rn, ftz);
+  const std::string cmd = "g++ -O2 -std=c++17 -I'" + csrc_dir() + "' -I'" + tools + "' " + defs + " '" + tools +
+                          "/gen.cpp' -o '" + exe + "' >/dev/null 2>&1 && '" + exe + "' '" + dir +
+                          "' >/dev/null 2>&1";
+  const int rc = std::system(cmd.c_str());
+  std::remove(exe.c_str());
+  if (rc != 0 || stat(hdr.c_str(), &st) != 0) {
+    std::fprintf(stderr, "[bfp jit] runtime LOP3 mapping unavailable for 1/%u/%u (rc %d); using templates\n",
+                 e, s, rc);
+    return "";
+  }
+  return dir;
+}
+
+std::string cover_include(unsigned e, unsigned s, int rn, int ftz) {
+  return "#include \"gen_" + std::to_string(e) + "_" + std::to_string(s) + "_" + std::to_string(rn) + "_" +
+         std::to_string(ftz) + ".cuh\"\n";
 }
 
 struct JitKernel {
@@ -318,8 +366,10 @@ class JitFormat final : public Impl {
     }
     std::vector<char> cubin;
     std::string name;
-    if (!nvrtc_compile("#include \"bfp_kernels.cuh\"\n", expr, true, &cubin, &name))
-      return cudaErrorNotSupported;
+    const std::string cover = runtime_cover_dir(e_, s_, rn_, ftz_);
+    std::string src = "#include \"bfp_kernels.cuh\"\n";
+    if (!cover.empty()) src += cover_include(e_, s_, rn_, ftz_);
+    if (!nvrtc_compile(src, expr, true, &cubin, &name, cover)) return cudaErrorNotSupported;
     cudaLibrary_t lib = nullptr;
     cudaError_t e = cudaLibraryLoadData(&lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
     if (e != cudaSuccess) return e;
@@ -472,10 +522,13 @@ cudaError_t chain_kernel(unsigned e, unsigned s, int rn, int ftz, const std::str
   const std::string gen = csrc_dir() + "/gen/gen_" + std::to_string(e) + "_" + std::to_string(s) + ".cuh";
   FILE* fg = std::getenv("BFP_CHAIN_NOGEN") ? nullptr : std::fopen(gen.c_str(), "r");
   if (fg) std::fclose(fg);
-  const std::string src = chain_source(e, s, rn, ftz, prog, fg != nullptr, f32);
+  std::string src = chain_source(e, s, rn, ftz, prog, fg != nullptr, f32);
+  std::string cover;
+  if (!fg && !(cover = runtime_cover_dir(e, s, rn, ftz)).empty())
+    src = cover_include(e, s, rn, ftz) + src;  // specialisations before the kernel
   std::vector<char> cubin;
   std::string name;
-  if (!nvrtc_compile(src, "bfp_chain_k", false, &cubin, &name)) return cudaErrorNotSupported;
+  if (!nvrtc_compile(src, "bfp_chain_k", false, &cubin, &name, cover)) return cudaErrorNotSupported;
   cudaLibrary_t lib = nullptr;
   cudaError_t err = cudaLibraryLoadData(&lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
   if (err != cudaSuccess) return err;

@@ -233,3 +233,38 @@ def test_layout_fuzz(oracle):
             assert np.array_equal(bfp.to_u64(bfp.unpack(vf), spec).cpu().numpy().astype(np.uint64), wf), (t, fmt, "f32")
             bf = bfp.unpack_f32(vf).cpu().numpy().view(np.uint32)
             assert np.array_equal(bf, oracle.decode_f32(fmt, wf).view(np.uint32)), (t, fmt, "f32 back")
+
+
+def test_jit_runtime_covers(tmp_path, ref_oracle):
+    """BFP_JIT_MAP=1: a runtime format gets LOP3-mapped covers generated on
+    first use (tools/lutmap, GEN_ONE mode) -- same bits as the reference."""
+    import os
+    import subprocess
+    import sys
+    from conftest import ROOT
+    code = (
+        "import sys, numpy as np, torch, ctypes as C\n"
+        "sys.path.insert(0, 'tests'); sys.path.insert(0, 'oracle')\n"
+        "import oracle as O\n"
+        "from conftest import operands\n"
+        "from paper_1602_04716_b200 import _lib\n"
+        "L = _lib.lib()\n"
+        "rng = np.random.default_rng(5)\n"
+        "for fmt in [(3, 11, 1, 0), (7, 20, 0, 1)]:\n"
+        "    e, s = fmt[:2]; nb = 1 + e + s; n = 1 << 13\n"
+        "    x, y, c = (operands(e, s, n, rng) for _ in range(3))\n"
+        "    px, py, pc = (O.pack_planes(v, nb) for v in (x, y, c))\n"
+        "    f = _lib.BfpFormat(*fmt, b'')\n"
+        "    for op, name in enumerate(['add', 'sub', 'mul', 'div', 'mul_add']):\n"
+        "        dx, dy, dc = (torch.from_numpy(a.view(np.int32)).cuda() for a in (px, py, pc))\n"
+        "        dz = torch.empty_like(dx)\n"
+        "        assert L.bfp_arith(op, C.byref(f), dx.data_ptr(), dy.data_ptr(), dc.data_ptr(), dz.data_ptr(),\n"
+        "                           n, None) == 0\n"
+        "        want = O.ref_binop_planes(name, fmt, px, py, pc if name == 'mul_add' else None)\n"
+        "        assert np.array_equal(dz.cpu().numpy().view(np.uint32), want), (fmt, name)\n"
+        "print('ok')\n")
+    env = dict(os.environ, BFP_JIT_CACHE=str(tmp_path), BFP_JIT_MAP="1", PYTHONPATH=str(ROOT))
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-3000:]
+    hdrs = sorted(p.name for p in (tmp_path / "gen").glob("*.cuh"))
+    assert hdrs == ["gen_3_11_1_0.cuh", "gen_7_20_0_1.cuh"], hdrs
