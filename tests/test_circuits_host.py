@@ -211,3 +211,47 @@ def test_template_format_sweep(tmp_path, oracle):
     r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr
     assert r.stdout.strip().endswith("total bad 0"), r.stdout
+
+
+def test_runtime_cover_generator(tmp_path):
+    """tools/lutmap/gen.cpp in GEN_ONE mode (what BFP_JIT_MAP=1 runs for a
+    runtime format): its header equals the template networks bit for bit."""
+    import subprocess
+    from conftest import ROOT
+    csrc = ROOT / "paper_1602_04716_b200" / "csrc"
+    lut = ROOT / "tools" / "lutmap"
+    e, s, rn, ftz = 3, 11, 1, 0
+    gen = tmp_path / "gen"
+    subprocess.run(["g++", "-O2", "-std=c++17", f"-I{csrc}", f"-I{lut}", f"-DGEN_ONE_E={e}", f"-DGEN_ONE_S={s}",
+                    f"-DGEN_ONE_RN={rn}", f"-DGEN_ONE_FTZ={ftz}", str(lut / "gen.cpp"), "-o", str(gen)], check=True)
+    subprocess.run([str(gen), str(tmp_path)], check=True)
+    hdr = tmp_path / f"gen_{e}_{s}_{rn}_{ftz}.cuh"
+    assert hdr.exists()
+    src = tmp_path / "check.cpp"
+    src.write_text(f"""
+#include "bfp_circuits.cuh"
+#include "{hdr.name}"
+#include <cstdio>
+#include <random>
+using namespace bfpg;
+using F = Format<{e}, {s}, {str(bool(rn)).lower()}, {str(bool(ftz)).lower()}>;
+int main() {{
+  std::mt19937 r(3);
+  long bad = 0;
+  for (int it = 0; it < 4000; ++it) {{
+    w32 X[F::N], Y[F::N], C[F::N], Z1[F::N], Z2[F::N];
+    for (int j = 0; j < F::N; ++j) {{ X[j] = r(); Y[j] = r(); C[j] = r(); }}
+    Gen<F, 0>::run(X, Y, C, Z1); add_w<F, false>(X, Y, Z2); for (int j = 0; j < F::N; ++j) bad += Z1[j] != Z2[j];
+    Gen<F, 1>::run(X, Y, C, Z1); add_w<F, true>(X, Y, Z2); for (int j = 0; j < F::N; ++j) bad += Z1[j] != Z2[j];
+    Gen<F, 2>::run(X, Y, C, Z1); mul_w<F>(X, Y, Z2); for (int j = 0; j < F::N; ++j) bad += Z1[j] != Z2[j];
+    Gen<F, 3>::run(X, Y, C, Z1); div_w<F>(X, Y, Z2); for (int j = 0; j < F::N; ++j) bad += Z1[j] != Z2[j];
+    Gen<F, 4>::run(X, Y, C, Z1); mul_add_w<F>(X, Y, C, Z2); for (int j = 0; j < F::N; ++j) bad += Z1[j] != Z2[j];
+  }}
+  std::printf("bad %ld\\n", bad);
+  return bad != 0;
+}}
+""")
+    exe = tmp_path / "check"
+    subprocess.run(["g++", "-O1", "-std=c++17", f"-I{csrc}", f"-I{tmp_path}", str(src), "-o", str(exe)], check=True)
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "bad 0" in r.stdout, r.stdout + r.stderr
