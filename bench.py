@@ -824,6 +824,12 @@ CONFIG_TEXT = {
 }
 
 
+def scaling_of(cfg: str) -> str:
+    """C5 splits a fixed 2^32 elements over the GPUs (strong); every other
+    config fixes the per-GPU N (weak)."""
+    return "strong" if cfg == "C5" else "weak"
+
+
 def config_block(cfg: str, world: int, jobs=None) -> dict:
     text, fmt, n = CONFIG_TEXT[cfg]
     d = {"workload": text, "format": fmt, "rounding": "rn" if MODE[0] else "rz",
@@ -855,7 +861,7 @@ def main_reference(args) -> None:
             "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": UNIT,
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(r["median_s"] * 1e3, 3), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u64 lanes (lane<1024> bitslice)",
+            "scaling": scaling_of(cfg), "vs_baseline": None, "dtype": "u64 lanes (lane<1024> bitslice)",
             "data": "synthetic (seeded SplitMix64 operands; BASELINE.json configs)",
             "config": config_block(cfg, world),
             "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": r["cores"],
@@ -982,7 +988,7 @@ def main_ours(args) -> None:
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 5),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "higher_is_better": True, "scaling": scaling_of(cfg), "vs_baseline": None,
             "dtype": "u32 (bitslice words)",
             "data": "synthetic (seeded SplitMix64 operands; BASELINE.json configs)",
             "config": config_block(cfg, world, jobs),
