@@ -1,34 +1,49 @@
 #!/usr/bin/env python3
 """Benchmark of the B200 bitslice FP hot path (BASELINE.json metric:
-"bitslice FP ops/sec (Gelem/s) per format vs LOP3/HBM roofline").
+"bitslice FP ops/sec (Gelem/s) per format vs LOP3/HBM roofline, 1/2/4/8 B200").
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config C2|C1|C3|C4|C5|all]
+                    [--config default|C1..C5|X1..X3u|all] [--dry-run]
 
-Default workload: configs[1] = C2 -- 1/4/3 (fp8, RN, gradual) elementwise
-multiply AND subtract over N = 2^26 elements per GPU; one step = one mul
-launch + one sub launch over resident planes.  The metric counts result
-elements: value = 2 * N * world / step time (Gelem/s).  Under torchrun each
-rank owns its own 2^26-element shard (weak scaling, no collective on the data
-path).
+Default workload (`--config default`): the headline is configs[4] = C5, the
+largest configuration that fits one GPU -- z = round(round(a*b) + c) in 1/6/9
+(the reference chain bfp_add(bfp_mul(a, b), c), arith.hpp:235-373) over a
+FIXED N = 2^32 elements split evenly over the GPUs (strong scaling, no
+collective on the data path: SURVEY.md §8e); one step = one fused mul_add
+launch per GPU over resident planes.  value = 2^32 / step time (max over
+ranks), Gelem/s.  The same line carries C4's per-format sweep (add and mul
+for 1/3/2, 1/5/3, 1/5/7, 1/8/7, 1/8/15 at 2^28 elements per GPU) and C5 in
+`per_format`, each kernel with its binding roofline leg.
+
+--gpus N with no torchrun environment re-launches itself through
+torch.distributed.run with N ranks (one per GPU, NCCL for the barrier and
+the max-over-ranks times only).  --dry-run does the same with gloo on the
+CPU and a stand-in step: it checks the launcher, the shard ranges, the
+max-over-ranks reduction and the rank-0-only output without a GPU.
 
 JSON line (rank 0): value (device, inputs resident in HBM), e2e (the same
-step through the C ABI with host planes: H2D + kernels + D2H), roofline
-(dominant kernel, HBM leg + measured LOP3 leg), cpu_baseline (the reference
-itself -- oracle/_ref, the unmodified headers compiled in place -- on the
-host cores, bounded sample), clocks (nvidia-smi during a sustained window of
-the same step), gpu_launches.
+step through the C ABI with pinned host buffers: H2D + kernel + D2H inside
+the timed region), roofline (the dominant kernel on its BINDING leg: the
+LOP3 issue rate against the measured probe peak, or HBM bytes against the
+measured copy peak; DRAM traffic measured by an ncu subprocess in this run),
+cpu_baseline (the reference itself -- oracle/_ref, the unmodified headers
+compiled in place -- on the host cores, ~10 s, best and median), clocks
+(nvidia-smi during a sustained window of the same step), gpu_launches.
 
 --impl reference times the reference's own CPU implementation (oracle/_ref)
-on this host's cores on the same config/metric; rank 0 only.
+on this host's cores for the same config / metric; rank 0 only.
 """
 from __future__ import annotations
 
 import argparse
+import csv
 import ctypes as C
 import faulthandler
+import io
 import json
 import os
+import re
+import socket
 import statistics
 import subprocess
 import sys
@@ -42,14 +57,93 @@ sys.path.insert(0, str(ROOT))
 METRIC = "bitslice FP ops/sec (Gelem/s) per format vs LOP3/HBM roofline"
 UNIT = "Gelem/s"
 OPNAMES = {"add": 0, "sub": 1, "mul": 2, "div": 3, "mul_add": 4}
+L2_BYTES = 126 * 1024 * 1024
+
+# (rn, ftz) of every config: the reference default RN + gradual
+# (format.hpp:26-27); --rounding / --subnormals select the secondary rows.
+MODE = (1, 0)
 
 
-# ---------------------------------------------------------------- utilities
+def log(msg: str) -> None:
+    print(f"[bench r{os.environ.get('RANK', '0')}] {msg}", file=sys.stderr, flush=True)
+
+
+def mode_text() -> str:
+    return ("rn" if MODE[0] else "rz") + ("+ftz" if MODE[1] else "")
+
+
+# ------------------------------------------------------- distributed plumbing
 def env_dist():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return world, rank, local
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def maybe_relaunch(args) -> None:
+    """--gpus N > 1 without a torchrun environment: run this script under
+    torch.distributed.run with N ranks on this node and exit with its code."""
+    if "WORLD_SIZE" in os.environ or args.gpus <= 1:
+        return
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={_free_port()}", str(Path(__file__).resolve())] + sys.argv[1:]
+    log(f"launching {args.gpus} ranks: {' '.join(cmd[1:6])} ...")
+    sys.exit(subprocess.run(cmd).returncode)
+
+
+class Dist:
+    """One process per GPU (gloo on the CPU for --dry-run).  Collectives are
+    used only for the barrier around timed regions, the max-over-ranks times
+    and the per-rank report -- never on the data path."""
+
+    def __init__(self, backend: str):
+        import torch
+        import torch.distributed as dist
+        self.world, self.rank, self.local = env_dist()
+        self.backend = backend
+        self.dist = dist if self.world > 1 else None
+        self.dev = torch.device("cuda", self.local) if backend == "nccl" else torch.device("cpu")
+        if self.world > 1:
+            if backend == "nccl":
+                os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator init on stderr
+                os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+                torch.cuda.set_device(self.dev)
+                dist.init_process_group("nccl", device_id=self.dev)
+            else:
+                dist.init_process_group("gloo")
+            assert dist.get_world_size() == self.world and dist.get_rank() == self.rank
+            log(f"{backend} process group up: rank {self.rank}/{self.world}, device {self.dev}")
+
+    def barrier(self) -> None:
+        if self.dist:
+            self.dist.barrier()
+
+    def reduce(self, vals: list[float], op: str = "max") -> list[float]:
+        if not self.dist:
+            return list(vals)
+        import torch
+        t = torch.tensor(vals, dtype=torch.float64, device=self.dev)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX if op == "max" else self.dist.ReduceOp.SUM)
+        return [float(v) for v in t.cpu()]
+
+    def gather(self, obj) -> list:
+        if not self.dist:
+            return [obj]
+        out = [None] * self.world
+        self.dist.all_gather_object(out, obj)
+        return out
+
+    def close(self) -> None:
+        if self.dist:
+            self.dist.barrier()
+            self.dist.destroy_process_group()
 
 
 def measured_peaks() -> dict:
@@ -108,7 +202,7 @@ class ClockSampler:
             for nm, v in zip(names, r[4:8]):
                 if v.lower() == "active":
                     reasons.add(nm)
-        num = lambda v: float(v) if v.replace(".", "", 1).isdigit() else None
+        num = lambda v: float(v) if v.replace(".", "", 1).isdigit() else None  # noqa: E731
         pw = [num(r[2]) for r in self.rows if len(r) >= 8 and num(r[2]) is not None]
         lim = [num(r[8]) for r in self.rows if len(r) >= 9 and num(r[8]) is not None]
         return {"sm_mhz": statistics.median(sm) if sm else None,
@@ -132,8 +226,8 @@ _SASS = None
 
 
 def sass_lop3(fmt, rn, ftz, op: int) -> int | None:
-    """Static LOP3 count of the arithmetic kernel (one 32-element unit per
-    loop iteration) from cuobjdump of the loaded library."""
+    """Static LOP3 count of the shipped arithmetic kernel (one 32-element unit
+    per loop iteration) from cuobjdump of the loaded library."""
     global _SASS
     try:
         if _SASS is None:
@@ -153,12 +247,26 @@ def sass_lop3(fmt, rn, ftz, op: int) -> int | None:
 
 # ------------------------------------------------------------ the workloads
 class Job:
-    """One timed kernel of a step: `launch(i)` issues it on the current
-    stream (i = step index, for rotating outputs)."""
+    """One timed kernel of a step: `launch(i, stream)` issues it (i = step
+    index: operand sets / outputs rotate with it).  `touch(i)` = (set id,
+    bytes read from that set, bytes written) for the L2 reuse accounting."""
 
-    def __init__(self, label, op, spec, n, launch, algo_bytes, host=None):
+    def __init__(self, label, op, spec, n, launch, algo_bytes, host=None, touch=None):
         self.label, self.op, self.spec, self.n = label, op, spec, n
         self.launch, self.algo_bytes, self.host = launch, algo_bytes, host
+        self.touch = touch or (lambda i, lb=label, b=algo_bytes: (lb, b, 0))
+
+    @property
+    def fmt(self) -> str:
+        return f"1/{self.spec.exp_bits}/{self.spec.sig_bits}"
+
+
+class JobMeta:
+    """What the report needs of a Job once its device operands are freed."""
+
+    def __init__(self, j: Job):
+        self.label, self.op, self.spec, self.n, self.algo_bytes = j.label, j.op, j.spec, j.n, j.algo_bytes
+        self.fmt = j.fmt
 
 
 def _chunked_pack_f32(gen, n, spec, device, chunk=1 << 27):
@@ -180,40 +288,42 @@ def _chunked_pack_f32(gen, n, spec, device, chunk=1 << 27):
     return v
 
 
-L2_BYTES = 126 * 1024 * 1024
-
-# (rn, ftz) of every config: the reference default RN + gradual
-# (format.hpp:26-27); --rounding / --subnormals select the secondary rows.
-MODE = (1, 0)
-
-
-def mode_text() -> str:
-    return ("rn" if MODE[0] else "rz") + ("+ftz" if MODE[1] else "")
-
-
 def spec_of(e: int, s: int):
     import paper_1602_04716_b200 as bfp
     return bfp.make_spec(e, s, bfp.rounding_mode(MODE[0]), bfp.subnormal_policy(MODE[1]))
 
 
-def input_sets(spec, n, n_inputs: int) -> int:
-    """Rotating input sets so that consecutive uses of one set are separated
-    by >= 2x L2 of other traffic (inputs always come from HBM)."""
-    set_bytes = n_inputs * spec.plane_bytes(n)
-    return max(1, -(-2 * L2_BYTES // set_bytes))
+def rotation_sets(spec, n, n_inputs: int, launches_per_step: int = 1) -> int:
+    """Operand sets rotated launch by launch so that a set is re-read only
+    after >= 2x L2 of OTHER traffic (reads of the other sets + every write):
+    with k sets and one launch touching (n_inputs + 1) planes of n elements,
+    a set comes back after k - 1 launches' traffic plus its own launch's write."""
+    pb = spec.plane_bytes(n)
+    launch = (n_inputs + 1) * pb
+    k = 1
+    while (k - 1) * launch + pb < 2 * L2_BYTES:
+        k += 1
+    # every launch of a step uses a different set, so k >= launches per step
+    return max(k, launches_per_step)
 
 
-def _arith_job(label, op, spec, n, sets, device):
-    """sets: list of (a, b, c) operand tuples rotated step by step."""
-    import torch
+def _arith_job(label, op, spec, n, sets, device, slot=0, stride=1):
+    """sets: list of (a, b, c) operand tuples; launch i of this job uses set
+    (stride * i + slot) mod len(sets) -- jobs of one step take different slots
+    so no launch re-reads the set its predecessor just read."""
     import paper_1602_04716_b200 as bfp
     L = bfp.lib()
     outs = [bfp.empty(spec, n, device) for _ in range(2)]  # rotating outputs
+    nin = 3 if sets[0][2] is not None else 2
+    pb = spec.plane_bytes(n)
+
+    def idx(i):
+        return (stride * i + slot) % len(sets)
 
     def launch(i, st):
         # resident operands that nothing in the step writes: BFP_INPUTS_READY
         # lets each kernel's first loads overlap its predecessor's tail
-        a, b, c = sets[i % len(sets)]
+        a, b, c = sets[idx(i)]
         rc = L.bfp_arith_ex(OPNAMES[op], spec.c, a.planes.data_ptr(), b.planes.data_ptr(),
                             c.planes.data_ptr() if c is not None else None,
                             outs[i & 1].planes.data_ptr(), n, st, 1)
@@ -222,13 +332,29 @@ def _arith_job(label, op, spec, n, sets, device):
 
     nbits = spec.total_bits()
     a, b, c = sets[0]
-    nin = 3 if c is not None else 2
     return Job(label, op, spec, n, launch, (nin + 1) * nbits / 8 * n,
                host={"kind": "arith", "op": op, "inputs": [a, b] + ([c] if c is not None else []),
-                     "sets": len(sets)})
+                     "sets": len(sets)},
+               touch=lambda i: ((id(sets), idx(i)), nin * pb, pb))
+
+
+def _clone_sets(first, k):
+    return [first] + [tuple(v.clone() if v is not None else None for v in first) for _ in range(k - 1)]
 
 
 X1_FMTS = [(3, 2), (4, 3), (5, 3), (5, 7), (5, 10), (8, 7), (8, 15)]
+C4_FMTS = [(3, 2), (5, 3), (5, 7), (8, 7), (8, 15)]
+
+
+def config_n(cfg: str, rank: int, world: int) -> tuple[int, int]:
+    """Element range [lo, hi) of this rank: C5 splits a fixed 2^32 total over
+    the ranks (strong scaling); every other config gives each rank its own
+    block of the per-GPU N (weak scaling).  Both block-aligned, contiguous."""
+    from paper_1602_04716_b200 import workloads as W
+    if cfg == "C5":
+        return W.shard(1 << 32, rank, world)
+    n = CONFIG_TEXT[cfg][2]
+    return rank * n, (rank + 1) * n
 
 
 def make_jobs(cfg: str, rank: int, world: int, device) -> list:
@@ -238,33 +364,27 @@ def make_jobs(cfg: str, rank: int, world: int, device) -> list:
     from paper_1602_04716_b200 import workloads as W
 
     L = bfp.lib()
+    lo, hi = config_n(cfg, rank, world)
+    n = hi - lo
     if cfg == "C1":
-        n = 1 << 24
         spec = spec_of(4, 3)
-        lo = rank * n
-        sets = []
-        for r in range(input_sets(spec, n, 2)):  # same data, distinct buffers
-            if r == 0:
-                a = bfp.pack_f32(W.c1_floats(lo, lo + n, W.SEED_A, device), spec)
-                b = bfp.pack_f32(W.c1_floats(lo, lo + n, W.SEED_B, device), spec)
-            sets.append((a, b, None) if r == 0 else (a.clone(), b.clone(), None))
+        a = bfp.pack_f32(W.c1_floats(lo, hi, W.SEED_A, device), spec)
+        b = bfp.pack_f32(W.c1_floats(lo, hi, W.SEED_B, device), spec)
+        sets = _clone_sets((a, b, None), rotation_sets(spec, n, 2))  # same data, distinct buffers
         return [_arith_job("add", "add", spec, n, sets, device)]
     if cfg == "C2":
-        n = 1 << 26
         spec = spec_of(4, 3)
-        lo = rank * n
-        a = bfp.pack(W.c2_encodings(lo, lo + n, W.SEED_A, device), spec)
-        b = bfp.pack(W.c2_encodings(lo, lo + n, W.SEED_B, device), spec)
-        sets = [(a, b, None)] + [(a.clone(), b.clone(), None)
-                                 for _ in range(input_sets(spec, n, 2) - 1)]
-        return [_arith_job("mul", "mul", spec, n, sets, device),
-                _arith_job("sub", "sub", spec, n, sets, device)]
+        a = bfp.pack(W.c2_encodings(lo, hi, W.SEED_A, device), spec)
+        b = bfp.pack(W.c2_encodings(lo, hi, W.SEED_B, device), spec)
+        sets = _clone_sets((a, b, None), rotation_sets(spec, n, 2, launches_per_step=2))
+        # mul takes even launches' sets, sub odd ones: the sub never re-reads
+        # the operands the mul just streamed through L2
+        return [_arith_job("mul", "mul", spec, n, sets, device, slot=0, stride=2),
+                _arith_job("sub", "sub", spec, n, sets, device, slot=1, stride=2)]
     if cfg == "C3":
-        n = 1 << 28
         spec = spec_of(5, 10)
-        lo = rank * n
-        xa = W.c3_floats(lo, lo + n, W.SEED_A, device)
-        xb = W.c3_floats(lo, lo + n, W.SEED_B, device)
+        xa = W.c3_floats(lo, hi, W.SEED_A, device)
+        xb = W.c3_floats(lo, hi, W.SEED_B, device)
         a, b = bfp.pack_f32(xa, spec), bfp.pack_f32(xb, spec)
         del xb
         torch.cuda.empty_cache()
@@ -282,51 +402,36 @@ def make_jobs(cfg: str, rank: int, world: int, device) -> list:
                 raise RuntimeError(L.bfp_last_error())
 
         nb = spec.total_bits()
+        pb = spec.plane_bytes(n)
         return [Job("pack_f32", "pack_f32", spec, n, pack_launch, (4 + nb / 8) * n,
-                    host={"kind": "pack_f32", "x": xa}),
+                    host={"kind": "pack_f32", "x": xa}, touch=lambda i: ("xa", 4 * n, pb)),
                 _arith_job("add", "add", spec, n, [(a, b, None)], device),
                 _arith_job("mul", "mul", spec, n, [(a, b, None)], device),
                 Job("unpack_f32", "unpack_f32", spec, n, unpack_launch, (nb / 8 + 4) * n,
-                    host={"kind": "unpack_f32", "v": a})]
-    if cfg == "C4":
-        n = 1 << 28
-        lo = rank * n
+                    host={"kind": "unpack_f32", "v": a}, touch=lambda i: ("a", pb, 4 * n))]
+    if cfg in ("C4", "X1"):
         jobs = []
-        for (e, s) in W.CONFIGS["C4"]["fmts"]:
+        fmts = C4_FMTS if cfg == "C4" else X1_FMTS
+        ops = ("add", "mul") if cfg == "C4" else ("div",)
+        for (e, s) in fmts:
             spec = spec_of(e, s)
-            a = bfp.pack(W.c4_encodings(e, s, lo, lo + n, W.SEED_A, device), spec)
-            b = bfp.pack(W.c4_encodings(e, s, lo, lo + n, W.SEED_B, device), spec)
+            a = bfp.pack(W.c4_encodings(e, s, lo, hi, W.SEED_A, device), spec)
+            b = bfp.pack(W.c4_encodings(e, s, lo, hi, W.SEED_B, device), spec)
             torch.cuda.empty_cache()
-            jobs.append(_arith_job(f"add_1/{e}/{s}", "add", spec, n, [(a, b, None)], device))
-            jobs.append(_arith_job(f"mul_1/{e}/{s}", "mul", spec, n, [(a, b, None)], device))
+            for op in ops:
+                jobs.append(_arith_job(f"{op}_1/{e}/{s}", op, spec, n, [(a, b, None)], device))
         return jobs
     if cfg == "C5":
-        total = 1 << 32
-        lo, hi = W.shard(total, rank, world)
-        n = hi - lo
         spec = spec_of(6, 9)
         ops = [_chunked_pack_f32(lambda a_, b_, sd=sd: W.c5_floats(lo + a_, lo + b_, sd, device), n,
                                  spec, device)
                for sd in (W.SEED_A, W.SEED_B, W.SEED_C)]
         torch.cuda.empty_cache()
         return [_arith_job("mul_add", "mul_add", spec, n, [tuple(ops)], device)]
-    if cfg == "X1":  # secondary: bfp_div over the C4 formats + 1/4/3, 1/5/10
-        n = 1 << 28
-        lo = rank * n
-        jobs = []
-        for (e, s) in X1_FMTS:
-            spec = spec_of(e, s)
-            a = bfp.pack(W.c4_encodings(e, s, lo, lo + n, W.SEED_A, device), spec)
-            b = bfp.pack(W.c4_encodings(e, s, lo, lo + n, W.SEED_B, device), spec)
-            torch.cuda.empty_cache()
-            jobs.append(_arith_job(f"div_1/{e}/{s}", "div", spec, n, [(a, b, None)], device))
-        return jobs
     if cfg == "X2":  # secondary: fused float32-in/out ops, C3 operands
-        n = 1 << 28
         spec = spec_of(5, 10)
-        lo = rank * n
-        xa = W.c3_floats(lo, lo + n, W.SEED_A, device)
-        xb = W.c3_floats(lo, lo + n, W.SEED_B, device)
+        xa = W.c3_floats(lo, hi, W.SEED_A, device)
+        xb = W.c3_floats(lo, hi, W.SEED_B, device)
         outs = [torch.empty(n, dtype=torch.float32, device=device) for _ in range(2)]
         jobs = []
         for op in ("add", "mul"):
@@ -336,13 +441,11 @@ def make_jobs(cfg: str, rank: int, world: int, device) -> list:
                 if rc != 0:
                     raise RuntimeError(L.bfp_last_error())
             jobs.append(Job(f"{op}_f32", f"{op}_f32", spec, n, launch, 12 * n,
-                            host={"kind": "none"}))
+                            host={"kind": "none"}, touch=lambda i: ("x", 8 * n, 4 * n)))
         return jobs
     if cfg in ("X3", "X3u"):  # secondary: z = a*b + c*d, fused (bfp_chain) or as 3 kernels
-        n = 1 << 28
         spec = spec_of(5, 10)
-        lo = rank * n
-        vs = [bfp.pack(W.c4_encodings(5, 10, lo, lo + n, sd, device), spec)
+        vs = [bfp.pack(W.c4_encodings(5, 10, lo, hi, sd, device), spec)
               for sd in (W.SEED_A, W.SEED_B, W.SEED_C, W.SEED_C + 1)]
         torch.cuda.empty_cache()
         outs = [bfp.empty(spec, n, device) for _ in range(2)]
@@ -370,17 +473,31 @@ def make_jobs(cfg: str, rank: int, world: int, device) -> list:
     raise ValueError(cfg)
 
 
-def run_device(cfg: str, steps: int, warmup: int, world: int, rank: int, local: int,
-               jobs=None) -> dict:
+def l2_reuse_distance(jobs, steps: int = 128) -> int:
+    """Smallest amount of other traffic (bytes) between two reads of the same
+    operand set over `steps` consecutive steps of the launch sequence (-1 if
+    no set is read twice in that window)."""
+    seq = [j.touch(i) for i in range(steps) for j in jobs]
+    best = None
+    for p, (sid, _, _) in enumerate(seq):
+        for q in range(p + 1, len(seq)):
+            if seq[q][0] == sid:
+                d = seq[p][2] + sum(r + w for _, r, w in seq[p + 1:q])
+                best = d if best is None else min(best, d)
+                break
+    return best if best is not None else -1
+
+
+# ---------------------------------------------------------- device timing
+def run_device(cfg: str, steps: int, warmup: int, D: Dist, jobs=None) -> dict:
     import torch
-    import torch.distributed as dist
     import paper_1602_04716_b200 as bfp
 
-    device = torch.device("cuda", local)
+    device = D.dev
     torch.cuda.set_device(device)
     L = bfp.lib()
     if jobs is None:
-        jobs = make_jobs(cfg, rank, world, device)
+        jobs = make_jobs(cfg, D.rank, D.world, device)
     stream = torch.cuda.current_stream(device)
     st = stream.cuda_stream
 
@@ -417,36 +534,32 @@ def run_device(cfg: str, steps: int, warmup: int, world: int, rank: int, local: 
     g_all.replay()  # untimed: graph upload + one more warm pass
     torch.cuda.synchronize()
 
-    # sustained window of the same graph for the clock record (~1.5 s)
-    t_probe = time.perf_counter()
-    g_all.replay()
-    torch.cuda.synchronize()
-    one = max(time.perf_counter() - t_probe, 1e-5)
-    with ClockSampler(local) as cs:
-        for _ in range(max(1, int(1.5 / one))):
-            g_all.replay()
-        torch.cuda.synchronize()
-    clocks = cs.summary()
-
     def timed_replay(g) -> float:
         t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        if world > 1:
-            dist.barrier()
+        D.barrier()
         torch.cuda.synchronize()
         t0.record(stream)  # replay() launches the graph on the current stream
         g.replay()
         t1.record(stream)
         torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
+        D.barrier()
         return t0.elapsed_time(t1)
 
-    # Timed region (the value): K whole steps, back to back.
-    ms_total = timed_replay(g_all)
-    if world > 1:
-        t = torch.tensor([ms_total], device=device)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_total = float(t.item())
+    # Timed region (the value): K whole steps, back to back, bracketed by a
+    # barrier + synchronize on both sides; nvidia-smi samples the clocks
+    # during it and during a sustained window of the same graph (~1.5 s).
+    t_probe = time.perf_counter()
+    g_all.replay()
+    torch.cuda.synchronize()
+    one = max(time.perf_counter() - t_probe, 1e-5)
+    with ClockSampler(local_index(device)) as cs:
+        ms_total = timed_replay(g_all)
+        for _ in range(max(1, int(1.5 / one))):
+            g_all.replay()
+        torch.cuda.synchronize()
+    clocks = cs.summary()
+    ms_rank = ms_total
+    ms_total = D.reduce([ms_total])[0]
     # The same K steps issued eagerly (one host call per kernel), for reference.
     te0, te1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
@@ -458,27 +571,37 @@ def run_device(cfg: str, steps: int, warmup: int, world: int, rank: int, local: 
     ms_total_eager = te0.elapsed_time(te1)
     # Per-kernel durations (the roofline): for each kernel of the step, a graph
     # of its K launches (same rotating operands) timed with events around the
-    # replay on the launching stream -> mean launch duration.
+    # replay on the launching stream -> mean launch duration, max over ranks.
     kern_ms = []
-    for k, j in enumerate(jobs):
+    for j in jobs:
         g, _ = capture(lambda s, j=j: [j.launch(i, s) for i in range(steps)])
         g.replay()
         torch.cuda.synchronize()
         kern_ms.append(timed_replay(g) / steps)
         del g
+    kern_ms = D.reduce(kern_ms)
     del g_all
-    return {"jobs": jobs, "ms_total": ms_total, "kern_ms": kern_ms, "clocks": clocks,
-            "launches": int(launches), "ms_total_eager": ms_total_eager}
+    return {"jobs": jobs, "ms_total": ms_total, "ms_total_rank": ms_rank, "kern_ms": kern_ms,
+            "clocks": clocks, "launches": int(launches), "ms_total_eager": ms_total_eager}
 
 
-def run_e2e(cfg: str, jobs, steps: int, world: int, rank: int, local: int) -> dict:
+def local_index(device) -> int:
+    """nvidia-smi index of a torch device (honours CUDA_VISIBLE_DEVICES)."""
+    vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+    idx = device.index or 0
+    if vis:
+        ids = [v.strip() for v in vis.split(",") if v.strip()]
+        if idx < len(ids) and ids[idx].isdigit():
+            return int(ids[idx])
+    return idx
+
+
+def run_e2e(jobs, steps: int, D: Dist) -> dict | None:
     """The same step through the C ABI with HOST buffers (pinned): every step
     copies its inputs H2D and its results D2H inside the timed region."""
     import torch
-    import torch.distributed as dist
     import paper_1602_04716_b200 as bfp
 
-    device = torch.device("cuda", local)
     L = bfp.lib()
     ctx = L.bfp_host_ctx_create(int(os.environ.get("BFP_E2E_CHUNK", 1 << 24)))
     bufs = []
@@ -490,12 +613,13 @@ def run_e2e(cfg: str, jobs, steps: int, world: int, rank: int, local: int) -> di
         bufs.append(p)
         return p
 
-    def host_copy(t: torch.Tensor):
+    def host_copy(t: torch.Tensor, chunk: int = 1 << 30):
         nbytes = t.numel() * t.element_size()
         p = pinned(nbytes)
-        src = t.cpu().numpy()  # keep alive across the copy
-        C.memmove(p, src.ctypes.data, nbytes)
-        del src
+        flat = t.reshape(-1).view(torch.uint8)
+        for o in range(0, nbytes, chunk):  # bounded pageable temporaries
+            src = flat[o:o + chunk].cpu().numpy()
+            C.memmove(p + o, src.ctypes.data, src.nbytes)
         return p
 
     try:
@@ -532,7 +656,7 @@ def run_e2e(cfg: str, jobs, steps: int, world: int, rank: int, local: int) -> di
                 calls.append((lambda spec=spec, hp=hp, hz=hz, n=n:
                               L.bfp_unpack_f32_host(ctx, spec.c, hp, hz, n), pb, 4 * n, n))
         torch.cuda.empty_cache()
-        if not calls:  # no host-buffer entry point for these kernels (X2)
+        if not calls:  # no host-buffer entry point for these kernels (X2, X3)
             return None
 
         def step():
@@ -542,17 +666,13 @@ def run_e2e(cfg: str, jobs, steps: int, world: int, rank: int, local: int) -> di
                     raise RuntimeError(L.bfp_last_error())
 
         step()
-        if world > 1:
-            dist.barrier()
         k = max(2, min(steps // 4, 10))
+        D.barrier()
         t = time.perf_counter()
         for _ in range(k):
             step()
         dt = (time.perf_counter() - t) / k
-        if world > 1:
-            tt = torch.tensor([dt], device=device)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            dt = float(tt.item())
+        dt = D.reduce([dt])[0]
         return {"s_per_step": dt, "h2d": sum(c[1] for c in calls),
                 "d2h": sum(c[2] for c in calls), "elems": sum(c[3] for c in calls), "steps": k}
     finally:
@@ -561,13 +681,12 @@ def run_e2e(cfg: str, jobs, steps: int, world: int, rank: int, local: int) -> di
         L.bfp_host_ctx_destroy(ctx)
 
 
-def hbm_2r1w_probe(local: int, nbytes: int = 1 << 30) -> float:
+def hbm_2r1w_probe(dev, nbytes: int = 1 << 30) -> float:
     """HBM rate of a plain 2-read : 1-write stream (torch bitwise_xor over
     1 GiB int32 operands, best of 10 by CUDA events) -- the access mix of a
     binary op.  MEASURED_PEAKS.json's copy is 1:1, which HBM serves slightly
     slower, so the binary-op kernels can exceed it; this is the context."""
     import torch
-    dev = torch.device("cuda", local)
     n = nbytes // 4
     a = torch.randint(0, 1 << 30, (n,), dtype=torch.int32, device=dev)
     b = torch.randint(0, 1 << 30, (n,), dtype=torch.int32, device=dev)
@@ -585,11 +704,10 @@ def hbm_2r1w_probe(local: int, nbytes: int = 1 << 30) -> float:
     return round(3 * nbytes / (best * 1e-3) / 1e9, 1)
 
 
-def pcie_probe(local: int, nbytes: int = 1 << 28) -> dict:
+def pcie_probe(dev, nbytes: int = 1 << 28) -> dict:
     """Pinned-host <-> device copy bandwidth on this box (the e2e ceiling):
     H2D alone, D2H alone, and both directions at once on two streams."""
     import torch
-    dev = torch.device("cuda", local)
     h_in = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
     h_out = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
     d_a = torch.empty(nbytes, dtype=torch.uint8, device=dev)
@@ -623,24 +741,13 @@ def pcie_probe(local: int, nbytes: int = 1 << 28) -> dict:
             "bidir_gbs": round(2 * nbytes / t3 / 1e9, 1)}
 
 
-def load_clock_frac(lop3: float, dur: float, peak: dict, clocks: dict) -> float | None:
-    """Logic fraction against the probe's LOP3 rate scaled to the SM clock the
-    step ran at (sampled during the timed graph replays): logic-heavy kernels
-    run power-capped below the probe's clock, which the burst figure ignores."""
-    mhz, pmhz = clocks.get("sm_mhz"), peak.get("sustained_sm_mhz")
-    if not mhz or not pmhz:
-        return None
-    return round(lop3 / (peak["sustained"] * mhz / pmhz) / dur, 4)
-
-
-def lop3_peak(local: int = 0) -> dict | None:
+def lop3_peak(dev) -> dict | None:
     """LOP3 issue rate of the probe kernel (bfp_probe_lop3: 8 independent
     chains per thread on every SM).  burst = one launch on a cool GPU (the
-    clock ceiling); sustained = back-to-back launches for ~2 s, median of the
-    second half, with the SM clock it settled at (the denominator for kernels
-    timed inside long steps; in practice the register-only probe is not
-    power-capped and settles at the clock ceiling, so load_clock_frac scales
-    it to the clock the kernels actually ran at)."""
+    clock ceiling; the roofline denominator); sustained = back-to-back
+    launches for ~2 s, median of the second half, with the SM clock it
+    settled at (the register-only probe is not power-capped and settles at
+    the ceiling, so load-clock fractions scale it to the kernels' clock)."""
     import paper_1602_04716_b200 as bfp
     L = bfp.lib()
     ms, rate = C.c_float(), C.c_double()
@@ -648,7 +755,7 @@ def lop3_peak(local: int = 0) -> dict | None:
         return None
     burst = rate.value
     rates = []
-    with ClockSampler(local) as cs:
+    with ClockSampler(local_index(dev)) as cs:
         t = time.perf_counter()
         while time.perf_counter() - t < 2.0:
             if L.bfp_probe_lop3(4000, C.byref(ms), C.byref(rate)) != 0:
@@ -656,6 +763,76 @@ def lop3_peak(local: int = 0) -> dict | None:
             rates.append(rate.value)
     sus = statistics.median(rates[len(rates) // 2:])
     return {"burst": burst, "sustained": sus, "sustained_sm_mhz": cs.summary().get("sm_mhz")}
+
+
+# ------------------------------------------- DRAM traffic, measured in-run
+def _under_profiler() -> bool:
+    return any(k in os.environ for k in ("CUDA_INJECTION64_PATH", "NV_TPS_LAUNCH_TOKEN", "NV_NSIGHT_INJECTION_TRANSPORT_TYPE"))
+
+
+def ncu_traffic(cfgs: list[str], local: int, timeout: int = 600) -> dict:
+    """DRAM bytes per launch of every timed kernel, measured in THIS run: an
+    ncu subprocess (dram__bytes_read/write.sum; no timing is taken from it)
+    over tools/profile_kernels.py, which builds the same resident operands and
+    issues each config's kernels once, in job order.  Returns
+    {cfg: [{"kernel", "bytes", "ncu_us"} per job]} or {"error": ...}."""
+    if _under_profiler():
+        return {"error": "bench itself runs under a profiler"}
+    exe = "ncu"
+    try:
+        subprocess.run([exe, "--version"], capture_output=True, check=True, timeout=60)
+    except (OSError, subprocess.SubprocessError):
+        return {"error": "ncu not available"}
+    out = {}
+    env = dict(os.environ)
+    env.pop("WORLD_SIZE", None)
+    env.pop("RANK", None)
+    env.pop("LOCAL_RANK", None)
+    if "CUDA_VISIBLE_DEVICES" not in env:
+        env["CUDA_VISIBLE_DEVICES"] = str(local)
+    mode = ["--rounding", "rn" if MODE[0] else "rz", "--subnormals", "ftz" if MODE[1] else "gradual"]
+    for cfg in cfgs:
+        kre = {"C3": "k_arith|k_pack_f32|k_unpack_f32", "X3": "bfp_chain_k"}.get(cfg, "k_arith")
+        logf = Path(os.environ.get("TMPDIR", "/tmp")) / f"bench_ncu_{os.getpid()}_{cfg}.csv"
+        cmd = [exe, "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum",
+               "--clock-control", "none", "-k", f"regex:{kre}", "--csv", "--print-units", "base",
+               "--log-file", str(logf),
+               sys.executable, str(ROOT / "tools" / "profile_kernels.py"), "--config", cfg,
+               "--iters", "1", "--marker"] + mode
+        try:
+            r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, env=env, cwd=ROOT)
+            txt = logf.read_text() if logf.exists() else ""
+        except subprocess.TimeoutExpired:
+            out[cfg] = {"error": "ncu timed out"}
+            continue
+        finally:
+            logf.unlink(missing_ok=True)
+        rows, order = {}, []
+        for rec in csv.reader(io.StringIO(txt)):
+            if len(rec) < 15 or rec[0] == "ID":
+                continue
+            kid, kname, metric, value = rec[0], rec[4], rec[12], rec[14]
+            if kid not in rows:
+                rows[kid] = {"kernel": kname}
+                order.append(kid)
+            try:
+                rows[kid][metric] = float(value.replace(",", ""))
+            except ValueError:
+                pass
+        # profile_kernels prints "TIMED k" before the timed launches; operand
+        # setup comes first, so the timed ones are the LAST k profiled kernels
+        m = re.search(r"TIMED (\d+)", r.stdout)
+        if not m or r.returncode != 0:
+            out[cfg] = {"error": f"ncu rc={r.returncode}: {(r.stderr or r.stdout)[-300:]}"}
+            continue
+        k = int(m.group(1))
+        if len(order) < k:
+            out[cfg] = {"error": f"ncu saw {len(order)} kernels, expected >= {k}"}
+            continue
+        out[cfg] = [{"kernel": rows[i]["kernel"][:160],
+                     "bytes": int(rows[i].get("dram__bytes_read.sum", 0) + rows[i].get("dram__bytes_write.sum", 0)),
+                     "ncu_us": round(rows[i].get("gpu__time_duration.sum", 0) / 1e3, 2)} for i in order[-k:]]
+    return out
 
 
 # --------------------------------------------------------- reference (CPU)
@@ -666,7 +843,7 @@ def ref_cpu_jobs(cfg: str, sample: int, threads: int):
     C3's pack / unpack time encode_scalar + the shipped pack and the shipped
     unpack + decode_scalar (the reference's own conversion path; its
     transpose output is wrong -- SURVEY.md §0.4 -- but its cost is what a
-    reference user pays)."""
+    reference user pays).  Labels equal the GPU jobs' labels."""
     import numpy as np
     sys.path.insert(0, str(ROOT / "oracle"))
     import oracle as O
@@ -706,23 +883,17 @@ def ref_cpu_jobs(cfg: str, sample: int, threads: int):
         arith("mul", "mul", fmt, encs)
         jobs.append(("unpack_f32", lambda: R.ref_unpack_f32_path(
             pa.ctypes.data_as(O._u32p), sample, fl_out.ctypes.data_as(O._f32p), 5, 10, threads)))
-    elif cfg == "C4":
-        for (e, s) in W.CONFIGS["C4"]["fmts"]:
+    elif cfg in ("C4", "X1"):
+        for (e, s) in (C4_FMTS if cfg == "C4" else X1_FMTS):
             fmt = (e, s) + MODE
             encs = [W.c4_encodings(e, s, 0, sample, sd, "cpu").numpy().astype(np.uint64)
                     for sd in (1, 2)]
-            arith(f"add_1/{e}/{s}", "add", fmt, encs)
-            arith(f"mul_1/{e}/{s}", "mul", fmt, encs)
+            for op in (("add", "mul") if cfg == "C4" else ("div",)):
+                arith(f"{op}_1/{e}/{s}", op, fmt, encs)
     elif cfg == "C5":
         fmt = (6, 9) + MODE
         encs = [O.encode_f32(fmt, W.c5_floats(0, sample, sd, "cpu").numpy()) for sd in (1, 2, 3)]
         arith("mul_add", "mul_add", fmt, encs)
-    elif cfg == "X1":
-        for (e, s) in X1_FMTS:
-            fmt = (e, s) + MODE
-            encs = [W.c4_encodings(e, s, 0, sample, sd, "cpu").numpy().astype(np.uint64)
-                    for sd in (1, 2)]
-            arith(f"div_1/{e}/{s}", "div", fmt, encs)
     elif cfg in ("X3", "X3u"):
         fmt = (5, 10) + MODE
         planes = [O.pack_planes(W.c4_encodings(5, 10, 0, sample, sd, "cpu").numpy().astype(np.uint64), 16)
@@ -761,16 +932,27 @@ def ref_cpu_jobs(cfg: str, sample: int, threads: int):
     return jobs, O.ref_lib_path().name
 
 
-REF_SAMPLE = {"C1": 1 << 22, "C2": 1 << 22, "C3": 1 << 20, "C4": 1 << 20, "C5": 1 << 20,
-              "X1": 1 << 20, "X2": 1 << 20, "X3": 1 << 20, "X3u": 1 << 20}
+# CPU sample per config (elements per op per timed step).  C5 follows
+# a 2^26 slice of the 2^32 workload gives the rate; the
+# other configs run a bounded slice of their per-GPU N so one step stays
+# well under a second on ~16 host threads.
+REF_SAMPLE = {"C1": 1 << 24, "C2": 1 << 26, "C3": 1 << 24, "C4": 1 << 24, "C5": 1 << 26,
+              "X1": 1 << 22, "X2": 1 << 22, "X3": 1 << 22, "X3u": 1 << 22}
 
 
-def ref_cpu_run(cfg: str, sample: int, reps: int | None = None, seconds: float = 10.0,
-                threads: int | None = None) -> dict:
-    """Time the reference's CPU path: whole steps (every job once) repeated
-    `reps` times or for ~`seconds`; rate from the best step."""
+def ref_cpu_run(cfg: str, sample: int, seconds: float = 10.0, min_reps: int = 1,
+                warmup: int = 1, threads: int | None = None, jobs=None) -> dict:
+    """Time the reference's CPU path: whole steps (every job once), `warmup`
+    untimed, then repeated for at least `seconds` and `min_reps` steps; the
+    rate comes from the best step, the median alongside.  Both arms call this
+    same function with the same sample, so their CPU figures agree."""
     threads = threads or os.cpu_count() or 1
-    jobs, libname = ref_cpu_jobs(cfg, sample, threads)
+    if jobs is None:
+        jobs = ref_cpu_jobs(cfg, sample, threads)
+    jobs, libname = jobs
+    for _ in range(warmup):
+        for _, fn in jobs:
+            fn()
     times, per_job = [], {lbl: [] for lbl, _ in jobs}
     t_start = time.perf_counter()
     while True:
@@ -780,15 +962,16 @@ def ref_cpu_run(cfg: str, sample: int, reps: int | None = None, seconds: float =
             fn()
             per_job[lbl].append(time.perf_counter() - tj)
         times.append(time.perf_counter() - t)
-        if reps is not None and len(times) >= reps:
+        if len(times) >= min_reps and time.perf_counter() - t_start >= seconds:
             break
-        if reps is None and time.perf_counter() - t_start >= seconds:
-            break
-    best = min(times)
-    return {"value": len(jobs) * sample / best / 1e9, "cores": threads, "reps": len(times),
-            "best_s": best, "median_s": statistics.median(times), "lib": libname,
+    best, med = min(times), statistics.median(times)
+    return {"value": len(jobs) * sample / best / 1e9, "value_median": len(jobs) * sample / med / 1e9,
+            "cores": threads, "reps": len(times), "best_s": best, "median_s": med, "lib": libname,
+            "seconds": round(time.perf_counter() - t_start, 2),
             "ops": [lbl for lbl, _ in jobs], "sample": sample,
-            "per_op_gelems": {lbl: round(sample / min(v) / 1e9, 5) for lbl, v in per_job.items()}}
+            "per_op_gelems": {lbl: round(sample / min(v) / 1e9, 5) for lbl, v in per_job.items()},
+            "per_op_gelems_median": {lbl: round(sample / statistics.median(v) / 1e9, 5)
+                                     for lbl, v in per_job.items()}}
 
 
 def cpu_model() -> str:
@@ -801,6 +984,22 @@ def cpu_model() -> str:
     return "unknown"
 
 
+def cpu_block(cfg: str, seconds: float, min_reps: int = 1, warmup: int = 1) -> dict:
+    """cpu_baseline of `cfg`: all host threads for >= `seconds` (best and
+    median), plus a 1-thread run of the same sample for the scaling check."""
+    sample = REF_SAMPLE[cfg]
+    cb = ref_cpu_run(cfg, sample, seconds=seconds, min_reps=min_reps, warmup=warmup)
+    c1 = ref_cpu_run(cfg, sample, seconds=0.0, min_reps=2, warmup=0, threads=1)
+    return {"value": round(cb["value"], 4), "unit": UNIT, "cores": cb["cores"], "kind": "reference",
+            "value_median": round(cb["value_median"], 4),
+            "sample": f"{sample} elements x {cb['ops']} per step, {cb['reps']} steps over "
+                      f"{cb['seconds']} s (value = best step, value_median = median step), "
+                      f"lane<1024>, {cb['cores']} threads, {cpu_model()}, {cb['lib']}",
+            "per_op": cb["per_op_gelems"], "per_op_median": cb["per_op_gelems_median"],
+            "nproc": os.cpu_count(), "value_1_thread": round(c1["value"], 4),
+            "thread_scaling": round(cb["value"] / c1["value"], 2)}
+
+
 CONFIG_TEXT = {
     "C1": ("C1: fp8 1/4/3 elementwise add, N=2^24 per GPU; float32 U[-16,16] -> encode_scalar "
            "-> planes", "1/4/3", 1 << 24),
@@ -810,8 +1009,8 @@ CONFIG_TEXT = {
            "each timed separately; float32 normal(0,100) clamped to +-65504", "1/5/10", 1 << 28),
     "C4": ("C4: add + mul sweep over 1/3/2, 1/5/3, 1/5/7, 1/8/7, 1/8/15, N=2^28 per GPU per "
            "format; uniform finite bit patterns", "sweep", 1 << 28),
-    "C5": ("C5: 1/6/9 z=round(round(a*b)+c) fused, N=2^32 total split evenly over the GPUs; "
-           "float32 sign x 2^U[-10,9] x U[1,2) -> encode_scalar", "1/6/9", None),
+    "C5": ("C5: 1/6/9 z=round(round(a*b)+c) fused (one mul_add kernel), N=2^32 total split evenly "
+           "over the GPUs; float32 sign x 2^U[-10,9] x U[1,2) -> encode_scalar", "1/6/9", None),
     "X1": ("X1 (secondary, not a BASELINE config): div sweep over 1/3/2, 1/4/3, 1/5/3, 1/5/7, 1/5/10, "
            "1/8/7, 1/8/15, N=2^28 per GPU per format; C4 operand distribution", "sweep", 1 << 28),
     "X2": ("X2 (secondary, not a BASELINE config): 1/5/10 add and mul with float32 in / float32 out "
@@ -823,6 +1022,21 @@ CONFIG_TEXT = {
             "(mul, mul, add through HBM), N=2^28 per GPU; uniform finite operands", "1/5/10", 1 << 28),
 }
 
+OPS_OF = {
+    "C1": ["add"], "C2": ["mul", "sub"], "C3": ["pack_f32", "add", "mul", "unpack_f32"],
+    "C4": [f"{op}_1/{e}/{s}" for (e, s) in C4_FMTS for op in ("add", "mul")],
+    "C5": ["mul_add"], "X1": [f"div_1/{e}/{s}" for (e, s) in X1_FMTS],
+    "X2": ["add_f32", "mul_f32"], "X3": ["a*b+c*d"], "X3u": ["mul a*b", "mul c*d", "add"],
+}
+
+
+def label_fmt_op(cfg: str, lbl: str) -> tuple[str, str]:
+    """("1/8/15", "mul") of a job label such as "mul_1/8/15" or C5's "mul_add"."""
+    if "_1/" in lbl:
+        op, fmt = lbl.split("_1/")
+        return "1/" + fmt, op
+    return CONFIG_TEXT[cfg][1], lbl
+
 
 def scaling_of(cfg: str) -> str:
     """C5 splits a fixed 2^32 elements over the GPUs (strong); every other
@@ -830,230 +1044,370 @@ def scaling_of(cfg: str) -> str:
     return "strong" if cfg == "C5" else "weak"
 
 
-def config_block(cfg: str, world: int, jobs=None) -> dict:
+def config_block(cfg: str, world: int, sweep: list[str] | None = None) -> dict:
+    """Identical for both arms (same workload, ops and sizes)."""
     text, fmt, n = CONFIG_TEXT[cfg]
     d = {"workload": text, "format": fmt, "rounding": "rn" if MODE[0] else "rz",
          "subnormals": "ftz" if MODE[1] else "gradual",
          "parallelism": f"dp{world} (independent block-aligned shards, no collective)",
-         "l2": "inputs larger than L2: operand sets rotate step by step so each set is reused "
-               "only after >= 2x L2 (126 MB) of other traffic; outputs rotate over two buffers"}
+         "ops_per_step": OPS_OF[cfg],
+         "l2": "inputs larger than L2 (no flush): no operand set is re-read before >= 2x L2 (252 MiB) "
+               "of other reads and writes -- sets rotate launch by launch where one set is smaller "
+               "(measured distance: roofline.step.l2_reuse_distance_bytes); outputs rotate over two "
+               "buffers"}
     if n:
         d["n_per_gpu"] = n
     else:
         d["n_total"] = 1 << 32
-    if jobs is not None:
-        d["ops_per_step"] = [j.label for j in jobs]
+        d["n_per_gpu"] = (1 << 32) // world
+    if sweep:
+        d["per_format_configs"] = sweep
     return d
 
 
 # ------------------------------------------------------------------- arms
-def main_reference(args) -> None:
-    world, rank, local = env_dist()
-    if rank != 0:
-        return
-    for cfg in args.configs:
-        sample = REF_SAMPLE[cfg]
-        r = ref_cpu_run(cfg, sample, reps=args.warmup)  # warm-up steps
-        r = ref_cpu_run(cfg, sample, reps=args.steps)
-        r1 = ref_cpu_run(cfg, sample, reps=3, threads=1)  # thread-scaling check
-        value = r["value"]
-        line = {
-            "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": UNIT,
-            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": round(r["median_s"] * 1e3, 3), "higher_is_better": True,
-            "scaling": scaling_of(cfg), "vs_baseline": None, "dtype": "u64 lanes (lane<1024> bitslice)",
-            "data": "synthetic (seeded SplitMix64 operands; BASELINE.json configs)",
-            "config": config_block(cfg, world),
-            "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": r["cores"],
-                             "kind": "reference",
-                             "sample": f"{r['sample']} elements x {r['ops']} per step, "
-                                       f"lane<1024>, {r['cores']} threads, {cpu_model()}, "
-                                       f"{r['lib']}",
-                             "per_op": r["per_op_gelems"], "nproc": os.cpu_count(),
-                             "value_1_thread": round(r1["value"], 4),
-                             "thread_scaling": round(value / r1["value"], 2)},
-            "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0},
-        }
-        print(json.dumps(line), flush=True)
+def op_entry(j, ms: float, n_total: int, peaks: dict, peak_lop3: dict | None, clocks: dict) -> dict:
+    """One kernel on both roofline legs (per GPU) and which one binds."""
+    dur = ms * 1e-3
+    ach = j.algo_bytes / dur / 1e9
+    ent = {"ms": round(ms, 4), "gelem_s": round(n_total / dur / 1e9, 2),
+           "gelem_s_per_gpu": round(j.n / dur / 1e9, 2),
+           "hbm_gbs": round(ach, 1), "hbm_frac": round(ach / peaks["hbm_gbs"], 4),
+           "algorithmic_bytes": int(j.algo_bytes), "bound": "hbm",
+           "frac": round(ach / peaks["hbm_gbs"], 4)}
+    e, s = j.spec.exp_bits, j.spec.sig_bits
+    chain_ops = ([{"+": "add", "-": "sub", "*": "mul", "/": "div"}[ch]
+                  for ch in j.op.split(":", 1)[1] if ch in "+-*/"]
+                 if j.op.startswith("chain:") else None)
+    if j.op in OPNAMES or chain_ops:
+        rn, ftz = int(j.spec.rounding), int(j.spec.subnormals)
+        if chain_ops:
+            parts = [sass_lop3((e, s), rn, ftz, OPNAMES[o]) for o in chain_ops]
+            lop3 = None if None in parts else sum(parts)
+        else:
+            lop3 = sass_lop3((e, s), rn, ftz, OPNAMES[j.op])
+        if lop3 is not None and peak_lop3:
+            pe = lop3 / 32.0
+            hbm_t = j.algo_bytes / (peaks["hbm_gbs"] * 1e9)
+            logic_t = pe * j.n / peak_lop3["burst"]
+            lf = logic_t / dur
+            ent.update({"lop3_per_elem": round(pe, 3),
+                        "tlop3_s": round(pe * j.n / dur / 1e12, 3),
+                        "logic_frac": round(lf, 4)})
+            mhz, pmhz = clocks.get("sm_mhz"), peak_lop3.get("sustained_sm_mhz")
+            if mhz and pmhz:  # against the LOP3 rate of the clock the step ran at
+                ent["logic_frac_at_load_clock"] = round(pe * j.n / (peak_lop3["sustained"] * mhz / pmhz) / dur, 4)
+            if logic_t > hbm_t:
+                ent["bound"], ent["frac"] = "logic", round(lf, 4)
+    return ent
+
+
+def roofline_block(jd, ent: dict, peaks: dict, peak_lop3: dict | None, traffic) -> dict:
+    """The dominant kernel on its binding leg: bound / achieved / peak / unit /
+    frac recomputable from the line (logic: LOP3 per element x elements per
+    launch / launch time vs the probe's measured LOP3 rate)."""
+    dur = ent["ms"] * 1e-3
+    hbm = {"achieved": ent["hbm_gbs"], "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": ent["hbm_frac"],
+           "peak_source": peaks["source"], "algorithmic_bytes_per_launch": ent["algorithmic_bytes"]}
+    r = {"kernel": f"{jd.label} ({jd.fmt} {mode_text()})", "launch_ms": ent["ms"],
+         "elements_per_launch": jd.n}
+    logic = None
+    if "lop3_per_elem" in ent and peak_lop3:
+        logic = {"achieved": round(ent["lop3_per_elem"] * jd.n / dur / 1e12, 4),
+                 "peak": round(peak_lop3["burst"] / 1e12, 4), "unit": "TLOP3/s", "frac": ent["logic_frac"],
+                 "lop3_per_elem": ent["lop3_per_elem"],
+                 "lop3_source": "SASS LOP3 count of the shipped kernel (cuobjdump of the loaded "
+                                "libbfpgpu.so) / 32 elements per unit",
+                 "peak_source": "bfp_probe_lop3 measured in this run (burst; 148 SM x 64/clk x f_SM)",
+                 "peak_sustained": round(peak_lop3["sustained"] / 1e12, 4),
+                 "peak_sustained_sm_mhz": peak_lop3["sustained_sm_mhz"]}
+        if "logic_frac_at_load_clock" in ent:
+            logic["frac_at_load_clock"] = ent["logic_frac_at_load_clock"]
+    lead = logic if ent["bound"] == "logic" and logic else hbm
+    r.update({"bound": ent["bound"], "achieved": lead["achieved"], "peak": lead["peak"],
+              "unit": lead["unit"], "frac": lead["frac"]})
+    r["traffic"] = traffic.get("bytes") if isinstance(traffic, dict) else None
+    if isinstance(traffic, dict):
+        r["traffic_over_algorithmic"] = round(traffic["bytes"] / ent["algorithmic_bytes"], 4) \
+            if traffic.get("bytes") else None
+        r["traffic_source"] = traffic.get("source")
+    r["legs"] = {"hbm": hbm}
+    if logic:
+        r["legs"]["logic"] = logic
+    return r
+
+
+def measure_config(cfg: str, args, D: Dist, probes: dict) -> dict:
+    """Device timing (+ e2e, + probes once) of one config on this rank."""
+    import torch
+    log(f"device timing {cfg}")
+    res = run_device(cfg, args.steps, args.warmup, D)
+    if clocks_rejected(res["clocks"]):  # re-measure once
+        log("clocks rejected; re-measuring")
+        res = run_device(cfg, args.steps, args.warmup, D, jobs=res["jobs"])
+    jobs = res["jobs"]
+    log(f"device done: {res['ms_total'] / args.steps:.4f} ms/step (max over ranks)")
+    res["n_total"] = [int(v) for v in D.reduce([float(j.n) for j in jobs], op="sum")]
+    res["l2_reuse"] = l2_reuse_distance(jobs)
+    e2e = None
+    if not args.no_e2e and (cfg == args.configs[0] or args.e2e_all):
+        log("e2e (host buffers through the C ABI)")
+        e2e = run_e2e(jobs, args.steps, D)
+    if "lop3" not in probes:
+        log("lop3 / hbm probes")
+        probes["lop3"] = lop3_peak(D.dev)
+        probes["hbm_2r1w"] = hbm_2r1w_probe(D.dev)
+    if e2e is not None and "pcie" not in probes:
+        probes["pcie"] = pcie_probe(D.dev)
+    res["e2e"] = e2e
+    res["jobs"] = None
+    res["job_meta"] = [JobMeta(j) for j in jobs]  # the operands are released here
+    del jobs
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    return res
+
+
+def build_line(cfg: str, res: dict, args, D: Dist, probes: dict, traffic: dict) -> dict:
+    peaks = measured_peaks()
+    jobs = res["job_meta"]
+    ms_step = res["ms_total"] / args.steps
+    value = sum(res["n_total"]) / (ms_step * 1e-3) / 1e9
+    per_op, per_format = {}, {}
+    tr = traffic.get(cfg)
+    for k, (j, ms, nt) in enumerate(zip(jobs, res["kern_ms"], res["n_total"])):
+        ent = op_entry(j, ms, nt, peaks, probes.get("lop3"), res["clocks"])
+        if isinstance(tr, list) and k < len(tr):
+            ent["traffic"] = tr[k]["bytes"]
+            ent["traffic_over_algorithmic"] = round(tr[k]["bytes"] / j.algo_bytes, 4)
+        per_op[j.label] = ent
+        per_format.setdefault(j.fmt, {})[j.op] = {
+            key: ent[key] for key in ("gelem_s", "bound", "frac", "ms", "hbm_frac", "logic_frac",
+                                      "logic_frac_at_load_clock", "lop3_per_elem", "traffic_over_algorithmic")
+            if key in ent}
+        per_format[j.fmt][j.op]["config"] = cfg
+    k_dom = max(range(len(jobs)), key=lambda k: res["kern_ms"][k])
+    jd = jobs[k_dom]
+    t_dom = None
+    if isinstance(tr, list) and k_dom < len(tr):
+        t_dom = {"bytes": tr[k_dom]["bytes"], "source": f"ncu dram__bytes_read.sum + dram__bytes_write.sum "
+                 f"of this kernel, measured by an ncu subprocess in this run ({tr[k_dom]['kernel'][:60]}...)"}
+    elif isinstance(tr, dict):
+        t_dom = {"bytes": None, "source": f"not measured: {tr.get('error')}"}
+    roof = roofline_block(jd, per_op[jd.label], peaks, probes.get("lop3"), t_dom)
+    roof["hbm_2r1w_probe_gbs"] = probes.get("hbm_2r1w")
+    roof["per_op"] = per_op
+    step_bytes = sum(j.algo_bytes for j in jobs)
+    step_gbs = step_bytes / (ms_step * 1e-3) / 1e9
+    # self-check: inputs never stay in L2 between uses, so no step or kernel
+    # can beat the HBM copy peak by much; a faster figure means broken timing
+    for j, ms in zip(jobs, res["kern_ms"]):
+        if j.algo_bytes / (ms * 1e-3) / 1e9 > 1.15 * peaks["hbm_gbs"]:
+            raise RuntimeError(f"{cfg}:{j.label}: {ms} ms per launch is faster than HBM allows")
+    if step_gbs > 1.15 * peaks["hbm_gbs"]:
+        raise RuntimeError(f"{cfg}: step time {ms_step} ms is faster than HBM allows")
+    roof["step"] = {"algorithmic_bytes_per_gpu": int(step_bytes), "ms": round(ms_step, 5),
+                    "achieved_gbs_per_gpu": round(step_gbs, 1),
+                    "hbm_frac": round(step_gbs / peaks["hbm_gbs"], 4),
+                    "note": "whole step: K steps captured once into a CUDA graph through the C ABI and "
+                            "replayed (consecutive kernels overlap through programmatic dependent "
+                            "launch); per-kernel figures come from one graph per kernel holding its K "
+                            "launches; all times max over ranks",
+                    "ms_per_step_eager": round(res["ms_total_eager"] / args.steps, 5)}
+    pw = res["clocks"].get("power_w")
+    if pw:  # board energy per result element at the sampled draw (logic kernels run power-capped)
+        roof["step"]["pj_per_elem"] = round(pw * ms_step * 1e-3 / (sum(res["n_total"]) / D.world) * 1e12, 1)
+    cfgb = config_block(cfg, D.world)
+    reuse = res["l2_reuse"]
+    roof["step"]["l2_reuse_distance_bytes"] = reuse
+    if 0 <= reuse < 2 * L2_BYTES:
+        raise RuntimeError(f"{cfg}: L2 reuse distance {reuse} B < 2x L2")
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": D.world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 5),
+        "higher_is_better": True, "scaling": scaling_of(cfg), "vs_baseline": None,
+        "dtype": "u32 (bitslice words)",
+        "data": "synthetic (seeded SplitMix64 operands; BASELINE.json configs)",
+        "config": cfgb, "roofline": roof, "per_format": per_format,
+        "clocks": res["clocks"], "gpu_launches": res["launches"],
+    }
+    e2e = res.get("e2e")
+    if e2e is not None:
+        pcie = probes["pcie"]
+        bound_s = max(e2e["h2d"] / (pcie["h2d_gbs"] * 1e9), e2e["d2h"] / (pcie["d2h_gbs"] * 1e9),
+                      (e2e["h2d"] + e2e["d2h"]) / (pcie["bidir_gbs"] * 1e9))
+        line["e2e"] = {"value": round(e2e["elems"] * D.world / e2e["s_per_step"] / 1e9, 3),
+                       "unit": UNIT, "h2d_bytes_per_step": int(e2e["h2d"]),
+                       "d2h_bytes_per_step": int(e2e["d2h"]),
+                       "pcie_measured": pcie, "frac_of_pcie_bound": round(bound_s / e2e["s_per_step"], 4),
+                       "path": "C ABI host entry points (bfp_arith_host_batch / bfp_pack_f32_host / "
+                               "bfp_unpack_f32_host) on pinned host buffers: inputs copied H2D in chunk "
+                               "order on one stream, kernels on a second, results copied back (or "
+                               "written in place over PCIe for small calls); per-GPU bytes",
+                       "steps": e2e["steps"]}
+    return line
 
 
 def main_ours(args) -> None:
     import torch
-    import torch.distributed as dist
-
-    world, rank, local = env_dist()
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    log = (lambda m: print(f"[bench r{rank}] {m}", file=sys.stderr, flush=True))
-    peak_lop3 = None
-    hbm_2r1w = None
+    D = Dist("nccl")
+    torch.cuda.set_device(D.dev)
+    info = {"rank": D.rank, "local_rank": D.local, "host": socket.gethostname(),
+            "device": torch.cuda.get_device_name(D.dev),
+            "pci_bus_id": getattr(torch.cuda.get_device_properties(D.dev), "pci_bus_id", None)}
+    probes: dict = {}
+    results = []
     for cfg in args.configs:
-        log(f"device timing {cfg}")
-        res = run_device(cfg, args.steps, args.warmup, world, rank, local)
-        if clocks_rejected(res["clocks"]):  # re-measure once
-            log("clocks rejected; re-measuring")
-            res = run_device(cfg, args.steps, args.warmup, world, rank, local, jobs=res["jobs"])
-        jobs = res["jobs"]
-        log(f"device done: {res['ms_total'] / args.steps:.4f} ms/step; e2e")
-        e2e = run_e2e(cfg, jobs, args.steps, world, rank, local) if not args.no_e2e else None
-        if peak_lop3 is None and rank == 0:
-            log("lop3 probe")
-            peak_lop3 = lop3_peak(local)
-            hbm_2r1w = hbm_2r1w_probe(local)
-
-        total_elems = sum(j.n for j in jobs) * world
-        ms_step = res["ms_total"] / args.steps
-        value = total_elems / (ms_step * 1e-3) / 1e9
-        peaks = measured_peaks()
-        per_op = {}
-        roofs = []
-        tfile = ROOT / "profiles" / "ncu_traffic.json"
-        tmap = json.loads(tfile.read_text()) if tfile.exists() else {}
-        tsuf = "" if MODE == (1, 0) else f":{mode_text()}"
-        for j, ms in zip(jobs, res["kern_ms"]):
-            dur = ms * 1e-3
-            ach = j.algo_bytes / dur / 1e9
-            e, s = j.spec.exp_bits, j.spec.sig_bits
-            ent = {"ms": round(ms, 4), "gelem_s": round(j.n / dur / 1e9, 2),
-                   "hbm_gbs": round(ach, 1), "hbm_frac": round(ach / peaks["hbm_gbs"], 4)}
-            chain_ops = ([{"+": "add", "-": "sub", "*": "mul", "/": "div"}[ch]
-                          for ch in j.op.split(":", 1)[1] if ch in "+-*/"]
-                         if j.op.startswith("chain:") else None)
-            if j.op in OPNAMES or chain_ops:
-                if chain_ops:
-                    parts = [sass_lop3((e, s), int(j.spec.rounding), int(j.spec.subnormals), OPNAMES[o])
-                             for o in chain_ops]
-                    lop3 = None if None in parts else sum(parts)
-                else:
-                    lop3 = sass_lop3((e, s), int(j.spec.rounding), int(j.spec.subnormals), OPNAMES[j.op])
-                if lop3 is not None and peak_lop3:
-                    pe = lop3 / 32.0
-                    hbm_t = j.algo_bytes / (peaks["hbm_gbs"] * 1e9)
-                    logic_t = pe * j.n / peak_lop3["burst"]
-                    ent.update({"lop3_per_elem": round(pe, 3),
-                                "logic_frac": round(logic_t / dur, 4),
-                                "logic_frac_at_load_clock": load_clock_frac(pe * j.n, dur, peak_lop3,
-                                                                            res["clocks"]),
-                                "binding": "logic" if logic_t > hbm_t else "hbm",
-                                "frac_of_binding": round(max(hbm_t, logic_t) / dur, 4)})
-            tr = tmap.get(f"{cfg}:{j.label}{tsuf}")
-            if isinstance(tr, dict):
-                ent["ncu"] = {k: v for k, v in tr.items() if k != "bytes"}
-                tr = tr.get("bytes")
-            if tr is not None:
-                ent["traffic"] = tr
-                ent["traffic_over_algorithmic"] = round(tr / j.algo_bytes, 3)
-            per_op[j.label] = ent
-            roofs.append((ms, j, ach))
-        ms_dom, jd, ach = max(roofs, key=lambda r: r[0])
-        traffic = tmap.get(f"{cfg}:{jd.label}{tsuf}")
-        if isinstance(traffic, dict):
-            traffic = traffic.get("bytes")
-        roof = {"bound": "hbm", "kernel": f"{jd.label} (1/{jd.spec.exp_bits}/{jd.spec.sig_bits} {mode_text()})",
-                "achieved": round(ach, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                "frac": round(ach / peaks["hbm_gbs"], 4), "traffic": traffic,
-                "peak_source": peaks["source"],
-                "hbm_2r1w_probe_gbs": hbm_2r1w,
-                "algorithmic_bytes_per_launch": int(jd.algo_bytes),
-                "launch_ms": round(ms_dom, 4), "per_op": per_op}
-        if peak_lop3:
-            roof["peak_lop3_per_s_measured"] = peak_lop3["burst"]
-            roof["peak_lop3_per_s_sustained"] = peak_lop3["sustained"]
-            roof["peak_lop3_sustained_sm_mhz"] = peak_lop3["sustained_sm_mhz"]
-        step_bytes = sum(j.algo_bytes for j in jobs)
-        step_gbs = step_bytes / (ms_step * 1e-3) / 1e9
-        # self-check: inputs rotate through > 2x L2, so no step or kernel can
-        # beat the HBM copy peak; a faster figure means the timing is broken
-        for j, ms in zip(jobs, res["kern_ms"]):
-            if j.algo_bytes / (ms * 1e-3) / 1e9 > 1.1 * peaks["hbm_gbs"] * world:
-                raise RuntimeError(f"{cfg}:{j.label}: {ms} ms per launch is faster than HBM allows")
-        if step_gbs > 1.1 * peaks["hbm_gbs"] * world:
-            raise RuntimeError(f"{cfg}: step time {ms_step} ms is faster than HBM allows")
-        roof["step"] = {"algorithmic_bytes": int(step_bytes), "ms": round(ms_step, 5),
-                        "achieved_gbs": round(step_gbs, 1),
-                        "frac": round(step_gbs / peaks["hbm_gbs"], 4),
-                        "note": "whole step: K steps captured once into a CUDA graph through the "
-                                "C ABI and replayed (consecutive kernels overlap through "
-                                "programmatic dependent launch); per-kernel figures above come "
-                                "from one graph per kernel holding its K launches",
-                        "ms_per_step_eager": round(res["ms_total_eager"] / args.steps, 5)}
-        pw = res["clocks"].get("power_w")
-        if pw:  # board energy per result element at the sampled draw (the logic kernels run power-capped)
-            roof["step"]["pj_per_elem"] = round(pw * ms_step * 1e-3 / (total_elems / world) * 1e12, 1)
-        dd = per_op[jd.label]
-        if "binding" in dd:
-            roof["binding_leg"] = dd["binding"]
-            roof["frac_of_binding"] = dd["frac_of_binding"]
-        line = {
-            "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 5),
-            "higher_is_better": True, "scaling": scaling_of(cfg), "vs_baseline": None,
-            "dtype": "u32 (bitslice words)",
-            "data": "synthetic (seeded SplitMix64 operands; BASELINE.json configs)",
-            "config": config_block(cfg, world, jobs),
-            "roofline": roof,
-            "clocks": res["clocks"],
-            "gpu_launches": res["launches"],
-        }
-        if e2e is not None:
-            pcie = pcie_probe(local)
-            # copy-only time of the step's traffic at the measured link rates
-            bound_s = max(e2e["h2d"] / (pcie["h2d_gbs"] * 1e9), e2e["d2h"] / (pcie["d2h_gbs"] * 1e9),
-                          (e2e["h2d"] + e2e["d2h"]) / (pcie["bidir_gbs"] * 1e9))
-            line["e2e"] = {"value": round(e2e["elems"] * world / e2e["s_per_step"] / 1e9, 3),
-                           "pcie_measured": pcie,
-                           "frac_of_pcie_bound": round(bound_s / e2e["s_per_step"], 4),
-                           "unit": UNIT, "h2d_bytes_per_step": int(e2e["h2d"]),
-                           "d2h_bytes_per_step": int(e2e["d2h"]),
-                           "path": "C ABI host entry points (bfp_arith_host_batch / "
-                                   "bfp_pack_f32_host / bfp_unpack_f32_host: pinned host buffers; "
-                                   "inputs copied H2D in chunk order on one stream, kernels on a "
-                                   "second write each chunk's results in place into the pinned "
-                                   "host outputs over PCIe; ops sharing operands copy them once)",
-                           "steps": e2e["steps"]}
-        if rank == 0 and world == 1 and not args.no_cpu_baseline:
-            log("cpu baseline")
-            cb = ref_cpu_run(cfg, REF_SAMPLE[cfg], seconds=args.cpu_seconds)
-            c1 = ref_cpu_run(cfg, REF_SAMPLE[cfg], reps=3, threads=1)  # thread-scaling check
-            line["cpu_baseline"] = {
-                "value": round(cb["value"], 4), "unit": UNIT, "cores": cb["cores"],
-                "kind": "reference",
-                "sample": f"{cb['sample']} elements x {cb['ops']} per step, best of {cb['reps']} "
-                          f"steps (~{args.cpu_seconds:.0f} s), lane<1024>, {cb['cores']} threads, "
-                          f"{cpu_model()}, {cb['lib']}",
-                "per_op": cb["per_op_gelems"], "nproc": os.cpu_count(),
-                "value_1_thread": round(c1["value"], 4),
-                "thread_scaling": round(cb["value"] / c1["value"], 2)}
-        del jobs, res
+        res = measure_config(cfg, args, D, probes)
+        lo, hi = config_n(cfg, D.rank, D.world)
+        res["rank_info"] = D.gather(dict(info, shard=[lo, hi], ms_per_step=round(
+            res["ms_total_rank"] / args.steps, 5)))
+        results.append((cfg, res))
         torch.cuda.empty_cache()
-        if rank == 0:
+    traffic = {}
+    if not args.no_ncu:
+        if D.rank == 0:
+            log("DRAM traffic: ncu subprocess over tools/profile_kernels.py")
+            traffic = ncu_traffic(list(args.configs), D.local)
+        D.barrier()
+    lines = [build_line(cfg, res, args, D, probes, traffic) for cfg, res in results]
+    for line, (cfg, res) in zip(lines, results):
+        line["ranks"] = res["rank_info"]
+    if D.rank == 0 and D.world == 1 and not args.no_cpu_baseline:
+        for line, (cfg, _) in zip(lines, results):
+            if cfg in REF_SAMPLE:
+                log(f"cpu baseline {cfg}")
+                cb = line["cpu_baseline"] = cpu_block(cfg, args.cpu_seconds)
+                for lbl, v in cb["per_op"].items():
+                    fmt, op = label_fmt_op(cfg, lbl)
+                    if op in line["per_format"].get(fmt, {}):
+                        line["per_format"][fmt][op]["cpu_gelem_s"] = v
+    if args.headline:  # one line: the first config, the others folded into per_format
+        head = lines[0]
+        for line, (cfg, _) in zip(lines[1:], results[1:]):
+            for fmt, ops in line["per_format"].items():
+                head["per_format"].setdefault(fmt, {}).update(ops)
+            head.setdefault("secondary", {})[cfg] = {
+                "value": line["value"], "ms_per_step": line["ms_per_step"], "clocks": line["clocks"],
+                "roofline": {k: line["roofline"][k] for k in ("kernel", "bound", "achieved", "peak", "unit",
+                                                             "frac", "traffic")},
+                "config": line["config"]}
+        head["config"]["per_format_configs"] = [cfg for cfg, _ in results]
+        lines = [head]
+    if D.rank == 0:
+        for line in lines:
             print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
+    D.close()
+
+
+def main_reference(args) -> None:
+    """The reference's own CPU implementation (oracle/_ref) on this host's
+    cores, same config / metric / unit; rank 0 only (other ranks exit 0)."""
+    world, rank, _ = env_dist()
+    if rank != 0:
+        return
+    lines = []
+    for cfg in args.configs:
+        sample = REF_SAMPLE[cfg]
+        log(f"reference {cfg}: {sample} elements per op per step")
+        cb = cpu_block(cfg, args.cpu_seconds, min_reps=args.steps, warmup=args.warmup)
+        value = cb["value"]
+        per_format = {}
+        for lbl, v in cb["per_op"].items():
+            fmt, op = label_fmt_op(cfg, lbl)
+            per_format.setdefault(fmt, {})[op] = {"gelem_s": v, "gelem_s_median": cb["per_op_median"][lbl],
+                                                  "config": cfg}
+        lines.append({
+            "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": UNIT,
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(len(cb["per_op"]) * sample / (value * 1e9) * 1e3, 3),
+            "higher_is_better": True, "scaling": scaling_of(cfg), "vs_baseline": None,
+            "dtype": "u64 lanes (lane<1024> bitslice)",
+            "data": "synthetic (seeded SplitMix64 operands; BASELINE.json configs)",
+            "config": config_block(cfg, world), "per_format": per_format,
+            "cpu_baseline": cb,
+            "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        })
+    if args.headline:
+        head = lines[0]
+        for line in lines[1:]:
+            for fmt, ops in line["per_format"].items():
+                head["per_format"].setdefault(fmt, {}).update(ops)
+        head["config"]["per_format_configs"] = list(args.configs)
+        lines = [head]
+    for line in lines:
+        print(json.dumps(line), flush=True)
+
+
+def main_dry_run(args) -> None:
+    """gloo on the CPU: the launcher, shard ranges, barrier + max-over-ranks
+    reduction and rank-0-only output of the real path, with a stand-in step
+    (a SplitMix64 pass over a slice of the rank's shard plus a rank-dependent
+    delay, so the maximum is the slowest rank)."""
+    import torch
+    from paper_1602_04716_b200 import workloads as W
+    D = Dist("gloo")
+    cfg = args.configs[0]
+    lo, hi = config_n(cfg, D.rank, D.world)
+    ts = []
+    for i in range(args.warmup + args.steps):
+        D.barrier()
+        t = time.perf_counter()
+        W.splitmix64(torch.arange(lo, min(hi, lo + (1 << 16)), dtype=torch.int64), W.SEED_A).sum()
+        time.sleep(0.002 * (D.rank + 1))
+        D.barrier()
+        if i >= args.warmup:
+            ts.append((time.perf_counter() - t) * 1e3)
+    ms_rank = sum(ts)
+    ms_max = D.reduce([ms_rank])[0]
+    n_total = int(D.reduce([float(hi - lo)], op="sum")[0])
+    ranks = D.gather({"rank": D.rank, "local_rank": D.local, "shard": [lo, hi], "ms_total": ms_rank,
+                      "host": socket.gethostname()})
+    if D.rank == 0:
+        print(json.dumps({"dry_run": True, "metric": METRIC, "n_gpus": D.world, "steps": args.steps,
+                          "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "ms_total_max": ms_max,
+                          "n_total": n_total, "scaling": scaling_of(cfg), "config": config_block(cfg, D.world),
+                          "ranks": ranks}), flush=True)
+    D.close()
 
 
 def main() -> None:
     faulthandler.enable()
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", default="C2", help="C1..C5, comma list, or 'all'")
+    ap.add_argument("--config", default="default",
+                    help="default (C5 headline + C4 per-format sweep in one line), C1..C5, X1..X3u, "
+                         "a comma list (one line each), or 'all'")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-all", action="store_true", help="e2e for every config, not just the first")
+    ap.add_argument("--no-ncu", action="store_true", help="skip the in-run ncu traffic measurement")
+    ap.add_argument("--dry-run", action="store_true", help="gloo on the CPU with a stand-in step")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--rounding", choices=["rn", "rz"], default="rn")
     ap.add_argument("--subnormals", choices=["gradual", "ftz"], default="gradual")
     args = ap.parse_args()
     global MODE
     MODE = (int(args.rounding == "rn"), int(args.subnormals == "ftz"))
-    args.configs = (["C1", "C2", "C3", "C4", "C5"] if args.config == "all"
-                    else args.config.split(","))
+    args.headline = args.config == "default"
+    args.configs = (["C5", "C4"] if args.config == "default" else
+                    ["C1", "C2", "C3", "C4", "C5"] if args.config == "all" else args.config.split(","))
+    for c in args.configs:
+        if c not in CONFIG_TEXT:
+            ap.error(f"unknown config {c}")
     if args.warmup < 3:
         args.warmup = 3
-    if args.impl == "reference":
+    maybe_relaunch(args)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if "WORLD_SIZE" in os.environ and args.gpus not in (1, world):
+        ap.error(f"--gpus {args.gpus} but the launcher started WORLD_SIZE={world} ranks")
+    args.gpus = world
+    if args.dry_run:
+        main_dry_run(args)
+    elif args.impl == "reference":
         main_reference(args)
     else:
         main_ours(args)

@@ -132,11 +132,17 @@ class bfp_vector {
   format_spec spec;
 
   bfp_vector() = default;
-  bfp_vector(format_spec s, std::size_t count) : spec(std::move(s)), count_(count) {
+  // Zero planes like the reference's value-initialised lanes (pack.hpp:50).
+  // The fill is ordered on `stream` -- the stream the producing kernel then
+  // runs on -- so it can never land after that kernel's stores, whatever the
+  // stream's flags (a legacy-stream cudaMemset does not order against a
+  // cudaStreamNonBlocking stream).
+  bfp_vector(format_spec s, std::size_t count, cudaStream_t stream = nullptr)
+      : spec(std::move(s)), count_(count) {
     const bfp_format f = spec.c();
     bytes_ = bfp_plane_bytes(&f, count_);
     if (bytes_) detail::cuda(cudaMalloc(reinterpret_cast<void**>(&planes_), bytes_), "cudaMalloc planes");
-    if (bytes_) detail::cuda(cudaMemset(planes_, 0, bytes_), "cudaMemset planes");
+    if (bytes_) detail::cuda(cudaMemsetAsync(planes_, 0, bytes_, stream), "cudaMemsetAsync planes");
   }
   bfp_vector(const bfp_vector&) = delete;
   bfp_vector& operator=(const bfp_vector&) = delete;
@@ -172,7 +178,7 @@ inline bfp_vector pack(std::span<const encoding> encs, const format_spec& spec,
   validate(spec);
   const bfp_format f = spec.c();
   const std::size_t eb = bfp_enc_bytes(&f);
-  bfp_vector v(spec, encs.size());
+  bfp_vector v(spec, encs.size(), stream);
   if (encs.empty()) return v;
   std::vector<std::uint8_t> narrow(encs.size() * eb);
   for (std::size_t i = 0; i < encs.size(); ++i) std::memcpy(&narrow[i * eb], &encs[i], eb);
@@ -210,7 +216,7 @@ inline std::vector<encoding> unpack(const bfp_vector& v, std::size_t count,
 inline bfp_vector pack_f32(const float* d_in, std::size_t count, const format_spec& spec,
                            cudaStream_t stream = nullptr) {
   validate(spec);
-  bfp_vector v(spec, count);
+  bfp_vector v(spec, count, stream);
   const bfp_format f = spec.c();
   detail::check(bfp_pack_f32(&f, d_in, v.planes(), count, stream), "pack_f32");
   return v;
@@ -226,7 +232,7 @@ inline void unpack_f32(const bfp_vector& v, float* d_out, cudaStream_t stream = 
 inline bfp_vector pack_f64(const double* d_in, std::size_t count, const format_spec& spec,
                            cudaStream_t stream = nullptr) {
   validate(spec);
-  bfp_vector v(spec, count);
+  bfp_vector v(spec, count, stream);
   const bfp_format f = spec.c();
   detail::check(bfp_pack_f64(&f, d_in, v.planes(), count, stream), "pack_f64");
   return v;
@@ -270,7 +276,7 @@ inline bfp_vector pack_bfpraw(std::span<const std::uint8_t> bytes, const format_
   const std::size_t stride = bfpraw_stride(spec);
   if (bytes.size() % stride != 0)
     throw std::invalid_argument("bfpraw: byte count not a multiple of the encoding stride");
-  bfp_vector v(spec, bytes.size() / stride);
+  bfp_vector v(spec, bytes.size() / stride, stream);
   if (bytes.empty()) return v;
   void* d = nullptr;
   detail::cuda(cudaMalloc(&d, bytes.size()), "cudaMalloc bfpraw");
@@ -305,7 +311,7 @@ inline bfp_vector arith(int op, const bfp_vector& x, const bfp_vector& y, const 
   if (c) require_same_shape(x.spec, c->spec);
   if (x.size() != y.size() || (c && c->size() != x.size()))
     throw std::invalid_argument(std::string(where) + ": operand sizes differ");
-  bfp_vector z(x.spec, x.size());
+  bfp_vector z(x.spec, x.size(), stream);
   const bfp_format f = x.spec.c();
   check(bfp_arith(op, &f, x.planes(), y.planes(), c ? c->planes() : nullptr, z.planes(), x.size(),
                   stream),
@@ -344,7 +350,7 @@ inline bfp_vector chain(const char* program, std::initializer_list<const bfp_vec
     if (v->size() != x.size()) throw std::invalid_argument("chain: operand sizes differ");
     ptrs.push_back(v->planes());
   }
-  bfp_vector z(x.spec, x.size());
+  bfp_vector z(x.spec, x.size(), st);
   const bfp_format f = x.spec.c();
   detail::check(bfp_chain(&f, program, int(ptrs.size()), ptrs.data(), z.planes(), x.size(), st), "chain");
   return z;

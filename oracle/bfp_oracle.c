@@ -122,15 +122,16 @@ enum { ORC_ADD = 0, ORC_SUB = 1, ORC_MUL = 2, ORC_DIV = 3, ORC_MUL_ADD = 4 };
 
 static double rounded_op(int op, double a, double b, int rn) {
   volatile double va = a, vb = b, r;
+  const int want = rn ? FE_TONEAREST : FE_TOWARDZERO;
   const int old = fegetround();
-  fesetround(rn ? FE_TONEAREST : FE_TOWARDZERO);
+  if (old != want) fesetround(want);
   switch (op) {
     case ORC_ADD: r = va + vb; break;
     case ORC_SUB: r = va - vb; break;
     case ORC_MUL: r = va * vb; break;
     default: r = va / vb; break;
   }
-  fesetround(old);
+  if (old != want) fesetround(old);
   return r;
 }
 
@@ -205,4 +206,235 @@ void orc_encode_f64_array(const double* in, size_t n, uint64_t* out, unsigned e,
 
 void orc_decode_f64_array(const uint64_t* enc, size_t n, double* out, unsigned e, unsigned s) {
   for (size_t i = 0; i < n; ++i) out[i] = orc_decode(enc[i], e, s);
+}
+
+/* ------------------------------------------------------------------------
+ * Full-size verification (tests only): the oracle's expected result of every
+ * element, compared with the device's output, on all host threads.
+ *
+ * orc_verify: op 0..4 = add/sub/mul/div/mul_add, 5 = pack (the encoding of a
+ * itself), 6 = unpack to float32 ((float)decode(encode(a))).  Inputs a, b, c
+ * are u32 encodings (in_kind 0) or float32 values through encode_scalar
+ * (in_kind 1), element i at index i.  got = the device planes
+ * (field_from_elements image, bitfield.hpp:33-52) for ops 0..5, float32 bits
+ * for op 6.  Returns the number of mismatching elements; the first one (by
+ * index) is reported through first / first_got / first_want.
+ * ------------------------------------------------------------------------ */
+#include <pthread.h>
+
+typedef struct {
+  int op;
+  orc_fmt f;
+  int in_kind;
+  const void *a, *b, *c;
+  const void* got;
+  size_t n, b0, b1; /* element count, block range [b0, b1) */
+  uint64_t bad, first, first_got, first_want;
+} orc_vjob;
+
+static uint64_t in_enc(const orc_vjob* j, const void* p, size_t i) {
+  if (j->in_kind == 0) return ((const uint32_t*)p)[i];
+  return orc_encode((double)((const float*)p)[i], j->f.e, j->f.s, j->f.rn, j->f.ftz);
+}
+
+static void note_bad(orc_vjob* j, size_t i, uint64_t got, uint64_t want) {
+  if (j->bad++ == 0 || i < j->first) {
+    j->first = i;
+    j->first_got = got;
+    j->first_want = want;
+  }
+}
+
+static void* orc_vthread(void* arg) {
+  orc_vjob* j = (orc_vjob*)arg;
+  const orc_fmt* f = &j->f;
+  const unsigned nb = 1 + f->e + f->s;
+  uint64_t want[1024];
+  uint32_t blk[64 * 32];
+  for (size_t b = j->b0; b < j->b1; ++b) {
+    const size_t i0 = b * 1024;
+    const size_t cnt = j->n - i0 < 1024 ? j->n - i0 : 1024;
+    for (size_t k = 0; k < cnt; ++k) {
+      const size_t i = i0 + k;
+      const uint64_t x = in_enc(j, j->a, i);
+      switch (j->op) {
+        case 5: want[k] = x; break;
+        case 6: {
+          const float v = (float)orc_decode(x, f->e, f->s);
+          uint32_t w;
+          memcpy(&w, &v, 4);
+          want[k] = w;
+          break;
+        }
+        case ORC_MUL_ADD:
+          want[k] = orc_mul_add(f->e, f->s, f->rn, f->ftz, x, in_enc(j, j->b, i), in_enc(j, j->c, i));
+          break;
+        default: want[k] = orc_binop(j->op, f->e, f->s, f->rn, f->ftz, x, in_enc(j, j->b, i)); break;
+      }
+    }
+    if (j->op == 6) {
+      const uint32_t* g = (const uint32_t*)j->got + i0;
+      for (size_t k = 0; k < cnt; ++k)
+        if (g[k] != (uint32_t)want[k]) note_bad(j, i0 + k, g[k], want[k]);
+      continue;
+    }
+    for (size_t k = cnt; k < 1024; ++k) want[k] = 0; /* zero-filled tail, pack.hpp:50 */
+    memset(blk, 0, nb * 128);
+    for (unsigned k = 0; k < 1024; ++k)
+      for (unsigned p = 0; p < nb; ++p) blk[p * 32 + (k >> 5)] |= (uint32_t)((want[k] >> p) & 1u) << (k & 31);
+    const uint32_t* g = (const uint32_t*)j->got + b * nb * 32;
+    if (memcmp(g, blk, nb * 128) != 0) {
+      for (unsigned k = 0; k < cnt; ++k) {
+        uint64_t v = 0;
+        for (unsigned p = 0; p < nb; ++p) v |= (uint64_t)((g[p * 32 + (k >> 5)] >> (k & 31)) & 1u) << p;
+        if (v != want[k]) note_bad(j, i0 + k, v, want[k]);
+      }
+    }
+  }
+  return NULL;
+}
+
+uint64_t orc_verify(int op, unsigned e, unsigned s, int rn, int ftz, int in_kind, const void* a,
+                    const void* b, const void* c, const void* got, size_t n, int threads,
+                    uint64_t* first, uint64_t* first_got, uint64_t* first_want) {
+  if (threads < 1) threads = 1;
+  if (threads > 256) threads = 256;
+  const size_t blocks = (n + 1023) / 1024;
+  orc_vjob jobs[256];
+  pthread_t tid[256];
+  int started = 0;
+  for (int t = 0; t < threads; ++t) {
+    orc_vjob* j = &jobs[t];
+    memset(j, 0, sizeof *j);
+    j->op = op;
+    j->f.e = e;
+    j->f.s = s;
+    j->f.rn = rn;
+    j->f.ftz = ftz;
+    j->in_kind = in_kind;
+    j->a = a;
+    j->b = b;
+    j->c = c;
+    j->got = got;
+    j->n = n;
+    j->b0 = blocks * (size_t)t / (size_t)threads;
+    j->b1 = blocks * (size_t)(t + 1) / (size_t)threads;
+    j->first = n;
+    if (pthread_create(&tid[t], NULL, orc_vthread, j) == 0) {
+      ++started;
+    } else {
+      orc_vthread(j); /* run inline */
+      tid[t] = 0;
+    }
+  }
+  uint64_t bad = 0, fi = n, fg = 0, fw = 0;
+  for (int t = 0; t < threads; ++t) {
+    if (tid[t]) pthread_join(tid[t], NULL);
+    bad += jobs[t].bad;
+    if (jobs[t].bad && jobs[t].first < fi) {
+      fi = jobs[t].first;
+      fg = jobs[t].first_got;
+      fw = jobs[t].first_want;
+    }
+  }
+  (void)started;
+  if (first) *first = fi;
+  if (first_got) *first_got = fg;
+  if (first_want) *first_want = fw;
+  return bad;
+}
+
+/* mul_add over ALL (a, b) pairs of a 16-bit format against nc fixed c values:
+ * pair i of the chunk is a = a0 + i / 65536, b = i % 65536; result planes
+ * got[k] hold bfp_add(bfp_mul(a, b), c_k) for the chunk's na * 65536 pairs.
+ * The product is computed once per pair (orc_binop), each c through a
+ * 65536-entry table add_tab[k * 65536 + p] = orc_binop(ADD, p, c_k). */
+typedef struct {
+  orc_fmt f;
+  uint32_t a0;
+  int nc;
+  const uint16_t* add_tab;
+  const uint32_t* const* got;
+  size_t b0, b1;
+  uint64_t bad, first, first_k, first_got, first_want;
+} orc_pjob;
+
+static void* orc_pthread(void* arg) {
+  orc_pjob* j = (orc_pjob*)arg;
+  const orc_fmt* f = &j->f;
+  uint16_t prod[1024];
+  for (size_t b = j->b0; b < j->b1; ++b) {
+    for (unsigned k = 0; k < 1024; ++k) {
+      const size_t i = b * 1024 + k;
+      prod[k] = (uint16_t)orc_binop(ORC_MUL, f->e, f->s, f->rn, f->ftz, j->a0 + (i >> 16), i & 0xffff);
+    }
+    for (int q = 0; q < j->nc; ++q) {
+      const uint16_t* tab = j->add_tab + (size_t)q * 65536;
+      const uint32_t* g = j->got[q] + b * 16 * 32;
+      for (unsigned w = 0; w < 32; ++w) {
+        for (unsigned p = 0; p < 16; ++p) {
+          uint32_t word = 0;
+          for (unsigned t = 0; t < 32; ++t) word |= (uint32_t)((tab[prod[w * 32 + t]] >> p) & 1u) << t;
+          if (word != g[p * 32 + w]) {
+            for (unsigned t = 0; t < 32; ++t) {
+              const unsigned k = w * 32 + t;
+              uint64_t v = 0;
+              for (unsigned pp = 0; pp < 16; ++pp) v |= (uint64_t)((g[pp * 32 + w] >> t) & 1u) << pp;
+              const uint64_t want = tab[prod[k]];
+              if (v != want && (j->bad++ == 0)) {
+                j->first = b * 1024 + k;
+                j->first_k = (uint64_t)q;
+                j->first_got = v;
+                j->first_want = want;
+              }
+            }
+            break; /* this word's 32 elements are counted once */
+          }
+        }
+      }
+    }
+  }
+  return NULL;
+}
+
+uint64_t orc_verify_mul_add_pairs(unsigned e, unsigned s, int rn, int ftz, uint32_t a0, uint32_t na,
+                                  const uint16_t* add_tab, int nc, const uint32_t* const* got, int threads,
+                                  uint64_t* info /* first index, c slot, got, want */) {
+  if (threads < 1) threads = 1;
+  if (threads > 256) threads = 256;
+  const size_t blocks = (size_t)na * 64; /* na * 65536 pairs / 1024 */
+  orc_pjob jobs[256];
+  pthread_t tid[256];
+  for (int t = 0; t < threads; ++t) {
+    orc_pjob* j = &jobs[t];
+    memset(j, 0, sizeof *j);
+    j->f.e = e;
+    j->f.s = s;
+    j->f.rn = rn;
+    j->f.ftz = ftz;
+    j->a0 = a0;
+    j->nc = nc;
+    j->add_tab = add_tab;
+    j->got = got;
+    j->b0 = blocks * (size_t)t / (size_t)threads;
+    j->b1 = blocks * (size_t)(t + 1) / (size_t)threads;
+    if (pthread_create(&tid[t], NULL, orc_pthread, j) != 0) {
+      orc_pthread(j);
+      tid[t] = 0;
+    }
+  }
+  uint64_t bad = 0;
+  int have = 0;
+  for (int t = 0; t < threads; ++t) {
+    if (tid[t]) pthread_join(tid[t], NULL);
+    if (jobs[t].bad && !have && info) {
+      info[0] = jobs[t].first;
+      info[1] = jobs[t].first_k;
+      info[2] = jobs[t].first_got;
+      info[3] = jobs[t].first_want;
+      have = 1;
+    }
+    bad += jobs[t].bad;
+  }
+  return bad;
 }

@@ -74,6 +74,13 @@ def orc():
                                            C.c_int, C.c_int]
         L.orc_decode_f64_array.restype = None
         L.orc_decode_f64_array.argtypes = [_u64p, C.c_size_t, C.POINTER(C.c_double), C.c_uint, C.c_uint]
+        L.orc_verify.restype = C.c_uint64
+        L.orc_verify.argtypes = [C.c_int, C.c_uint, C.c_uint, C.c_int, C.c_int, C.c_int, C.c_void_p,
+                                 C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_int,
+                                 _u64p, _u64p, _u64p]
+        L.orc_verify_mul_add_pairs.restype = C.c_uint64
+        L.orc_verify_mul_add_pairs.argtypes = [C.c_uint, C.c_uint, C.c_int, C.c_int, C.c_uint32, C.c_uint32,
+                                               C.c_void_p, C.c_int, C.c_void_p, C.c_int, _u64p]
         L.orc_binop_exhaustive.restype = None
         L.orc_binop_exhaustive.argtypes = [C.c_int, C.c_uint, C.c_uint, C.c_int, C.c_int, _u64p]
         _orc = L
@@ -289,3 +296,42 @@ def ref_gate_count(op: str, fmt) -> dict:
         raise ValueError(f"ref_gate_count rc={rc}")
     a, o, x, n = (int(v) for v in out)
     return {"and": a, "or": o, "xor": x, "not": n, "total": a + o + x + n}
+
+
+VERIFY_OPS = dict(OPS, pack=5, unpack_f32=6)
+
+
+def verify(op: str, fmt, a: np.ndarray, b: np.ndarray | None, c: np.ndarray | None, got: np.ndarray,
+           n: int, threads: int | None = None) -> tuple[int, int, int, int]:
+    """Full-size check on all host threads (orc_verify): the oracle's result of
+    `op` on every element of (a, b, c) -- u32 encodings or float32 values
+    through encode_scalar -- against the device output `got` (plane image, or
+    float32 for op "unpack_f32").  Returns (mismatches, first index, got, want)."""
+    e, s, rn, ftz = fmt
+    kind = 1 if a.dtype == np.float32 else 0
+    arrs = [np.ascontiguousarray(v, dtype=np.float32 if kind else np.uint32) if v is not None else None
+            for v in (a, b, c)]
+    got = np.ascontiguousarray(got)
+    fi, fg, fw = C.c_uint64(), C.c_uint64(), C.c_uint64()
+    bad = orc().orc_verify(VERIFY_OPS[op], e, s, int(rn), int(ftz), kind,
+                           *[v.ctypes.data if v is not None else None for v in arrs],
+                           got.ctypes.data, n, threads or os.cpu_count() or 1,
+                           C.byref(fi), C.byref(fg), C.byref(fw))
+    return int(bad), fi.value, fg.value, fw.value
+
+
+def verify_mul_add_pairs(fmt, a0: int, na: int, cs: np.ndarray, got: list, threads: int | None = None):
+    """All pairs (a0 <= a < a0 + na, every b) of a 16-bit format through
+    z = add(mul(a, b), c_k) for each c_k in cs, against the device result planes
+    got[k] (na * 65536 elements each).  Returns (mismatches, [index, k, got, want])."""
+    e, s, rn, ftz = fmt
+    assert 1 + e + s == 16
+    tabs = np.stack([binop("add", fmt, np.arange(1 << 16, dtype=np.uint64),
+                           np.full(1 << 16, int(c), dtype=np.uint64)) for c in cs]).astype(np.uint16)
+    tabs = np.ascontiguousarray(tabs)
+    gots = [np.ascontiguousarray(g, dtype=np.uint32) for g in got]
+    ptrs = (C.c_void_p * len(gots))(*[g.ctypes.data for g in gots])
+    info = np.zeros(4, dtype=np.uint64)
+    bad = orc().orc_verify_mul_add_pairs(e, s, int(rn), int(ftz), a0, na, tabs.ctypes.data, len(cs), ptrs,
+                                         threads or os.cpu_count() or 1, _p(info, _u64p))
+    return int(bad), [int(v) for v in info]

@@ -301,6 +301,22 @@ def unpack_f64(v: bfp_vector, count: int | None = None) -> torch.Tensor:
     return out
 
 
+def _check_planes(v: bfp_vector, like: bfp_vector, what: str) -> None:
+    """v must hold like.count elements of like.spec in contiguous int32 planes
+    on like's device, large enough for every plane word a kernel touches: a
+    short or foreign buffer is rejected before any launch writes past it."""
+    require_same_shape(like.spec, v.spec)
+    if v.count != like.count:
+        raise ValueError(f"{what}: element count {v.count} != {like.count}")
+    p = v.planes
+    if p.dtype != torch.int32 or not p.is_contiguous() or not p.is_cuda:
+        raise ValueError(f"{what}: planes must be a contiguous int32 CUDA tensor")
+    if p.device != like.planes.device:
+        raise ValueError(f"{what}: planes on {p.device}, operands on {like.planes.device}")
+    if p.numel() * 4 < v.spec.plane_bytes(v.count):
+        raise ValueError(f"{what}: {p.numel() * 4} plane bytes < {v.spec.plane_bytes(v.count)} needed")
+
+
 def _binop(op: int, x: bfp_vector, y: bfp_vector, c: bfp_vector | None = None,
            out: bfp_vector | None = None, inputs_ready: bool = False) -> bfp_vector:
     require_same_shape(x.spec, y.spec)
@@ -308,6 +324,12 @@ def _binop(op: int, x: bfp_vector, y: bfp_vector, c: bfp_vector | None = None,
         require_same_shape(x.spec, c.spec)
     if x.count != y.count or (c is not None and c.count != x.count):
         raise ValueError("operands must have the same element count")
+    _check_planes(x, x, "x")
+    _check_planes(y, x, "y")
+    if c is not None:
+        _check_planes(c, x, "c")
+    if out is not None:
+        _check_planes(out, x, "out")
     z = out if out is not None else empty(x.spec, x.count, x.planes.device)
     check(lib().bfp_arith_ex(op, x.spec.c, x.planes.data_ptr(), y.planes.data_ptr(),
                              c.planes.data_ptr() if c is not None else None, z.planes.data_ptr(),
@@ -380,6 +402,10 @@ def chain(program: str, *vs: bfp_vector, out: bfp_vector | None = None) -> bfp_v
         require_same_shape(vs[0].spec, v.spec)
         if v.count != vs[0].count:
             raise ValueError("operands must have the same element count")
+    for k, v in enumerate(vs):
+        _check_planes(v, vs[0], f"input {k}")
+    if out is not None:
+        _check_planes(out, vs[0], "out")
     z = out if out is not None else empty(vs[0].spec, vs[0].count, vs[0].planes.device)
     ptrs = (C.c_void_p * len(vs))(*[v.planes.data_ptr() for v in vs])
     check(lib().bfp_chain(vs[0].spec.c, program.encode(), len(vs), ptrs, z.planes.data_ptr(), vs[0].count,

@@ -438,7 +438,8 @@ bfp_host_ctx* bfp_host_ctx_create(size_t chunk_elems) {
     const long m = atol(v);
     if (m >= 1) c->min_chunks = size_t(m);
   }
-  // sized for the widest case: 32 planes or float32 elements
+  // 32 planes or float32 elements per chunk block; wider formats (up to 64
+  // planes) run proportionally fewer blocks per chunk (chunk_for)
   c->cap_bytes = c->chunk_blocks * 1024 * 4;
   cudaGetDevice(&c->dev);
   for (cudaStream_t* st : {&c->s_in, &c->s_k, &c->s_out})
@@ -481,11 +482,17 @@ namespace {
 // Chunk size of one call: the context's chunk, but small enough that the call
 // splits into >= min_chunks chunks (fill and drain cost one chunk each), and
 // never below 512 blocks (2^19 elements) so per-copy overhead stays small.
-size_t chunk_for(const bfp_host_ctx* c, size_t blocks) {
+// block_bytes = the widest per-block footprint of any staged buffer of the
+// call (planes: n * 128 B, up to 8 KiB for 64-plane formats; float32: 4 KiB):
+// a chunk never holds more than the slot buffers' cap_bytes.
+size_t chunk_for(const bfp_host_ctx* c, size_t blocks, size_t block_bytes) {
   constexpr size_t kMinBlocks = 512;
   const size_t split = (blocks + c->min_chunks - 1) / c->min_chunks;
   size_t cb = split < kMinBlocks ? kMinBlocks : split;
-  return cb < c->chunk_blocks ? cb : c->chunk_blocks;
+  if (cb > c->chunk_blocks) cb = c->chunk_blocks;
+  const size_t fit = c->cap_bytes / (block_bytes ? block_bytes : 1);
+  if (cb > fit) cb = fit;
+  return cb ? cb : 1;
 }
 
 struct Chunk {
@@ -517,10 +524,11 @@ void* mapped_alias(void* h) {
 // stage); otherwise they land in the slot's device buffers and are copied
 // D2H in chunk order on s_out.
 template <typename In, typename Body, typename Out>
-bfp_status host_pipeline(bfp_host_ctx* c, size_t count, int n_in, int n_out, In in_bytes,
-                         Body body, Out out_bytes) {
+bfp_status host_pipeline(bfp_host_ctx* c, size_t count, size_t block_bytes, int n_in, int n_out,
+                         In in_bytes, Body body, Out out_bytes) {
   if (!c) return fail(BFP_EARG, "null host context");
   if (count == 0) return BFP_OK;
+  if (block_bytes > c->cap_bytes) return fail(BFP_ESIZE, "host ctx: chunk buffers smaller than one block");
   // In-place writes cross PCIe at ~52.6 GB/s against ~57 GB/s for a D2H copy
   // (B200 box, tools/pcie_probe.py) but drop the copy stage's per-chunk
   // event hops and its drain: they win on calls whose output is small next
@@ -547,7 +555,7 @@ bfp_status host_pipeline(bfp_host_ctx* c, size_t count, int n_in, int n_out, In 
       for (int i = 0; i < bfp_host_ctx::kDepth; ++i)
         if (!c->out_buf(i, q)) return fail(BFP_ECUDA, "host ctx: output buffer allocation failed");
   const size_t blocks = nblocks(count);
-  const size_t cb = chunk_for(c, blocks);
+  const size_t cb = chunk_for(c, blocks, block_bytes);
   bool used[bfp_host_ctx::kDepth] = {};
   cudaError_t e = cudaSuccess;
   for (size_t b0 = 0, k = 0; b0 < blocks; b0 += cb, ++k) {
@@ -642,7 +650,7 @@ bfp_status bfp_arith_host_batch(bfp_host_ctx* c, int nops, const int* ops, const
   const size_t stride = nplanes(f) * 128;
   const void* ins[3] = {h_x, h_y, h_c};
   return host_pipeline(
-      c, count, need_c ? 3 : 2, nops,
+      c, count, stride, need_c ? 3 : 2, nops,
       [&](const Chunk& ch, int a, const void** src, size_t* bytes) {
         *src = static_cast<const char*>(ins[a]) + ch.b0 * stride;
         *bytes = ch.nb * stride;
@@ -675,7 +683,7 @@ bfp_status bfp_pack_f32_host(bfp_host_ctx* c, const bfp_format* f, const float* 
   if (!h_in || !h_planes) return fail(BFP_EARG, "null buffer");
   const size_t stride = nplanes(f) * 128;
   return host_pipeline(
-      c, count, 1, 1,
+      c, count, stride > 4096 ? stride : 4096, 1, 1,
       [&](const Chunk& ch, int, const void** src, size_t* bytes) {
         *src = h_in + ch.e0;
         *bytes = ch.ne * 4;
@@ -700,7 +708,7 @@ bfp_status bfp_unpack_f32_host(bfp_host_ctx* c, const bfp_format* f, const uint3
   if (!h_out || !h_planes) return fail(BFP_EARG, "null buffer");
   const size_t stride = nplanes(f) * 128;
   return host_pipeline(
-      c, count, 1, 1,
+      c, count, stride > 4096 ? stride : 4096, 1, 1,
       [&](const Chunk& ch, int, const void** src, size_t* bytes) {
         *src = reinterpret_cast<const char*>(h_planes) + ch.b0 * stride;
         *bytes = ch.nb * stride;

@@ -118,6 +118,45 @@ def test_wide_layout_and_bfpraw(ref_oracle, fmt2):
     assert np.array_equal(bfp.unpack_bfpraw(vr).cpu().numpy(), raw)
 
 
+@pytest.mark.parametrize("fmt2", [(11, 52), (10, 40)])
+def test_host_pipeline_wide_formats(ref_oracle, fmt2):
+    """Host-buffer pipeline on formats wider than 32 planes (up to 8 KiB per
+    block), over more chunks than buffer slots: each chunk must fit the
+    context's staging buffers (sized for 32 planes / float32 per block), so
+    a wide format runs fewer blocks per chunk.  The result equals the device
+    path over the same planes and the reference on both ends."""
+    O = ref_oracle
+    L = _lib.lib()
+    e, s = fmt2
+    nb = 1 + e + s
+    fmt = (e, s, 1, 0)
+    chunk = 1 << 19
+    n = 9 * chunk + 77  # > 8 chunks of the context, ragged tail
+    rng = np.random.default_rng(nb)
+    x, y = operands(e, s, n, rng), operands(e, s, n, rng)
+    px, py = O.pack_planes(x, nb), O.pack_planes(y, nb)
+    f = _lib.BfpFormat(e, s, 1, 0, b"")
+    ctx = L.bfp_host_ctx_create(chunk)
+    assert ctx
+    outs = [np.zeros_like(px) for _ in range(2)]
+    try:
+        arr = (C.c_int * 2)(2, 0)
+        zp = (C.c_void_p * 2)(*[o.ctypes.data for o in outs])
+        assert L.bfp_arith_host_batch(ctx, 2, arr, C.byref(f), px.ctypes.data, py.ctypes.data, None,
+                                      zp, n) == 0, L.bfp_last_error()
+    finally:
+        L.bfp_host_ctx_destroy(ctx)
+    for o, op in zip(outs, ("mul", "add")):
+        assert np.array_equal(o, _arith(op, fmt, px, py, px)), op
+        k = 4096
+        for lo in (0, n - k):  # the reference itself on the first / last blocks
+            blo = lo // 1024
+            pxs = px[blo * nb * 32:(blo + O.nblocks(k)) * nb * 32]
+            pys = py[blo * nb * 32:(blo + O.nblocks(k)) * nb * 32]
+            want = O.ref_binop_planes(op, fmt, pxs, pys, None)
+            assert np.array_equal(o[blo * nb * 32:blo * nb * 32 + len(want)], want), (op, lo)
+
+
 @pytest.mark.parametrize("fmt2", [(4, 3), (5, 10), (8, 23), (7, 30), (11, 52), (2, 1), (2, 5), (3, 11), (2, 40)])
 @pytest.mark.parametrize("mode", [(1, 0), (0, 1)])
 def test_pack_unpack_f64(oracle, fmt2, mode):

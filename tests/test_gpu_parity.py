@@ -215,6 +215,18 @@ def test_python_api_roundtrip(oracle):
         assert np.array_equal(z, oracle.binop(op, (4, 3, 1, 0), ex, ey)), op
     with pytest.raises(ValueError):
         bfp.bfp_add(vx, bfp.pack_f32(y, bfp.make_spec(4, 3, name="other")))
+    # out= must match the operands' spec, count and plane size (no OOB writes)
+    good = bfp.empty(spec, 3000)
+    assert bfp.bfp_mul(vx, vy, out=good) is good
+    bad = [bfp.empty(bfp.make_spec(3, 2), 3000),                        # narrower format
+           bfp.empty(spec, 1000),                                       # fewer elements
+           bfp.bfp_vector(spec, good.planes[:good.planes.numel() // 2], 3000),  # short planes
+           bfp.bfp_vector(spec, good.planes.cpu(), 3000)]               # host memory
+    for out in bad:
+        with pytest.raises(ValueError):
+            bfp.bfp_mul(vx, vy, out=out)
+        with pytest.raises(ValueError):
+            bfp.chain("ab*", vx, vy, out=out)
 
 
 def test_unsupported_and_errors():

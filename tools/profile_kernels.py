@@ -1,8 +1,13 @@
-"""Minimal driver for ncu: builds one config's resident operands and runs a
-few steps of its kernels, nothing else (so launch lists and --set full
-captures see only the hot path).
+"""Minimal driver for ncu: builds one config's resident operands (exactly as
+bench.py does) and runs a few steps of its kernels, nothing else, so launch
+lists and --set full captures see only the hot path.
 
-    python tools/profile_kernels.py [--config C2] [--iters 5]
+    python tools/profile_kernels.py [--config C5] [--iters 1] [--ops add_1/8/15,...]
+                                    [--rounding rn|rz] [--subnormals gradual|ftz] [--marker]
+
+--marker prints "TIMED <k>" before the timed launches (k = kernels per
+iteration x iters): bench.py's in-run traffic measurement takes the last k
+profiled launches as the timed ones (operand setup comes first).
 """
 from __future__ import annotations
 
@@ -16,18 +21,24 @@ sys.path.insert(0, str(ROOT))
 
 def main() -> None:
     ap = argparse.ArgumentParser()
-    ap.add_argument("--config", default="C2")
+    ap.add_argument("--config", default="C5")
     ap.add_argument("--iters", type=int, default=5)
-    ap.add_argument("--ops", default=None, help="comma list (C3/C4: which kernels)")
+    ap.add_argument("--ops", default=None, help="comma list of job labels to keep")
+    ap.add_argument("--rounding", choices=["rn", "rz"], default="rn")
+    ap.add_argument("--subnormals", choices=["gradual", "ftz"], default="gradual")
+    ap.add_argument("--marker", action="store_true")
     a = ap.parse_args()
     import torch
     dev = torch.device("cuda", 0)
     import bench
+    bench.MODE = (int(a.rounding == "rn"), int(a.subnormals == "ftz"))
     jobs = [(j.label, j.launch) for j in bench.make_jobs(a.config, 0, 1, dev)]
     if a.ops:
         keep = set(a.ops.split(","))
         jobs = [j for j in jobs if j[0] in keep]
     torch.cuda.synchronize()
+    if a.marker:
+        print(f"TIMED {len(jobs) * a.iters}", flush=True)
     st = torch.cuda.current_stream().cuda_stream
     for i in range(a.iters):
         for _, fn in jobs:
