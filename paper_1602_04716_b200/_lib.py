@@ -9,7 +9,10 @@ from __future__ import annotations
 import ctypes as C
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "libbfpgpu.so"
+import os
+
+# BFP_LIB: an alternative build of the same library (A/B measurements only)
+LIB_PATH = Path(os.environ.get("BFP_LIB") or Path(__file__).resolve().parent / "libbfpgpu.so")
 
 # bfp_status
 BFP_OK, BFP_EFORMAT, BFP_EMISMATCH, BFP_ESIZE, BFP_EUNSUPPORTED, BFP_ECUDA, BFP_EARG = range(7)

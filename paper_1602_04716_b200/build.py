@@ -19,8 +19,11 @@ from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
-BUILD = PKG / "_build"
-LIB = PKG / "libbfpgpu.so"
+# BFP_BUILD_TAG=<tag> builds an A/B variant into _build_<tag>/ and
+# ab/<tag>/libbfpgpu.so (loaded with BFP_LIB=...; tools/gpu_ab_libs.sh)
+_TAG = os.environ.get("BFP_BUILD_TAG", "")
+BUILD = PKG / (f"_build_{_TAG}" if _TAG else "_build")
+LIB = (PKG.parent / "ab" / _TAG / "libbfpgpu.so") if _TAG else PKG / "libbfpgpu.so"
 INCLUDE = PKG.parent / "include"
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -105,6 +108,7 @@ def build(jobs: int | None = None, force: bool = False, verbose: bool = True) ->
             if st != "up-to-date":
                 print(f"[bfp build] {s.name}: {st}", file=sys.stderr)
     if force or _stale(LIB, objs):
+        LIB.parent.mkdir(parents=True, exist_ok=True)
         cmd = [NVCC, *ARCH, "-shared", "--cudart", "static", "-o", str(LIB), *map(str, objs)]
         subprocess.run(cmd, check=True)
         if verbose:

@@ -12,10 +12,14 @@
 // for the compiled kernels).  Disabled with BFP_JIT=0.
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <fcntl.h>
+#include <spawn.h>
+#include <sys/wait.h>
 #include <sys/stat.h>
 #include <unistd.h>
 
 
+#include <cerrno>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -191,6 +195,26 @@ bool nvrtc_compile(const std::string& src, const std::string& expr, bool lower, 
   return true;
 }
 
+// Runs argv[0] (searched on PATH) with argv, stdout/stderr to /dev/null;
+// returns its exit status (-1 if it could not be started or was signalled).
+int run_quiet(const std::vector<std::string>& args) {
+  std::vector<char*> argv;
+  for (const std::string& a : args) argv.push_back(const_cast<char*>(a.c_str()));
+  argv.push_back(nullptr);
+  posix_spawn_file_actions_t fa;
+  posix_spawn_file_actions_init(&fa);
+  posix_spawn_file_actions_addopen(&fa, 1, "/dev/null", O_WRONLY, 0);
+  posix_spawn_file_actions_addopen(&fa, 2, "/dev/null", O_WRONLY, 0);
+  pid_t pid = 0;
+  const int e = posix_spawnp(&pid, argv[0], &fa, nullptr, argv.data(), environ);
+  posix_spawn_file_actions_destroy(&fa);
+  if (e != 0) return -1;
+  int status = 0;
+  while (waitpid(pid, &status, 0) < 0)
+    if (errno != EINTR) return -1;
+  return WIFEXITED(status) ? WEXITSTATUS(status) : -1;
+}
+
 // ---- runtime LOP3 covers (BFP_JIT_MAP=1) ---------------------------------
 // Formats without a build-time cover normally run the templates as ptxas maps
 // them (6-12% slower on logic-bound networks than the LOP3-mapped covers,
@@ -217,12 +241,14 @@ std::string runtime_cover_dir(unsigned e, unsigned s, int rn, int ftz) {
   for (size_t i = 1; i <= dir.size(); ++i)
     if (i == dir.size() || dir[i] == '/') mkdir(dir.substr(0, i).c_str(), 0755);
   const std::string exe = dir + "/" + stem + ".gen." + std::to_string(getpid());
-  char defs[160];
-  std::snprintf(defs, sizeof defs, "-DGEN_ONE_E=%u -DGEN_ONE_S=%u -DGEN_ONE_RN=%d -DGEN_ONE_FTZ=%d", e, s, rn, ftz);
-  const std::string cmd = "g++ -O2 -std=c++17 -I'" + csrc_dir() + "' -I'" + tools + "' " + defs + " '" + tools +
-                          "/gen.cpp' -o '" + exe + "' >/dev/null 2>&1 && '" + exe + "' '" + dir +
-                          "' >/dev/null 2>&1";
-  const int rc = std::system(cmd.c_str());
+  // argv vectors, no shell: paths are passed verbatim whatever they contain
+  const std::vector<std::string> compile = {
+      "g++", "-O2", "-std=c++17", "-I" + csrc_dir(), "-I" + tools,
+      "-DGEN_ONE_E=" + std::to_string(e), "-DGEN_ONE_S=" + std::to_string(s),
+      "-DGEN_ONE_RN=" + std::to_string(rn), "-DGEN_ONE_FTZ=" + std::to_string(ftz),
+      tools + "/gen.cpp", "-o", exe};
+  int rc = run_quiet(compile);
+  if (rc == 0) rc = run_quiet({exe, dir});
   std::remove(exe.c_str());
   if (rc != 0 || stat(hdr.c_str(), &st) != 0) {
     std::fprintf(stderr, "[bfp jit] runtime LOP3 mapping unavailable for 1/%u/%u (rc %d); using templates\n",

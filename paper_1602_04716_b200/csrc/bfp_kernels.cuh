@@ -132,6 +132,24 @@ constexpr int arith_minb() {
   return BFP_ARITH_MINB;
 }
 
+// L2 prefetch of the warp's NEXT block for the logic-bound networks: their
+// units are long, so the next unit's loads then start from L2 instead of HBM
+// and the unit-start stall shortens.  Each lane prefetches one or two of the
+// block's NIN x N plane lines (prefetch.global.L2, per-thread addresses fixed
+// before the loop: one 64-bit add per line per unit).  BFP_PREFETCH: 0 off,
+// 1 networks of >= 300 LOP3 per word (default), 2 every arithmetic kernel.
+#ifndef BFP_PREFETCH
+#define BFP_PREFETCH 1
+#endif
+__device__ __forceinline__ void prefetch_line_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+template <class F, int OP>
+constexpr bool arith_prefetch() {
+  if constexpr (Gen<F, OP>::ok) return BFP_PREFETCH == 2 || (BFP_PREFETCH == 1 && Gen<F, OP>::luts >= 300);
+  return BFP_PREFETCH == 2;
+}
+
 template <class F, int OP>
 __global__ void __launch_bounds__(kThreads, arith_minb<F, OP>()) k_arith(const w32* __restrict__ x,
                                                     const w32* __restrict__ y,
@@ -147,6 +165,15 @@ __global__ void __launch_bounds__(kThreads, arith_minb<F, OP>()) k_arith(const w
   constexpr int N = F::N;
   constexpr int NIN = OP == OP_MUL_ADD ? 3 : 2;
   const size_t stride = size_t(gridDim.x) * kThreads;
+  // this lane's prefetch lines l = lane, lane + 32 of a block (operand l / N,
+  // plane l % N; taken modulo the block's NIN x N lines, so every pointer is
+  // valid and a few lines are simply prefetched twice), as pointers into block 0
+  constexpr int NPF = NIN * N > 32 ? 2 : 1;
+  const w32* pf[NPF];
+  BFP_UNROLL for (int k = 0; k < NPF; ++k) {
+    const unsigned l = ((threadIdx.x & 31) + 32 * k) % unsigned(NIN * N);
+    pf[k] = (l < N ? x : (l < 2 * N ? y : c)) + (l % N) * 32;
+  }
   for (size_t u = size_t(blockIdx.x) * kThreads + threadIdx.x; u < units; u += stride) {
     const size_t base = (u >> 5) * (size_t(N) * 32) + (u & 31);
     Operands<N, NIN> cur;
@@ -154,6 +181,13 @@ __global__ void __launch_bounds__(kThreads, arith_minb<F, OP>()) k_arith(const w
     if (!waited) {
       asm volatile("griddepcontrol.wait;" ::: "memory");
       waited = true;
+    }
+    if constexpr (arith_prefetch<F, OP>()) {
+      const size_t un = u + stride;
+      if (un < units) {
+        const size_t nb = (un >> 5) * (size_t(N) * 32);
+        BFP_UNROLL for (int k = 0; k < NPF; ++k) prefetch_line_l2(pf[k] + nb);
+      }
     }
     // register-capped networks: releasing before the network keeps the
     // loop-carried values out of local memory (ptxas spilled 20-24 B of the

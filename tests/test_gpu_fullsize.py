@@ -10,8 +10,9 @@ tests/test_oracle.py) on all host threads (orc_verify):
   * C4: add and mul of every sweep format at 2^28;
   * the fused mul_add network (its own LOP3 cover, not the composition of the
     mul and add covers): 1/6/9 over ALL 2^32 (a, b) pairs for 32 c values
-    (signed zeros, subnormals, 1, max finite, Inf, NaN, random), and ALL 2^24
-    (a, b, c) triples of 1/4/3 and 2^18 of 1/3/2 in every mode.
+    (signed zeros, subnormals, 1, max finite, Inf, NaN, random) -- RN +
+    gradual by default, RZ + FTZ too with BFP_EXHAUSTIVE16=all (~4 min each)
+    -- and ALL 2^24 (a, b, c) triples of 1/4/3 and 2^18 of 1/3/2 in every mode.
 
 Inputs are generated on the device by the bench's own generators
 (workloads.py, torch ops -- not our kernels) and copied to the host for the
@@ -20,6 +21,7 @@ bitfield.hpp:33-52).  Log of a run: profiles/r02_fullsize.log.
 """
 from __future__ import annotations
 
+import os
 import time
 
 import numpy as np
@@ -124,7 +126,10 @@ C_1_6_9 = [0x0000, 0x8000, 0x0001, 0x8001, 0x01FF, 0x81FF, 0x0200, 0x8200, 0x3E0
            0x5A5A, 0xA5A5, 0x1234, 0x9876, 0x4321, 0xC0DE, 0x3FFF, 0x0100]
 
 
-@pytest.mark.parametrize("mode", [(1, 0), (0, 1)])
+MODES_PAIRS = [(1, 0), (0, 1)] if os.environ.get("BFP_EXHAUSTIVE16") == "all" else [(1, 0)]
+
+
+@pytest.mark.parametrize("mode", MODES_PAIRS)
 def test_mul_add_all_pairs_1_6_9(oracle, mode):
     """The fused cover over every (a, b) of 1/6/9 for 32 fixed c values."""
     rn, ftz = mode

@@ -12,13 +12,14 @@ from __future__ import annotations
 
 import argparse
 import json
+import os
 import re
 import subprocess
 from collections import Counter
 from pathlib import Path
 
 ROOT = Path(__file__).resolve().parent.parent
-LIB = ROOT / "paper_1602_04716_b200" / "libbfpgpu.so"
+LIB = Path(os.environ.get("BFP_LIB") or ROOT / "paper_1602_04716_b200" / "libbfpgpu.so")
 
 ALU_PIPE = {"LOP3", "IADD3", "SHF", "PRMT", "ISETP", "SEL", "IMNMX", "FLO", "LEA", "LOP",
             "VIADD", "IABS", "POPC", "BREV", "PLOP3", "VIMNMX", "SGXT", "BMSK", "FSEL", "FSETP", "P2R", "R2P"}
