@@ -794,7 +794,8 @@ def ncu_traffic(cfgs: list[str], local: int, timeout: int = 600) -> dict:
     for cfg in cfgs:
         kre = {"C3": "k_arith|k_pack_f32|k_unpack_f32", "X3": "bfp_chain_k"}.get(cfg, "k_arith")
         logf = Path(os.environ.get("TMPDIR", "/tmp")) / f"bench_ncu_{os.getpid()}_{cfg}.csv"
-        cmd = [exe, "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum",
+        cmd = [exe, "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,"
+                                 "sm__inst_executed_pipe_alu.sum",
                "--clock-control", "none", "-k", f"regex:{kre}", "--csv", "--print-units", "base",
                "--log-file", str(logf),
                sys.executable, str(ROOT / "tools" / "profile_kernels.py"), "--config", cfg,
@@ -831,6 +832,7 @@ def ncu_traffic(cfgs: list[str], local: int, timeout: int = 600) -> dict:
             continue
         out[cfg] = [{"kernel": rows[i]["kernel"][:160],
                      "bytes": int(rows[i].get("dram__bytes_read.sum", 0) + rows[i].get("dram__bytes_write.sum", 0)),
+                     "alu_warp_inst": rows[i].get("sm__inst_executed_pipe_alu.sum"),
                      "ncu_us": round(rows[i].get("gpu__time_duration.sum", 0) / 1e3, 2)} for i in order[-k:]]
     return out
 
@@ -1112,12 +1114,15 @@ def roofline_block(jd, ent: dict, peaks: dict, peak_lop3: dict | None, traffic) 
     r = {"kernel": f"{jd.label} ({jd.fmt} {mode_text()})", "launch_ms": ent["ms"],
          "elements_per_launch": jd.n}
     logic = None
-    if "lop3_per_elem" in ent and peak_lop3:
-        logic = {"achieved": round(ent["lop3_per_elem"] * jd.n / dur / 1e12, 4),
+    per_elem = ent.get("lop3_per_elem", ent.get("alu_inst_per_elem_measured"))
+    if per_elem is not None and "logic_frac" in ent and peak_lop3:
+        src = ("SASS LOP3 count of the shipped kernel (cuobjdump of the loaded libbfpgpu.so) / 32 "
+               "elements per unit" if "lop3_per_elem" in ent else
+               "executed ALU-pipe instructions per element (ncu sm__inst_executed_pipe_alu in this run)")
+        logic = {"achieved": round(per_elem * jd.n / dur / 1e12, 4),
                  "peak": round(peak_lop3["burst"] / 1e12, 4), "unit": "TLOP3/s", "frac": ent["logic_frac"],
-                 "lop3_per_elem": ent["lop3_per_elem"],
-                 "lop3_source": "SASS LOP3 count of the shipped kernel (cuobjdump of the loaded "
-                                "libbfpgpu.so) / 32 elements per unit",
+                 "lop3_per_elem": per_elem,
+                 "lop3_source": src,
                  "peak_source": "bfp_probe_lop3 measured in this run (burst; 148 SM x 64/clk x f_SM)",
                  "peak_sustained": round(peak_lop3["sustained"] / 1e12, 4),
                  "peak_sustained_sm_mhz": peak_lop3["sustained_sm_mhz"]}
@@ -1180,10 +1185,25 @@ def build_line(cfg: str, res: dict, args, D: Dist, probes: dict, traffic: dict) 
         if isinstance(tr, list) and k < len(tr):
             ent["traffic"] = tr[k]["bytes"]
             ent["traffic_over_algorithmic"] = round(tr[k]["bytes"] / j.algo_bytes, 4)
+            if tr[k].get("alu_warp_inst"):
+                # executed ALU-pipe instructions per element (one warp instruction
+                # = 32 threads x one 32-element unit each), measured by ncu in this run
+                ape = tr[k]["alu_warp_inst"] * 32 / j.n
+                ent["alu_inst_per_elem_measured"] = round(ape, 3)
+                lop3 = probes.get("lop3")
+                if "lop3_per_elem" not in ent and lop3:
+                    # kernels without a static LOP3 count (fused float32 codec, chains):
+                    # the logic leg from the executed ALU-pipe instructions
+                    lf = ape * j.n / lop3["burst"] / (ms * 1e-3)
+                    ent.update({"logic_frac": round(lf, 4), "logic_leg": "executed ALU-pipe instructions (ncu)",
+                                "tlop3_s": round(ape * j.n / (ms * 1e-3) / 1e12, 3)})
+                    if lf > ent["hbm_frac"]:
+                        ent["bound"], ent["frac"] = "logic", round(lf, 4)
         per_op[j.label] = ent
         per_format.setdefault(j.fmt, {})[j.op] = {
             key: ent[key] for key in ("gelem_s", "bound", "frac", "ms", "hbm_frac", "logic_frac",
-                                      "logic_frac_at_load_clock", "lop3_per_elem", "traffic_over_algorithmic")
+                                      "logic_frac_at_load_clock", "lop3_per_elem", "alu_inst_per_elem_measured",
+                                      "traffic_over_algorithmic")
             if key in ent}
         per_format[j.fmt][j.op]["config"] = cfg
     k_dom = max(range(len(jobs)), key=lambda k: res["kern_ms"][k])

@@ -137,9 +137,12 @@ constexpr int arith_minb() {
 // and the unit-start stall shortens.  Each lane prefetches one or two of the
 // block's NIN x N plane lines (prefetch.global.L2, per-thread addresses fixed
 // before the loop: one 64-bit add per line per unit).  BFP_PREFETCH: 0 off,
-// 1 networks of >= 300 LOP3 per word (default), 2 every arithmetic kernel.
+// 1 networks of >= 300 LOP3 per word, 2 every arithmetic kernel.  Off by
+// default: an interleaved A/B (profiles/r02_ab_prefetch.txt) showed no gain on
+// the logic-bound networks (C5 mul_add 591 vs 602 Gelem/s without, 1/8/15
+// mul 444 vs 456) for +10 ALU-pipe instructions per unit.
 #ifndef BFP_PREFETCH
-#define BFP_PREFETCH 1
+#define BFP_PREFETCH 0
 #endif
 __device__ __forceinline__ void prefetch_line_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));

@@ -48,20 +48,38 @@ def sass_functions(lib: Path) -> dict[str, list[str]]:
             continue
         if cur is None:
             continue
-        m = re.match(r"\s*/\*[0-9a-f]+\*/\s+(@!?U?P\w+\s+)?([A-Z][A-Z0-9_.]*)", line)
+        m = re.match(r"\s*/\*([0-9a-f]+)\*/\s+(@!?U?P\w+\s+)?([A-Z][A-Z0-9_.]*)(.*)", line)
         if m:
-            funcs[cur].append(m.group(2))
+            funcs[cur].append((int(m.group(1), 16), m.group(3), m.group(4)))
     return funcs
+
+
+def loop_body(ins: list) -> list[str]:
+    """Opcodes of the main loop: the span of the widest backward branch (the
+    grid-stride loop of the kernels; empty if there is none)."""
+    best = None
+    for a, op, rest in ins:
+        if op.startswith("BRA"):
+            t = re.search(r"0x([0-9a-f]+)", rest)
+            if t and int(t.group(1), 16) < a:
+                lo = int(t.group(1), 16)
+                if best is None or a - lo > best[1] - best[0]:
+                    best = (lo, a)
+    if best is None:
+        return []
+    return [op for a, op, _ in ins if best[0] <= a <= best[1]]
 
 
 def stats(lib: Path = LIB, pattern: str | None = None) -> dict[str, dict]:
     funcs = sass_functions(lib)
     dm = demangle(list(funcs))
     res = {}
-    for name, ins in funcs.items():
+    for name, tins in funcs.items():
         pretty = dm.get(name, name)
         if pattern and not re.search(pattern, pretty):
             continue
+        ins = [op for _, op, _ in tins]
+        body = Counter(i.split(".")[0] for i in loop_body(tins))
         base = Counter(i.split(".")[0] for i in ins)
         alu = sum(v for k, v in base.items() if k in ALU_PIPE)
         fma = sum(v for k, v in base.items() if k in FMA_PIPE)
@@ -72,6 +90,9 @@ def stats(lib: Path = LIB, pattern: str | None = None) -> dict[str, dict]:
             "alu_pipe": alu,
             "fma_pipe": fma,
             "mem": sum(v for k, v in base.items() if k in MEM),
+            "loop_LOP3": body.get("LOP3", 0),
+            "loop_alu_pipe": sum(v for k, v in body.items() if k in ALU_PIPE),
+            "loop_total": sum(body.values()),
             "top": base.most_common(8),
         }
     return res
@@ -87,7 +108,8 @@ def main() -> None:
     for name, r in sorted(res.items()):
         short = re.sub(r"bfpg::|Format<|unsigned int|const", "", name)[:90]
         print(f"{short:90s} tot={r['total']:5d} LOP3={r['LOP3']:5d} alu={r['alu_pipe']:5d} "
-              f"fma={r['fma_pipe']:4d} mem={r['mem']:3d}  LOP3/elem={r['LOP3'] / 32:.2f}")
+              f"fma={r['fma_pipe']:4d} mem={r['mem']:3d} loop: LOP3={r['loop_LOP3']:5d} "
+              f"alu={r['loop_alu_pipe']:5d}  LOP3/elem={r['LOP3'] / 32:.2f}")
     if a.json:
         Path(a.json).write_text(json.dumps(res, indent=1))
 
