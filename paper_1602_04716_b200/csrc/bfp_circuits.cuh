@@ -50,6 +50,12 @@ typedef unsigned long long uintptr_t;
 #define BFP_UNROLL
 #endif
 
+// Stage markers for the mapper's per-stage LUT report (tools/lutmap/stages.cpp);
+// no code anywhere else.
+#ifndef BFP_STAGE
+#define BFP_STAGE(name)
+#endif
+
 namespace bfpg {
 
 #if defined(BFP_SYMBOLIC_WORD)
@@ -254,6 +260,7 @@ BFP_HD void add_w(const w32* X, const w32* Y, w32* Z) {
   const w32 sx = X[M];
   const w32 sy = SUB ? ~Y[M] : Y[M];
 
+  BFP_STAGE("add.compare_swap");
   // Order by magnitude: swap = |X| < |Y| as (E+S)-bit encodings (borrow of X-Y).
   w32 bw = 0;
   BFP_UNROLL for (int i = 0; i < M; ++i) bw = maj(~X[i], Y[i], bw);
@@ -267,6 +274,7 @@ BFP_HD void add_w(const w32* X, const w32* Y, w32* Z) {
   const w32 sb = mux(swap, sx, sy);
   const w32 eff = sx ^ sy;  // effective subtraction
 
+  BFP_STAGE("add.classes_distance");
   // Hidden bits (exponent nonzero) and effective exponents (subnormals at 1).
   w32 ha = 0, hb = 0;
   BFP_UNROLL for (int i = 0; i < E; ++i) {
@@ -285,6 +293,7 @@ BFP_HD void add_w(const w32* X, const w32* Y, w32* Z) {
   w32 d[E];
   (void)sub_k<E>(ea, eb, d);
 
+  BFP_STAGE("add.align");
   // Align B: [jam, r, g, frac(S), hidden] right by d.  Distances >= WA-1 put
   // everything in the jam bit, so the amount saturates at 2^KA - 1 >= WA - 1.
   constexpr int WA = S + 4;
@@ -304,6 +313,7 @@ BFP_HD void add_w(const w32* X, const w32* Y, w32* Z) {
   }
   shr_jam<WA, KS>(f, amt);
 
+  BFP_STAGE("add.adder");
   // One adder for both effective operations: A + (B ^ eff) + eff.
   constexpr int WN = WA + 1;
   w32 x[WN];
@@ -323,6 +333,7 @@ BFP_HD void add_w(const w32* X, const w32* Y, w32* Z) {
     x[WA] = c & ~eff;  // only an effective add carries out
   }
 
+  BFP_STAGE("add.normalize");
   // Budget-limited normalise: shift left by sh = min(lz(x), ea) so results
   // below the smallest normal stop at the subnormal position.  The budget r
   // starts at min(ea, 2^KN - 1) and is decremented by every shift taken.
@@ -342,9 +353,15 @@ BFP_HD void add_w(const w32* X, const w32* Y, w32* Z) {
     BFP_UNROLL for (int i = WN - D; i < WN; ++i) any |= (i >= 0 ? x[i] : 0u);
     const w32 c = ok & ~any;
     sh[k] = c;
+    // The leading one of a sum without carry-out sits at most two places
+    // below the top when the exponent distance is >= 2 (x >= A - A/4), so a
+    // shift by D >= 4 only happens on a massive cancellation (effective
+    // subtraction, distance <= 1), where the jam and round bits x[0], x[1]
+    // are zero -- B moved by at most one place -- and stay zero: those
+    // stages shift zeros into positions D and D + 1.
     w32 nx[WN];
     BFP_UNROLL for (int i = 0; i < WN; ++i)
-      nx[i] = (i >= D) ? pmux(c, x[i - D], x[i]) : pandn(x[i], c);
+      nx[i] = (i >= D && (D < 4 || i - D >= 2)) ? pmux(c, x[i - D], x[i]) : pandn(x[i], c);
     BFP_UNROLL for (int i = 0; i < WN; ++i) x[i] = nx[i];
     if (k > 0) {
       // r -= c << k (r >= 2^k whenever c is set)
@@ -357,6 +374,7 @@ BFP_HD void add_w(const w32* X, const w32* Y, w32* Z) {
     }
   }
 
+  BFP_STAGE("add.round_pack");
   // sig = x[4..S+4], guard x[3], sticky x[0..2].
   const w32* sig = x + 4;
   w32 rnd = 0;
@@ -372,6 +390,7 @@ BFP_HD void add_w(const w32* X, const w32* Y, w32* Z) {
   w32 fr[S], ex[E + 1];
   pack_round<E, S, E>(Dx, sig, rnd, fr, ex);
 
+  BFP_STAGE("add.specials_out");
   // Exact zero: +0 from cancellation, -0 only for (-0) + (-0).
   w32 nz = 0;
   BFP_UNROLL for (int i = 0; i <= S; ++i) nz |= sig[i];
@@ -427,6 +446,7 @@ BFP_HD void finish_round(w32* R, const w32* ez, w32 sign, w32 zero_res, w32 inf_
   constexpr int E = F::E, S = F::S, M = E + S;
   static_assert(EW >= E + 2, "finish_round: working exponent narrower than E + 2");
   constexpr int WR = S + 3;
+  BFP_STAGE("fr.subnormal_shift");
   const w32 sub = ez[EW - 1];
   {
     // amt = -ez = ~ez + 1, live only on sub; saturate at 2^KR - 1 >= WR - 1.
@@ -446,6 +466,7 @@ BFP_HD void finish_round(w32* R, const w32* ez, w32 sign, w32 zero_res, w32 inf_
     w32 (&Rr)[WR] = *reinterpret_cast<w32(*)[WR]>(R);
     shr_jam<WR, KRS>(Rr, amt);
   }
+  BFP_STAGE("fr.round_pack");
   const w32* sig = R + 2;
   w32 rnd = 0;
   if constexpr (F::RN) rnd = R[1] & (R[0] | sig[0]);
@@ -463,6 +484,7 @@ BFP_HD void finish_round(w32* R, const w32* ez, w32 sign, w32 zero_res, w32 inf_
   BFP_UNROLL for (int i = E + 1; i < EW - 1; ++i) high |= ez[i];
   const w32 ovf = ex[E] | ex[E + 1] | eall | (high & ~sub);
 
+  BFP_STAGE("fr.specials_out");
   w32 flush = 0;
   if constexpr (F::FTZ) flush = sub & ~ex[0];  // still below the smallest normal
   const w32 quiet = ~(zero_res | inf_res | use_nan);
@@ -720,6 +742,7 @@ BFP_HD void mul_w(const w32* X, const w32* Y, w32* Z) {
   constexpr int E = F::E, S = F::S, M = E + S;
   constexpr int EW = mul_ew<F>();  // signed working exponent
   constexpr bool BOTH_SUB_ZERO = (1 - F::BIAS) <= -S - 1;
+  BFP_STAGE("mul.classes");
   const w32 sign = X[M] ^ Y[M];
   const Classes cx = classify<F>(X), cy = classify<F>(Y);
 
@@ -753,6 +776,7 @@ BFP_HD void mul_w(const w32* X, const w32* Y, w32* Z) {
   };
   if constexpr (BOTH_SUB_ZERO) {
     // s: the operand that may be subnormal (X unless X is normal), n: the other.
+    BFP_STAGE("mul.order_normalize");
     w32 ms[S + 1], mn[S + 1];
     BFP_UNROLL for (int i = 0; i < S; ++i) {
       ms[i] = pmux(cx.h, Y[i], X[i]);
@@ -764,8 +788,10 @@ BFP_HD void mul_w(const w32* X, const w32* Y, w32* Z) {
     w32 lz[KN];
     normalize_stages<S + 1, KN, KN - 1>(ms, lz);
     ms[S] = ONES;  // a zero significand (the only one without a leading one) forces a zero result
+    BFP_STAGE("mul.product");
     sig_product_best<S>(mn, ms, P);
     // 1-bit normalise: top = P[2S+1]; otherwise the leading one is at 2S.
+    BFP_STAGE("mul.normalize1_exponent");
     const w32 top = P[WP - 1];
     w32 st = 0;
     BFP_UNROLL for (int i = 0; i + 1 < S; ++i) st |= P[i];
@@ -795,6 +821,7 @@ BFP_HD void mul_w(const w32* X, const w32* Y, w32* Z) {
   }
 
   // Special-value rules of bfp_mul (arith.hpp:193-199).
+  BFP_STAGE("mul.special_masks");
   const w32 use_nan = cx.nan | cy.nan | (cx.inf & cy.z) | (cx.z & cy.inf);
   w32 zero_src = cx.z | cy.z;
   if constexpr (BOTH_SUB_ZERO) zero_src |= ~cx.h & ~cy.h;  // underflows to a signed zero

@@ -31,9 +31,24 @@ struct Graph {
   std::vector<Node> nodes{Node{0, 0, 0}};
   std::unordered_map<uint64_t, uint32_t> hash;
   uint32_t n_inputs = 0;
+  // stage of the template code that created each node (BFP_STAGE markers;
+  // the per-stage LUT report of tools/lutmap/stages.cpp)
+  std::vector<uint16_t> tag{0};
+  std::vector<std::string> stage_names{"(inputs)"};
+  uint16_t cur = 0;
+  void stage(const char* name) {
+    for (size_t i = 0; i < stage_names.size(); ++i)
+      if (stage_names[i] == name) {
+        cur = uint16_t(i);
+        return;
+      }
+    stage_names.push_back(name);
+    cur = uint16_t(stage_names.size() - 1);
+  }
 
   Lit input() {
     nodes.push_back(Node{1, 0, 0});
+    tag.push_back(0);
     ++n_inputs;
     return Lit(nodes.size() - 1) * 2;
   }
@@ -43,6 +58,7 @@ struct Graph {
     auto it = hash.find(key);
     if (it != hash.end()) return Lit(it->second) * 2;
     nodes.push_back(Node{kind, a, b});
+    tag.push_back(cur);
     hash.emplace(key, uint32_t(nodes.size() - 1));
     return Lit(nodes.size() - 1) * 2;
   }
