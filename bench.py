@@ -770,11 +770,12 @@ def _under_profiler() -> bool:
     return any(k in os.environ for k in ("CUDA_INJECTION64_PATH", "NV_TPS_LAUNCH_TOKEN", "NV_NSIGHT_INJECTION_TRANSPORT_TYPE"))
 
 
-def ncu_traffic(cfgs: list[str], local: int, timeout: int = 600) -> dict:
+def ncu_traffic(cfgs: list[str], local: int, world: int = 1, timeout: int = 600) -> dict:
     """DRAM bytes per launch of every timed kernel, measured in THIS run: an
     ncu subprocess (dram__bytes_read/write.sum; no timing is taken from it)
-    over tools/profile_kernels.py, which builds the same resident operands and
-    issues each config's kernels once, in job order.  Returns
+    over tools/profile_kernels.py, which builds the same resident operands as
+    rank 0 of this run (same shard size) and issues each config's kernels
+    once, in job order.  Returns
     {cfg: [{"kernel", "bytes", "ncu_us"} per job]} or {"error": ...}."""
     if _under_profiler():
         return {"error": "bench itself runs under a profiler"}
@@ -799,7 +800,7 @@ def ncu_traffic(cfgs: list[str], local: int, timeout: int = 600) -> dict:
                "--clock-control", "none", "-k", f"regex:{kre}", "--csv", "--print-units", "base",
                "--log-file", str(logf),
                sys.executable, str(ROOT / "tools" / "profile_kernels.py"), "--config", cfg,
-               "--iters", "1", "--marker"] + mode
+               "--iters", "1", "--marker", "--rank", "0", "--world", str(world)] + mode
         try:
             r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, env=env, cwd=ROOT)
             txt = logf.read_text() if logf.exists() else ""
@@ -1288,7 +1289,7 @@ def main_ours(args) -> None:
     if not args.no_ncu:
         if D.rank == 0:
             log("DRAM traffic: ncu subprocess over tools/profile_kernels.py")
-            traffic = ncu_traffic(list(args.configs), D.local)
+            traffic = ncu_traffic(list(args.configs), D.local, D.world)
         D.barrier()
     lines = [build_line(cfg, res, args, D, probes, traffic) for cfg, res in results]
     for line, (cfg, res) in zip(lines, results):

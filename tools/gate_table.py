@@ -53,7 +53,7 @@ def main() -> None:
     out = "\n".join(lines)
     print(out)
     if a.md:
-        Path(a.md).write_text("# Gate counts: reference counted_lane vs our SASS LOP3 (round 1)\n\n" + out + "\n")
+        Path(a.md).write_text("# Gate counts: reference counted_lane vs our SASS LOP3 (regenerated from the shipped libbfpgpu.so by tools/gate_table.py)\n\n" + out + "\n")
 
 
 if __name__ == "__main__":

@@ -27,12 +27,14 @@ def main() -> None:
     ap.add_argument("--rounding", choices=["rn", "rz"], default="rn")
     ap.add_argument("--subnormals", choices=["gradual", "ftz"], default="gradual")
     ap.add_argument("--marker", action="store_true")
+    ap.add_argument("--rank", type=int, default=0, help="build rank r's shard of a --world run (bench's sizes)")
+    ap.add_argument("--world", type=int, default=1)
     a = ap.parse_args()
     import torch
     dev = torch.device("cuda", 0)
     import bench
     bench.MODE = (int(a.rounding == "rn"), int(a.subnormals == "ftz"))
-    jobs = [(j.label, j.launch) for j in bench.make_jobs(a.config, 0, 1, dev)]
+    jobs = [(j.label, j.launch) for j in bench.make_jobs(a.config, a.rank, a.world, dev)]
     if a.ops:
         keep = set(a.ops.split(","))
         jobs = [j for j in jobs if j[0] in keep]
