@@ -254,7 +254,7 @@ class Job:
     def __init__(self, label, op, spec, n, launch, algo_bytes, host=None, touch=None):
         self.label, self.op, self.spec, self.n = label, op, spec, n
         self.launch, self.algo_bytes, self.host = launch, algo_bytes, host
-        self.touch = touch or (lambda i, lb=label, b=algo_bytes: (lb, b, 0))
+        self.touch = touch or (lambda i, lb=label, b=algo_bytes: (lb, b, 0))  # fixed operands
 
     @property
     def fmt(self) -> str:
@@ -295,14 +295,11 @@ def spec_of(e: int, s: int):
 
 def rotation_sets(spec, n, n_inputs: int, launches_per_step: int = 1) -> int:
     """Operand sets rotated launch by launch so that a set is re-read only
-    after >= 2x L2 of OTHER traffic (reads of the other sets + every write):
-    with k sets and one launch touching (n_inputs + 1) planes of n elements,
-    a set comes back after k - 1 launches' traffic plus its own launch's write."""
-    pb = spec.plane_bytes(n)
-    launch = (n_inputs + 1) * pb
-    k = 1
-    while (k - 1) * launch + pb < 2 * L2_BYTES:
-        k += 1
+    after >= 2x L2 of traffic: with k sets and one launch streaming (n_inputs
+    + 1) planes of n elements, a set's first line comes back after k launches'
+    reads and writes (its own launch's included)."""
+    launch = (n_inputs + 1) * spec.plane_bytes(n)
+    k = max(1, -(-2 * L2_BYTES // launch))
     # every launch of a step uses a different set, so k >= launches per step
     return max(k, launches_per_step)
 
@@ -474,15 +471,16 @@ def make_jobs(cfg: str, rank: int, world: int, device) -> list:
 
 
 def l2_reuse_distance(jobs, steps: int = 128) -> int:
-    """Smallest amount of other traffic (bytes) between two reads of the same
-    operand set over `steps` consecutive steps of the launch sequence (-1 if
-    no set is read twice in that window)."""
+    """Smallest amount of traffic (bytes) between a read of an operand set's
+    first line and its next read, over `steps` consecutive steps of the launch
+    sequence: everything the reading launch streams after it plus every launch
+    in between (-1 if no set is read twice in that window)."""
     seq = [j.touch(i) for i in range(steps) for j in jobs]
     best = None
     for p, (sid, _, _) in enumerate(seq):
         for q in range(p + 1, len(seq)):
             if seq[q][0] == sid:
-                d = seq[p][2] + sum(r + w for _, r, w in seq[p + 1:q])
+                d = sum(r + w for _, r, w in seq[p:q])
                 best = d if best is None else min(best, d)
                 break
     return best if best is not None else -1
