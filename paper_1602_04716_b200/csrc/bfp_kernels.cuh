@@ -111,7 +111,11 @@ __device__ __forceinline__ void eval_unit(const w32* X, const w32* Y, const w32*
 // networks are HBM-bound (the cap measured -2..-3% there).  The 1/8/15 mul
 // (~1000 LOP3 per word, 137 registers uncapped = 3 CTAs/SM) capped for 4
 // CTAs/SM (115 registers, no spills) measured +4% in two repeated A/Bs
-// (profiles/r01_ab_minb_wide.txt); mul_add at 5 or 6 stayed within +-2%.
+// (profiles/r01_ab_minb_wide.txt).  mul_add capped for 5 CTAs/SM (1/6/9:
+// 91 registers instead of 121, no spills in any format or mode, +9 LOP3 of
+// ptxas re-materialisation) measured +1.0% on C5 in a 4-round interleaved
+// A/B (profiles/r02_ab_muladd_minb5.txt: 639.6 vs 633.2 Gelem/s, every
+// round ahead); 6 spills.
 #ifndef BFP_MID_MINB
 #define BFP_MID_MINB 6
 #endif
@@ -119,7 +123,7 @@ __device__ __forceinline__ void eval_unit(const w32* X, const w32* Y, const w32*
 #define BFP_WIDE_MINB 4
 #endif
 #ifndef BFP_MULADD_MINB
-#define BFP_MULADD_MINB 1
+#define BFP_MULADD_MINB 5
 #endif
 template <class F, int OP>
 constexpr int arith_minb() {
