@@ -799,6 +799,17 @@ def ncu_traffic(cfgs: list[str], local: int, world: int = 1, timeout: int = 600)
                "--log-file", str(logf),
                sys.executable, str(ROOT / "tools" / "profile_kernels.py"), "--config", cfg,
                "--iters", "1", "--marker", "--rank", "0", "--world", str(world)] + mode
+        # the same command line first WITHOUT ncu: ncu only ever sees a
+        # program that just exited 0 with no CUDA fault (B200_PROFILING.md)
+        plain = cmd[cmd.index(sys.executable):]
+        try:
+            p0 = subprocess.run(plain, capture_output=True, text=True, timeout=timeout, env=env, cwd=ROOT)
+        except subprocess.TimeoutExpired:
+            out[cfg] = {"error": "plain run of the profiled command timed out"}
+            continue
+        if p0.returncode != 0 or re.search(r"CUDA error|illegal|Xid|fault", p0.stdout + p0.stderr, re.I):
+            out[cfg] = {"error": f"plain run failed (rc={p0.returncode}); ncu not run"}
+            continue
         try:
             r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, env=env, cwd=ROOT)
             txt = logf.read_text() if logf.exists() else ""

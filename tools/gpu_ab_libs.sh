@@ -8,8 +8,13 @@
 # Summary (median per kernel and tag): python tools/ab_summary.py gpurun_out/ab_*.jsonl
 set -u
 mkdir -p gpurun_out
+# the tag order rotates every round (a fixed order biases the later variants:
+# the box warms and its power-capped clock drifts within a round)
+read -r -a TAGA <<< "$TAGS"
+NT=${#TAGA[@]}
 for r in $(seq 1 ${ROUNDS:-3}); do
-  for tag in $TAGS; do
+  for k in $(seq 0 $((NT - 1))); do
+    tag=${TAGA[$(( (k + r - 1) % NT ))]}
     lib=paper_1602_04716_b200/libbfpgpu.so
     [ "$tag" != base ] && lib=ab/$tag/libbfpgpu.so
     BFP_LIB=$PWD/$lib timeout 900 python bench.py --config ${CONFIGS:-C5,C4} --steps ${STEPS:-20} --no-e2e \
