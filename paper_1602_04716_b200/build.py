@@ -113,6 +113,9 @@ def build(jobs: int | None = None, force: bool = False, verbose: bool = True) ->
         subprocess.run(cmd, check=True)
         if verbose:
             print(f"[bfp build] linked {LIB}", file=sys.stderr)
+    if _TAG:  # A/B variants keep only their library (the GPU snapshot is size-capped)
+        import shutil
+        shutil.rmtree(BUILD, ignore_errors=True)
     return LIB
 
 
