@@ -807,7 +807,8 @@ def ncu_traffic(cfgs: list[str], local: int, world: int = 1, timeout: int = 600)
         except subprocess.TimeoutExpired:
             out[cfg] = {"error": "plain run of the profiled command timed out"}
             continue
-        if p0.returncode != 0 or re.search(r"CUDA error|illegal|Xid|fault", p0.stdout + p0.stderr, re.I):
+        if p0.returncode != 0 or re.search(r"CUDA error|illegal memory access|illegal address|Xid|segmentation fault",
+                                           p0.stdout + p0.stderr, re.I):
             out[cfg] = {"error": f"plain run failed (rc={p0.returncode}); ncu not run"}
             continue
         try:
