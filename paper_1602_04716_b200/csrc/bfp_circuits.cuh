@@ -750,7 +750,12 @@ BFP_HD void mul_w(const w32* X, const w32* Y, w32* Z) {
   w32 P[WP];
   w32 R[S + 3];  // [jam, guard, sig(S+1)]
   w32 ez[EW];
-  // ez = ex_eff + ey_eff - bias - lz  (biased result exponent minus one).
+  // ez = ex_eff + ey_eff - bias - lz - borrow  (biased result exponent minus one).
+  // With -bias = 1 - 2^(E-1) and -lz - 1 = ~lz this is two carry chains:
+  //   t  = ex_eff + ey_eff + 1
+  //   ez = t + K + (1 - borrow),  K = ~lz (sign-extended) - 2^(E-1),
+  // and when lz has no bit at or above E-1, K is ~lz below KL and the constant
+  // ...1101...1 (zero at bit E-1) above: no separate pass for the bias.
   auto exponent = [&](const w32* lz, int KL, w32 borrow_in_sub) {
     w32 a[EW], b[EW];
     BFP_UNROLL for (int i = 0; i < EW; ++i) {
@@ -759,6 +764,18 @@ BFP_HD void mul_w(const w32* X, const w32* Y, w32* Z) {
     }
     a[0] |= ~cx.h;
     b[0] |= ~cy.h;
+    if (KL <= E - 1) {
+      w32 t[EW];
+      (void)add_k<EW>(a, b, ONES, t);
+      w32 c = ~borrow_in_sub;
+      BFP_UNROLL for (int i = 0; i < EW; ++i) {
+        const w32 ti = t[i];
+        const w32 ki = (i < KL) ? ~lz[i] : (i == E - 1 ? w32(0u) : ONES);
+        ez[i] = ti ^ ki ^ c;
+        c = maj(ti, ki, c);
+      }
+      return;
+    }
     w32 t[EW];
     (void)add_k<EW>(a, b, 0, t);
     w32 nb[EW];
