@@ -148,9 +148,6 @@ constexpr int arith_minb() {
 #ifndef BFP_PREFETCH
 #define BFP_PREFETCH 0
 #endif
-#ifndef BFP_STAGGER
-#define BFP_STAGGER 0
-#endif
 __device__ __forceinline__ void prefetch_line_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
@@ -175,21 +172,6 @@ __global__ void __launch_bounds__(kThreads, arith_minb<F, OP>()) k_arith(const w
   constexpr int N = F::N;
   constexpr int NIN = OP == OP_MUL_ADD ? 3 : 2;
   const size_t stride = size_t(gridDim.x) * kThreads;
-#if BFP_STAGGER
-  // Phase stagger of the resident CTAs of an SM (logic-bound networks only):
-  // the warps of a scheduler all start together and, sharing the ALU pipe
-  // evenly, tend to reach their next unit's loads together as well, leaving
-  // the pipe idle for a memory latency per round.  CTA slot s of an SM starts
-  // s solo-unit times late, which spreads the load phases over the round.
-  if constexpr (arith_minb<F, OP>() > 1) {
-    unsigned nsm;
-    asm("mov.u32 %0, %%nsmid;" : "=r"(nsm));
-    const unsigned slot = (blockIdx.x / nsm) % unsigned(arith_minb<F, OP>());
-    const long long t0 = clock64(), delay = (long long)slot * Gen<F, OP>::luts * 2 * BFP_STAGGER;
-    while (clock64() - t0 < delay) {
-    }
-  }
-#endif
   // this lane's prefetch lines l = lane, lane + 32 of a block (operand l / N,
   // plane l % N; taken modulo the block's NIN x N lines, so every pointer is
   // valid and a few lines are simply prefetched twice), as pointers into block 0
