@@ -1,6 +1,6 @@
 // tools/lutmap/count.cpp -- LOP3 count of the mapped networks, per format x op.
 //   g++ -O2 -std=c++17 -I... count.cpp && ./a.out
-#include "lutmap.hpp"
+#include "resub.hpp"
 #define BFP_SYMBOLIC_WORD lutmap::Sym
 #include "bfp_circuits.cuh"
 
@@ -26,11 +26,10 @@ size_t count(int op, size_t* gates) {
   }
   std::vector<lutmap::Lit> outs;
   for (int i = 0; i < N; ++i) outs.push_back(Z[i].l);
-  auto M = lutmap::map_luts(g, outs);
-  lutmap::recover_area(g, M, outs);
+  const lutmap::LutNet net = lutmap::optimised_cover(g, outs);
   *gates = g.nodes.size();
   lutmap::graph() = nullptr;
-  return M.luts;
+  return lutmap::count_luts(net);
 }
 
 template <int E, int S>

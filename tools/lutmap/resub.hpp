@@ -1078,3 +1078,36 @@ inline std::vector<Lit> to_graph(const LutNet& net, Graph& g) {
 }
 
 }  // namespace lutmap
+
+namespace lutmap {
+
+// The complete flow behind the generated covers: structural cover of the
+// template graph -> optimize_net -> re-map the optimised network (its LUT
+// boundaries give the structural mapper new choices) and optimise again, while
+// the network still shrinks.  graph() is left pointing at g.
+inline LutNet optimised_cover(Graph& g, const std::vector<Lit>& outs, bool optimise = true) {
+  auto M = map_luts(g, outs);
+  recover_area(g, M, outs);
+  LutNet net = from_mapping(g, M, outs);
+  if (!optimise) return net;
+  optimize_net(net);
+  size_t best = count_luts(net);
+  for (int it = 0; it < 3; ++it) {
+    Graph g2;
+    g2.stage_names = g.stage_names;
+    graph() = &g2;
+    const std::vector<Lit> o2 = to_graph(net, g2);
+    auto M2 = map_luts(g2, o2);
+    recover_area(g2, M2, o2);
+    LutNet n2 = from_mapping(g2, M2, o2);
+    optimize_net(n2);
+    graph() = &g;
+    const size_t n = count_luts(n2);
+    if (n >= best) break;
+    best = n;
+    net = n2;
+  }
+  return net;
+}
+
+}  // namespace lutmap

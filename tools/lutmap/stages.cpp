@@ -1,8 +1,8 @@
-// tools/lutmap/stages.cpp -- LUTs of the mapped networks per circuit stage
+// tools/lutmap/stages.cpp -- LUTs of the mapped networks per circuit stage, before / after resub.hpp
 // (BFP_STAGE markers in bfp_circuits.cuh): where the LOP3s of a kernel go.
 //   g++ -O2 -std=c++17 -Itools/lutmap -Ipaper_1602_04716_b200/csrc tools/lutmap/stages.cpp -o /tmp/stages
 //   /tmp/stages
-#include "lutmap.hpp"
+#include "resub.hpp"
 #define BFP_SYMBOLIC_WORD lutmap::Sym
 #define BFP_STAGE(name) lutmap::graph()->stage(name)
 #include "bfp_circuits.cuh"
@@ -30,12 +30,15 @@ void report(int op, const char* title) {
   }
   std::vector<lutmap::Lit> outs;
   for (int i = 0; i < N; ++i) outs.push_back(Z[i].l);
-  auto M = lutmap::map_luts(g, outs);
-  lutmap::recover_area(g, M, outs);
-  std::map<std::string, int> per;
-  for (uint32_t v : M.required) per[g.stage_names[g.tag[v]]]++;
-  std::printf("%s: %zu LUTs\n", title, M.luts);
-  for (auto& [k, n] : per) std::printf("  %-28s %5d\n", k.c_str(), n);
+  // structural cover (mapper alone) next to the shipped cover (after resub.hpp)
+  const lutmap::LutNet plain = lutmap::optimised_cover(g, outs, false);
+  const lutmap::LutNet opt = lutmap::optimised_cover(g, outs, true);
+  std::map<std::string, std::pair<int, int>> per;
+  for (uint32_t v : lutmap::live_order(plain)) per[g.stage_names[plain.nodes[v].tag]].first++;
+  for (uint32_t v : lutmap::live_order(opt)) per[g.stage_names[opt.nodes[v].tag]].second++;
+  std::printf("%s: %zu LUTs mapped, %zu after the post-mapping optimiser\n", title, lutmap::count_luts(plain),
+              lutmap::count_luts(opt));
+  for (auto& [k, n] : per) std::printf("  %-28s %5d %5d\n", k.c_str(), n.first, n.second);
   lutmap::graph() = nullptr;
 }
 
