@@ -225,9 +225,12 @@ def clocks_rejected(c: dict) -> bool:
 _SASS = None
 
 
-def sass_lop3(fmt, rn, ftz, op: int) -> int | None:
+def sass_lop3(fmt, rn, ftz, op: int, path: str = "fast") -> int | None:
     """Static LOP3 count of the shipped arithmetic kernel (one 32-element unit
-    per loop iteration) from cuobjdump of the loaded library."""
+    per loop iteration) from cuobjdump of the loaded library.  mul_add kernels
+    hold two covers behind a warp-uniform branch; `path` picks the count of
+    the instructions a unit executes on that side ("fast": the fast-domain
+    cover, "general": the general one) -- tools/sass_stats.py, `paths`."""
     global _SASS
     try:
         if _SASS is None:
@@ -239,7 +242,7 @@ def sass_lop3(fmt, rn, ftz, op: int) -> int | None:
               f"{'true' if ftz else 'false'}>, {op}>"
         for name, r in _SASS.items():
             if key in name:
-                return r["LOP3"]
+                return r["paths"][path] if r.get("paths") else r["LOP3"]
     except (OSError, subprocess.SubprocessError, ValueError, KeyError):  # no cuobjdump / odd SASS
         return None
     return None
@@ -251,9 +254,12 @@ class Job:
     index: operand sets / outputs rotate with it).  `touch(i)` = (set id,
     bytes read from that set, bytes written) for the L2 reuse accounting."""
 
-    def __init__(self, label, op, spec, n, launch, algo_bytes, host=None, touch=None):
+    def __init__(self, label, op, spec, n, launch, algo_bytes, host=None, touch=None, aux=None):
         self.label, self.op, self.spec, self.n = label, op, spec, n
         self.launch, self.algo_bytes, self.host = launch, algo_bytes, host
+        # aux: {name: launch}: variants of this kernel timed on their own after the
+        # step (same operands, never part of the step or of `value`)
+        self.aux = aux or {}
         self.touch = touch or (lambda i, lb=label, b=algo_bytes: (lb, b, 0))  # fixed operands
 
     @property
@@ -317,22 +323,27 @@ def _arith_job(label, op, spec, n, sets, device, slot=0, stride=1):
     def idx(i):
         return (stride * i + slot) % len(sets)
 
-    def launch(i, st):
+    def launch(i, st, flags=1):
         # resident operands that nothing in the step writes: BFP_INPUTS_READY
         # lets each kernel's first loads overlap its predecessor's tail
         a, b, c = sets[idx(i)]
         rc = L.bfp_arith_ex(OPNAMES[op], spec.c, a.planes.data_ptr(), b.planes.data_ptr(),
                             c.planes.data_ptr() if c is not None else None,
-                            outs[i & 1].planes.data_ptr(), n, st, 1)
+                            outs[i & 1].planes.data_ptr(), n, st, flags)
         if rc != 0:
             raise RuntimeError(L.bfp_last_error())
+
+    # mul_add kernels pick one of two covers per warp (the fast-domain one when
+    # the whole block is inside it: include/bfpgpu.h, BFP_GENERAL_NETWORK); the
+    # general cover is timed on the same operands beside the step
+    aux = {"general_network": lambda i, st: launch(i, st, 1 | 2)} if op == "mul_add" else None
 
     nbits = spec.total_bits()
     a, b, c = sets[0]
     return Job(label, op, spec, n, launch, (nin + 1) * nbits / 8 * n,
                host={"kind": "arith", "op": op, "inputs": [a, b] + ([c] if c is not None else []),
                      "sets": len(sets)},
-               touch=lambda i: ((id(sets), idx(i)), nin * pb, pb))
+               touch=lambda i: ((id(sets), idx(i)), nin * pb, pb), aux=aux)
 
 
 def _clone_sets(first, k):
@@ -578,9 +589,19 @@ def run_device(cfg: str, steps: int, warmup: int, D: Dist, jobs=None) -> dict:
         kern_ms.append(timed_replay(g) / steps)
         del g
     kern_ms = D.reduce(kern_ms)
+    # variants of a kernel (the general mul_add cover), timed the same way
+    aux_ms = {}
+    for j in jobs:
+        for name, fn in j.aux.items():
+            g, _ = capture(lambda s, fn=fn: [fn(i, s) for i in range(steps)])
+            g.replay()
+            torch.cuda.synchronize()
+            aux_ms[f"{j.label}:{name}"] = D.reduce([timed_replay(g) / steps])[0]
+            del g
     del g_all
     return {"jobs": jobs, "ms_total": ms_total, "ms_total_rank": ms_rank, "kern_ms": kern_ms,
-            "clocks": clocks, "launches": int(launches), "ms_total_eager": ms_total_eager}
+            "clocks": clocks, "launches": int(launches), "ms_total_eager": ms_total_eager,
+            "aux_ms": aux_ms}
 
 
 def local_index(device) -> int:
@@ -1081,7 +1102,8 @@ def config_block(cfg: str, world: int, sweep: list[str] | None = None) -> dict:
 
 
 # ------------------------------------------------------------------- arms
-def op_entry(j, ms: float, n_total: int, peaks: dict, peak_lop3: dict | None, clocks: dict) -> dict:
+def op_entry(j, ms: float, n_total: int, peaks: dict, peak_lop3: dict | None, clocks: dict,
+             path: str = "fast") -> dict:
     """One kernel on both roofline legs (per GPU) and which one binds."""
     dur = ms * 1e-3
     ach = j.algo_bytes / dur / 1e9
@@ -1100,7 +1122,7 @@ def op_entry(j, ms: float, n_total: int, peaks: dict, peak_lop3: dict | None, cl
             parts = [sass_lop3((e, s), rn, ftz, OPNAMES[o]) for o in chain_ops]
             lop3 = None if None in parts else sum(parts)
         else:
-            lop3 = sass_lop3((e, s), rn, ftz, OPNAMES[j.op])
+            lop3 = sass_lop3((e, s), rn, ftz, OPNAMES[j.op], path)
         if lop3 is not None and peak_lop3:
             pe = lop3 / 32.0
             hbm_t = j.algo_bytes / (peaks["hbm_gbs"] * 1e9)
@@ -1219,6 +1241,20 @@ def build_line(cfg: str, res: dict, args, D: Dist, probes: dict, traffic: dict) 
                                       "traffic_over_algorithmic")
             if key in ent}
         per_format[j.fmt][j.op]["config"] = cfg
+        for name, ams in res.get("aux_ms", {}).items():
+            if name.split(":")[0] != j.label:
+                continue
+            # the same kernel forced onto its general cover (BFP_GENERAL_NETWORK), same operands
+            aent = op_entry(j, ams, nt, peaks, probes.get("lop3"), res["clocks"], path="general")
+            per_format[j.fmt][f"{j.op} ({name.split(':')[1]})"] = dict(
+                {key: aent[key] for key in ("gelem_s", "bound", "frac", "ms", "hbm_frac", "logic_frac",
+                                            "logic_frac_at_load_clock", "lop3_per_elem") if key in aent},
+                config=cfg, note="same launch with BFP_GENERAL_NETWORK: every warp runs the general cover "
+                                 "(the one taken when a block holds zeros, subnormals or a small c); not part "
+                                 "of the step")
+            per_format[j.fmt][j.op]["cover"] = (
+                "fast-domain cover: this workload's operands (normal a, b with ea + eb >= bias + 1, "
+                "ec >= 16) pass the per-block test in every warp")
     k_dom = max(range(len(jobs)), key=lambda k: res["kern_ms"][k])
     jd = jobs[k_dom]
     t_dom = None

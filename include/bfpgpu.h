@@ -138,6 +138,14 @@ bfp_status bfp_arith(int op, const bfp_format* f, const uint32_t* d_x, const uin
  * identical; only a violated guarantee (inputs written by the immediately
  * preceding kernel) could observe stale data. */
 #define BFP_INPUTS_READY 1u
+/* BFP_GENERAL_NETWORK: mul_add kernels carry two LOP3 covers -- the general
+ * network and a smaller one valid when every element of a 1024-element block
+ * has normal (or Inf / NaN) a and b whose product cannot land below the normal
+ * range and a c of not-too-small exponent (csrc/bfp_circuits.cuh,
+ * mul_add_fast_domain); each warp tests its block and picks one.  Results are
+ * identical either way.  This flag forces the general cover (tests, A/B
+ * measurement); it is ignored by the other operations. */
+#define BFP_GENERAL_NETWORK 2u
 bfp_status bfp_arith_ex(int op, const bfp_format* f, const uint32_t* d_x, const uint32_t* d_y,
                         const uint32_t* d_c, uint32_t* d_z, size_t count, void* stream,
                         unsigned flags);

@@ -16,7 +16,8 @@ LIB_PATH = Path(os.environ.get("BFP_LIB") or Path(__file__).resolve().parent / "
 
 # bfp_status
 BFP_OK, BFP_EFORMAT, BFP_EMISMATCH, BFP_ESIZE, BFP_EUNSUPPORTED, BFP_ECUDA, BFP_EARG = range(7)
-BFP_INPUTS_READY = 1  # bfp_arith_ex flag (include/bfpgpu.h)
+BFP_INPUTS_READY = 1  # bfp_arith_ex flags (include/bfpgpu.h)
+BFP_GENERAL_NETWORK = 2
 
 
 class BfpFormat(C.Structure):

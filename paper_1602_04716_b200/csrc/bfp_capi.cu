@@ -174,7 +174,7 @@ bfp_status bfp_arith_ex(int op, const bfp_format* f, const uint32_t* d_x, const 
   const bfp_status s = resolve(f, &impl);
   if (s != BFP_OK) return s;
   if (op < 0 || op > 4) return fail(BFP_EARG, "bad op");
-  if (flags & ~unsigned(BFP_INPUTS_READY)) return fail(BFP_EARG, "unknown flags");
+  if (flags & ~unsigned(BFP_INPUTS_READY | BFP_GENERAL_NETWORK)) return fail(BFP_EARG, "unknown flags");
   if (count == 0) return BFP_OK;
   if (!d_x || !d_y || !d_z || (op == 4 && !d_c)) return fail(BFP_EARG, "null operand");
   ++g_launches;

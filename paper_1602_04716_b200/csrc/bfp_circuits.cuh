@@ -254,7 +254,12 @@ struct Gen {
 
 // ================================================================= ADD
 // Z = X + Y (SUB: X - Y).  bfp_add / bfp_sub semantics, arith.hpp:235-328.
-template <class F, bool SUB>
+//
+// FAST: the caller guarantees (mul_add_fast_domain below) that both exponent
+// fields are nonzero and the larger one is >= 2^KN, so the hidden bits are
+// constant ones and the normaliser's budget never binds; every signal equals
+// the general network's on that domain.
+template <class F, bool SUB, bool FAST = false>
 BFP_HD void add_w(const w32* X, const w32* Y, w32* Z) {
   constexpr int E = F::E, S = F::S, M = E + S;
   const w32 sx = X[M];
@@ -281,6 +286,7 @@ BFP_HD void add_w(const w32* X, const w32* Y, w32* Z) {
     ha |= A[S + i];
     hb |= B[S + i];
   }
+  if constexpr (FAST) ha = hb = ONES;
   w32 ea[E], eb[E];
   BFP_UNROLL for (int i = 0; i < E; ++i) {
     ea[i] = A[S + i];
@@ -342,6 +348,7 @@ BFP_HD void add_w(const w32* X, const w32* Y, w32* Z) {
   {
     w32 big = 0;
     BFP_UNROLL for (int k = KN; k < E; ++k) big |= ea[k];
+    if constexpr (FAST) big = ONES;
     BFP_UNROLL for (int k = 0; k < KN; ++k) r[k] = (k < E ? ea[k] : 0u) | big;
   }
   w32 sh[KN];
@@ -440,15 +447,16 @@ BFP_HD void add_w(const w32* X, const w32* Y, w32* Z) {
 // then overflow (Inf under RN, max-finite under RZ), FTZ after rounding
 // (still below the smallest normal) and the special-value overrides:
 // zero_res / inf_res force a signed zero / Inf, use_nan the canonical NaN.
-template <class F, int EW>
+// FAST: ez >= 0 is guaranteed (no subnormal-range shift, no flush).
+template <class F, int EW, bool FAST = false>
 BFP_HD void finish_round(w32* R, const w32* ez, w32 sign, w32 zero_res, w32 inf_res, w32 use_nan,
                          w32* Z) {
   constexpr int E = F::E, S = F::S, M = E + S;
   static_assert(EW >= E + 2, "finish_round: working exponent narrower than E + 2");
   constexpr int WR = S + 3;
   BFP_STAGE("fr.subnormal_shift");
-  const w32 sub = ez[EW - 1];
-  {
+  const w32 sub = FAST ? w32(0u) : ez[EW - 1];
+  if constexpr (!FAST) {
     // amt = -ez = ~ez + 1, live only on sub; saturate at 2^KR - 1 >= WR - 1.
     constexpr int KR = clog2(WR);
     constexpr int KRS = imin(KR, EW);
@@ -737,14 +745,24 @@ BFP_HD void sig_product_best(const w32* a, const w32* b, w32* P) {
 // (two muxes per significand bit; the exponent sum is symmetric) -- and the
 // product, then in [2^2S, 2^(2S+2)), needs a single 1-bit normalise instead of
 // a log shifter over all 2S+2 product bits.
-template <class F>
+//
+// FAST: both exponent fields are nonzero and their sum is >= 2^(E-1) = bias + 1
+// (mul_add_fast_domain), so neither operand needs normalising and the biased
+// result exponent minus one, ez, is >= 0: the pre-product normaliser and the
+// subnormal-range shifter of finish_round fold away.
+template <class F, bool FAST = false>
 BFP_HD void mul_w(const w32* X, const w32* Y, w32* Z) {
   constexpr int E = F::E, S = F::S, M = E + S;
   constexpr int EW = mul_ew<F>();  // signed working exponent
   constexpr bool BOTH_SUB_ZERO = (1 - F::BIAS) <= -S - 1;
+  static_assert(!FAST || BOTH_SUB_ZERO, "mul_w: the fast domain needs emin <= -S-1");
   BFP_STAGE("mul.classes");
   const w32 sign = X[M] ^ Y[M];
-  const Classes cx = classify<F>(X), cy = classify<F>(Y);
+  Classes cx = classify<F>(X), cy = classify<F>(Y);
+  if constexpr (FAST) {
+    cx.h = cy.h = ONES;
+    cx.z = cy.z = 0;
+  }
 
   constexpr int WP = 2 * S + 2;
   w32 P[WP];
@@ -844,7 +862,7 @@ BFP_HD void mul_w(const w32* X, const w32* Y, w32* Z) {
   if constexpr (BOTH_SUB_ZERO) zero_src |= ~cx.h & ~cy.h;  // underflows to a signed zero
   const w32 zero_res = zero_src & ~use_nan;
   const w32 inf_res = (cx.inf | cy.inf) & ~use_nan;
-  finish_round<F, EW>(R, ez, sign, zero_res, inf_res, use_nan, Z);
+  finish_round<F, EW, FAST>(R, ez, sign, zero_res, inf_res, use_nan, Z);
 }
 
 // ================================================================= DIV
@@ -960,6 +978,48 @@ BFP_HD void mul_add_w(const w32* A, const w32* B, const w32* Cc, w32* Z) {
   w32 p[F::N];
   mul_w<F>(A, B, p);
   add_w<F, false>(p, Cc, Z);
+}
+
+// ------------------------------------------------- mul_add: the fast domain
+// Most data never touches the subnormal machinery of the chain, which is a
+// fifth of its LUTs (operand normaliser, subnormal-range shifter, normaliser
+// budget).  A unit whose 32 elements ALL satisfy
+//   ea != 0, eb != 0            a, b normal (or Inf / NaN),
+//   ea + eb >= 2^(E-1)          the product cannot land below the normal range
+//                               (ez = ea + eb - bias - 1 + top >= 0),
+//   ec >= 2^KN                  the sum's exponent max(ep, ec) exceeds every
+//                               normalising shift, KN = clog2(S + 5),
+// may run mul_add_fast_w: the same network with those signals constant.  Inf
+// and NaN operands stay inside the domain (their masks are unchanged); zeros
+// and subnormals of a, b, and small c, fall back to the general network.  The
+// kernels evaluate the predicate per unit and vote per warp (bfp_kernels.cuh),
+// so a warp takes ONE of the two covers; results are identical either way
+// (tests: every triple of 1/4/3 inside the domain, and the GPU sweeps run
+// with the fast cover both enabled and disabled).
+template <class F>
+constexpr bool mul_add_fast_ok() {
+  return F::E > clog2(F::S + 5) && (1 - F::BIAS) <= -F::S - 1;
+}
+
+// Lanes of the unit inside the fast domain.
+template <class F>
+BFP_HD w32 mul_add_fast_domain(const w32* A, const w32* B, const w32* Cc) {
+  constexpr int E = F::E, S = F::S, KN = clog2(S + 5);
+  w32 ha = 0, hb = 0, cbig = 0, cy = 0;
+  BFP_UNROLL for (int i = 0; i < E; ++i) {
+    ha |= A[S + i];
+    hb |= B[S + i];
+  }
+  BFP_UNROLL for (int i = KN; i < E; ++i) cbig |= Cc[S + i];
+  BFP_UNROLL for (int i = 0; i < E - 1; ++i) cy = maj(A[S + i], B[S + i], cy);
+  return ha & hb & cbig & (cy | A[S + E - 1] | B[S + E - 1]);
+}
+
+template <class F>
+BFP_HD void mul_add_fast_w(const w32* A, const w32* B, const w32* Cc, w32* Z) {
+  w32 p[F::N];
+  mul_w<F, true>(A, B, p);
+  add_w<F, false, true>(p, Cc, Z);
 }
 
 }  // namespace bfpg

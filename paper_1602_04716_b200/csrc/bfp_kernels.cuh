@@ -98,6 +98,32 @@ __device__ __forceinline__ void eval_unit(const w32* X, const w32* Y, const w32*
   }
 }
 
+// mul_add with a fast-domain cover (Gen<F, 5>, bfp_circuits.cuh
+// mul_add_fast_domain): every lane evaluates the domain predicate of its unit
+// (~14 LOP3) and the warp votes, so all 32 lanes run the SAME cover -- the
+// fast one only when all 1024 elements of the block are inside the domain.
+// BFP_GENERAL_NETWORK (flags bit 1) forces the general cover.  All 32 lanes of
+// a warp are in the loop together (units is a multiple of 32 and a warp owns
+// 32 consecutive units), so the full-mask vote is safe.
+constexpr int OP_MUL_ADD_FAST = 5;
+template <class F, int OP>
+constexpr bool has_fast_cover() {
+  if constexpr (OP == OP_MUL_ADD) return Gen<F, OP_MUL_ADD_FAST>::ok;
+  return false;
+}
+template <class F, int OP>
+__device__ __forceinline__ void eval_unit_dyn(const w32* X, const w32* Y, const w32* Cc, w32* Z,
+                                              unsigned flags) {
+  if constexpr (has_fast_cover<F, OP>()) {
+    const bool in_domain = mul_add_fast_domain<F>(X, Y, Cc) == ONES;
+    if (__all_sync(0xffffffffu, in_domain) && !(flags & 2u)) {
+      Gen<F, OP_MUL_ADD_FAST>::run(X, Y, Cc, Z);
+      return;
+    }
+  }
+  eval_unit<F, OP>(X, Y, Cc, Z);
+}
+
 // One thread per unit, grid-stride.  (A register double-buffered variant --
 // next unit's loads issued before the current network -- measured slower on
 // the B200: the extra registers cost more occupancy than the overlap gained.)
@@ -201,7 +227,7 @@ __global__ void __launch_bounds__(kThreads, arith_minb<F, OP>()) k_arith(const w
     // 1/5/10 and 1/6/9 mul loops with the release after the stores)
     if constexpr (arith_minb<F, OP>() > 1) pdl_release_if(u + stride >= units);
     w32 Z[N];
-    eval_unit<F, OP>(cur.v[0], cur.v[1], cur.v[NIN - 1], Z);
+    eval_unit_dyn<F, OP>(cur.v[0], cur.v[1], cur.v[NIN - 1], Z, flags);
     BFP_UNROLL for (int j = 0; j < N; ++j) st_stream(z + base + j * 32, Z[j]);
     if constexpr (arith_minb<F, OP>() <= 1) pdl_release_if(u + stride >= units);
   }

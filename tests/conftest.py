@@ -80,7 +80,8 @@ class HostCircuits:
         self.L = L
 
     def binop(self, op: str, fmt, px, py, pc=None, generated: bool = False):
-        code = {"add": 0, "sub": 1, "mul": 2, "div": 3, "mul_add": 4}[op] + (10 if generated else 0)
+        code = {"add": 0, "sub": 1, "mul": 2, "div": 3, "mul_add": 4, "mul_add_fast": 5,
+                "mul_add_domain": 6}[op] + (10 if generated else 0)
         nb = 1 + fmt[0] + fmt[1]
         z = np.zeros_like(px)
         rc = self.L.host_binop(code, fmt[0], fmt[1], fmt[2], fmt[3], px.ctypes.data, py.ctypes.data,
@@ -153,3 +154,51 @@ def related(x: np.ndarray, e: int, s: int, rng: np.random.Generator) -> np.ndarr
     d = rng.integers(0, 4, size=len(x), dtype=np.uint64)
     mask = np.uint64((1 << (1 + e + s)) - 1)
     return (x ^ flip ^ d) & mask
+
+
+# ------------------------------------------------- mul_add: the fast domain
+def fast_domain(e: int, s: int, a, b, c) -> np.ndarray:
+    """mul_add_fast_domain (csrc/bfp_circuits.cuh) restated on encodings: a, b
+    with nonzero exponent fields whose sum is >= 2^(e-1), c's exponent field
+    >= 2^KN, KN = clog2(s + 5)."""
+    kn = int(np.ceil(np.log2(s + 5)))
+    ea, eb, ec = ((np.asarray(v, dtype=np.uint64) >> np.uint64(s)) & np.uint64((1 << e) - 1) for v in (a, b, c))
+    return (ea != 0) & (eb != 0) & (ea + eb >= (1 << (e - 1))) & (ec >= (1 << kn))
+
+
+def fast_domain_operands(O, fmt, n: int, rng: np.random.Generator):
+    """(a, b, c), all n triples inside the fast domain, weighted towards its
+    edges: exponent sums at the bound, Inf / NaN / max-finite operands, c a few
+    ulps from -(a*b) (massive cancellation) or at the smallest allowed exponent."""
+    e, s = fmt[:2]
+    emax, kn = (1 << e) - 1, int(np.ceil(np.log2(s + 5)))
+    half, sign, fm = 1 << (e - 1), np.uint64(1 << (e + s)), np.uint64((1 << s) - 1)
+
+    def frac(k):
+        f = rng.integers(0, 1 << s, size=k, dtype=np.uint64)
+        edge = rng.integers(0, 8, size=k)
+        f[edge == 0] = 0
+        f[edge == 1] = (1 << s) - 1
+        f[edge == 2] = 1
+        return f
+
+    ea = rng.integers(1, emax + 1, size=n, dtype=np.uint64)
+    ea[rng.integers(0, 8, size=n) == 0] = emax  # Inf / NaN stay inside the domain
+    need = np.maximum(np.int64(1), half - ea.astype(np.int64))  # smallest eb allowed
+    span = emax - need + 1
+    eb = need + (rng.integers(0, 1 << 30, size=n) % span)
+    k = rng.integers(0, 4, size=n)
+    eb = np.where(k == 0, need, np.where(k == 1, np.minimum(need + 1, emax), eb)).astype(np.uint64)
+    a = (rng.integers(0, 2, size=n, dtype=np.uint64) << np.uint64(e + s)) | (ea << np.uint64(s)) | frac(n)
+    b = (rng.integers(0, 2, size=n, dtype=np.uint64) << np.uint64(e + s)) | (eb << np.uint64(s)) | frac(n)
+    ec = rng.integers(1 << kn, emax + 1, size=n, dtype=np.uint64)
+    ec[rng.integers(0, 4, size=n) == 0] = 1 << kn
+    c = (rng.integers(0, 2, size=n, dtype=np.uint64) << np.uint64(e + s)) | (ec << np.uint64(s)) | frac(n)
+    # a quarter: c = -(a*b) +- a few ulps where that stays inside the domain
+    q = n // 4
+    p = (O.binop("mul", fmt, a[:q], b[:q]) ^ sign) + rng.integers(0, 5, size=q, dtype=np.uint64) - np.uint64(2)
+    p &= np.uint64((1 << (1 + e + s)) - 1)
+    ok = fast_domain(e, s, a[:q], b[:q], p)
+    c[:q] = np.where(ok, p, c[:q])
+    assert fast_domain(e, s, a, b, c).all()
+    return a, b, c

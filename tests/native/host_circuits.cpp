@@ -48,6 +48,24 @@ static void run(int op, const uint32_t* x, const uint32_t* y, const uint32_t* c,
         case 2: mul_w<F>(X, Y, Z); break;
         case 3: div_w<F>(X, Y, Z); break;
         case 4: mul_add_w<F>(X, Y, C, Z); break;
+        // mul_add on its fast domain: template, generated cover, and the
+        // domain predicate itself (plane 0 = lanes inside the domain)
+        case 5:
+          if constexpr (mul_add_fast_ok<F>()) mul_add_fast_w<F>(X, Y, C, Z);
+          else return;
+          break;
+        case 15:
+          if constexpr (Gen<F, 5>::ok) Gen<F, 5>::run(X, Y, C, Z);
+          else return;
+          break;
+        case 6:
+          if constexpr (mul_add_fast_ok<F>()) {
+            for (int j = 0; j < N; ++j) Z[j] = 0;
+            Z[0] = mul_add_fast_domain<F>(X, Y, C);
+          } else {
+            return;
+          }
+          break;
         default: return;
       }
       for (int j = 0; j < N; ++j) z[(b * N + j) * 32 + t] = Z[j];

@@ -156,5 +156,7 @@ def test_arith_ex_flags_validated(L):
     import ctypes as C
     from paper_1602_04716_b200 import _lib
     f = _lib.BfpFormat(4, 3, 1, 0, b"")
-    assert L.bfp_arith_ex(0, C.byref(f), None, None, None, None, 0, None, 2) == _lib.BFP_EARG
+    assert L.bfp_arith_ex(0, C.byref(f), None, None, None, None, 0, None, 4) == _lib.BFP_EARG
     assert L.bfp_arith_ex(0, C.byref(f), None, None, None, None, 0, None, _lib.BFP_INPUTS_READY) == _lib.BFP_OK
+    assert L.bfp_arith_ex(4, C.byref(f), None, None, None, None, 0, None,
+                          _lib.BFP_INPUTS_READY | _lib.BFP_GENERAL_NETWORK) == _lib.BFP_OK

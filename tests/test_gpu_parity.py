@@ -19,7 +19,7 @@ import numpy as np
 import pytest
 import torch
 
-from conftest import FORMATS, MODES, ROOT, all_pairs, operands, related
+from conftest import FORMATS, MODES, ROOT, all_pairs, fast_domain, fast_domain_operands, operands, related
 
 import paper_1602_04716_b200 as bfp
 from paper_1602_04716_b200 import _lib, workloads as W
@@ -38,7 +38,7 @@ def cfmt(fmt):
     return _lib.BfpFormat(fmt[0], fmt[1], fmt[2], fmt[3], b"")
 
 
-def gpu_arith(op: str, fmt, px, py, pc=None) -> np.ndarray:
+def gpu_arith(op: str, fmt, px, py, pc=None, flags: int = 0) -> np.ndarray:
     L = _lib.lib()
     nb = 1 + fmt[0] + fmt[1]
     count = (len(px) // (nb * 32)) * 1024
@@ -46,9 +46,9 @@ def gpu_arith(op: str, fmt, px, py, pc=None) -> np.ndarray:
     dc = dev(pc) if pc is not None else None
     dz = torch.empty_like(dx)
     f = cfmt(fmt)
-    rc = L.bfp_arith(OPS[op], C.byref(f), dx.data_ptr(), dy.data_ptr(),
-                     dc.data_ptr() if dc is not None else None, dz.data_ptr(), count,
-                     torch.cuda.current_stream().cuda_stream)
+    rc = L.bfp_arith_ex(OPS[op], C.byref(f), dx.data_ptr(), dy.data_ptr(),
+                        dc.data_ptr() if dc is not None else None, dz.data_ptr(), count,
+                        torch.cuda.current_stream().cuda_stream, flags)
     assert rc == 0, _lib.lib().bfp_last_error()
     return dz.cpu().numpy().view(np.uint32)
 
@@ -107,6 +107,60 @@ def test_random_wide(oracle, fmt2, mode):
     c = operands(e, s, n, rng)
     for op in ("add", "sub", "mul", "div", "mul_add"):
         check(oracle, op, fmt2 + mode, x, y, c if op == "mul_add" else None)
+
+
+# mul_add kernels carry two covers (include/bfpgpu.h, BFP_GENERAL_NETWORK): a
+# warp runs the fast-domain one when its whole 1024-element block is inside
+# the domain.  Blocks wholly inside, blocks with one element outside, and the
+# general cover forced on the same operands: all equal the oracle's chain.
+FAST_FMTS = [f for f in FORMATS if f != (3, 2)]  # 1/3/2 has no fast cover (E = KN)
+
+
+@pytest.mark.parametrize("fmt2", FAST_FMTS)
+@pytest.mark.parametrize("mode", MODES)
+def test_mul_add_fast_and_general_covers(oracle, fmt2, mode):
+    fmt = fmt2 + mode
+    e, s = fmt2
+    nb = 1 + e + s
+    rng = np.random.default_rng(4242 + e * 64 + s + 7 * mode[0] + 13 * mode[1])
+    n = 1 << 19
+    a, b, c = fast_domain_operands(oracle, fmt, n, rng)
+    want = oracle.binop("mul_add", fmt, a, b, c)
+    planes = [oracle.pack_planes(v, nb) for v in (a, b, c)]
+    for flags in (0, 2):  # every block on the fast cover / the general cover forced
+        got = oracle.unpack_planes(gpu_arith("mul_add", fmt, *planes, flags=flags), n, nb)
+        assert np.array_equal(got, want), (fmt, flags, int((got != want).sum()))
+    # every other block gets ONE element outside the domain (a zero, a
+    # subnormal a, a tiny c): those warps take the general cover
+    a2, b2, c2 = a.copy(), b.copy(), c.copy()
+    blk = np.arange(0, n // 1024, 2)
+    pos = blk * 1024 + rng.integers(0, 1024, size=len(blk))
+    kind = rng.integers(0, 3, size=len(blk))
+    a2[pos[kind == 0]] = 0
+    a2[pos[kind == 1]] &= np.uint64((1 << s) - 1)
+    c2[pos[kind == 2]] &= np.uint64((1 << s) - 1) | np.uint64(1 << (e + s))
+    inside = fast_domain(e, s, a2, b2, c2).reshape(-1, 1024).all(axis=1)
+    assert inside[1::2].all() and not inside[0::2].any()
+    want2 = oracle.binop("mul_add", fmt, a2, b2, c2)
+    got2 = oracle.unpack_planes(gpu_arith("mul_add", fmt, *(oracle.pack_planes(v, nb) for v in (a2, b2, c2))), n, nb)
+    assert np.array_equal(got2, want2), (fmt, int((got2 != want2).sum()))
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_mul_add_fast_cover_every_triple_1_4_3(oracle, mode):
+    """Every (a, b, c) of 1/4/3 inside the fast domain, packed so that each
+    block is wholly inside it: the fast cover over its entire domain."""
+    fmt = (4, 3) + mode
+    v = np.arange(1 << 8, dtype=np.uint64)
+    a, b, c = (g.ravel() for g in np.meshgrid(v, v, v, indexing="ij"))
+    keep = fast_domain(4, 3, a, b, c)
+    a, b, c = a[keep], b[keep], c[keep]
+    pad = -len(a) % 1024  # repeat the last triple: the tail block stays inside
+    a, b, c = (np.concatenate([x, np.repeat(x[-1:], pad)]) for x in (a, b, c))
+    assert len(a) >= 1 << 21
+    want = oracle.binop("mul_add", fmt, a, b, c)
+    got = oracle.unpack_planes(gpu_arith("mul_add", fmt, *(oracle.pack_planes(x, 8) for x in (a, b, c))), len(a), 8)
+    assert np.array_equal(got, want), (fmt, int((got != want).sum()))
 
 
 def test_golden_gpu(oracle):

@@ -50,7 +50,7 @@ def sass_functions(lib: Path) -> dict[str, list[str]]:
             continue
         m = re.match(r"\s*/\*([0-9a-f]+)\*/\s+(@!?U?P\w+\s+)?([A-Z][A-Z0-9_.]*)(.*)", line)
         if m:
-            funcs[cur].append((int(m.group(1), 16), m.group(3), m.group(4)))
+            funcs[cur].append((int(m.group(1), 16), m.group(3), m.group(4), (m.group(2) or "").strip()))
     return funcs
 
 
@@ -58,7 +58,7 @@ def loop_body(ins: list) -> list[str]:
     """Opcodes of the main loop: the span of the widest backward branch (the
     grid-stride loop of the kernels; empty if there is none)."""
     best = None
-    for a, op, rest in ins:
+    for a, op, rest, _ in ins:
         if op.startswith("BRA"):
             t = re.search(r"0x([0-9a-f]+)", rest)
             if t and int(t.group(1), 16) < a:
@@ -67,7 +67,43 @@ def loop_body(ins: list) -> list[str]:
                     best = (lo, a)
     if best is None:
         return []
-    return [op for a, op, _ in ins if best[0] <= a <= best[1]]
+    return [op for a, op, _, _ in ins if best[0] <= a <= best[1]]
+
+
+def cover_paths(ins: list) -> dict | None:
+    """mul_add kernels hold two LOP3 covers behind one warp-uniform branch
+    (`@P BRA else; <cover 1>; BRA join; else: <cover 2>; join:`, both forward,
+    inside the loop).  Returns the LOP3 count a unit executes on each side --
+    the whole function minus the OTHER cover -- as {"fast", "general"} (the
+    fast-domain cover is the smaller one), or None without that shape."""
+    addr = {i[0]: k for k, i in enumerate(ins)}
+
+    def target(rest):
+        t = re.search(r"0x([0-9a-f]+)", rest)
+        return int(t.group(1), 16) if t else None
+
+    best = None
+    for k, (a, op, rest, pred) in enumerate(ins):
+        if not (op.startswith("BRA") and pred):  # predicated forward branch
+            continue
+        els = target(rest)
+        if els is None or els <= a or els not in addr:
+            continue
+        ke = addr[els]
+        jop = ins[ke - 1]
+        if not jop[1].startswith("BRA") or jop[3]:
+            continue
+        join = target(jop[2])
+        if join is None or join <= els or join not in addr:
+            continue
+        c1 = sum(1 for i in ins[k + 1:ke] if i[1].startswith("LOP3"))
+        c2 = sum(1 for i in ins[ke:addr[join]] if i[1].startswith("LOP3"))
+        if min(c1, c2) >= 64 and (best is None or c1 + c2 > sum(best)):
+            best = (c1, c2)
+    if best is None:
+        return None
+    total = sum(1 for i in ins if i[1].startswith("LOP3"))
+    return {"fast": total - max(best), "general": total - min(best), "covers": sorted(best)}
 
 
 def stats(lib: Path = LIB, pattern: str | None = None) -> dict[str, dict]:
@@ -78,7 +114,7 @@ def stats(lib: Path = LIB, pattern: str | None = None) -> dict[str, dict]:
         pretty = dm.get(name, name)
         if pattern and not re.search(pattern, pretty):
             continue
-        ins = [op for _, op, _ in tins]
+        ins = [op for _, op, _, _ in tins]
         body = Counter(i.split(".")[0] for i in loop_body(tins))
         base = Counter(i.split(".")[0] for i in ins)
         alu = sum(v for k, v in base.items() if k in ALU_PIPE)
@@ -95,6 +131,9 @@ def stats(lib: Path = LIB, pattern: str | None = None) -> dict[str, dict]:
             "loop_total": sum(body.values()),
             "top": base.most_common(8),
         }
+        paths = cover_paths(tins)
+        if paths:
+            res[pretty]["paths"] = paths
     return res
 
 
@@ -109,7 +148,9 @@ def main() -> None:
         short = re.sub(r"bfpg::|Format<|unsigned int|const", "", name)[:90]
         print(f"{short:90s} tot={r['total']:5d} LOP3={r['LOP3']:5d} alu={r['alu_pipe']:5d} "
               f"fma={r['fma_pipe']:4d} mem={r['mem']:3d} loop: LOP3={r['loop_LOP3']:5d} "
-              f"alu={r['loop_alu_pipe']:5d}  LOP3/elem={r['LOP3'] / 32:.2f}")
+              f"alu={r['loop_alu_pipe']:5d}  LOP3/elem={r['LOP3'] / 32:.2f}"
+              + (f"  two covers {r['paths']['covers']}: fast path {r['paths']['fast'] / 32:.2f}, "
+                 f"general {r['paths']['general'] / 32:.2f} LOP3/elem" if r.get("paths") else ""))
     if a.json:
         Path(a.json).write_text(json.dumps(res, indent=1))
 
