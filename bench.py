@@ -1250,11 +1250,11 @@ def build_line(cfg: str, res: dict, args, D: Dist, probes: dict, traffic: dict) 
                 {key: aent[key] for key in ("gelem_s", "bound", "frac", "ms", "hbm_frac", "logic_frac",
                                             "logic_frac_at_load_clock", "lop3_per_elem") if key in aent},
                 config=cfg, note="same launch with BFP_GENERAL_NETWORK: every warp runs the general cover "
-                                 "(the one taken when a block holds zeros, subnormals or a small c); not part "
+                                 "(the one taken when a block holds a zero, subnormal, Inf, NaN, huge or tiny operand); not part "
                                  "of the step")
             per_format[j.fmt][j.op]["cover"] = (
-                "fast-domain cover: this workload's operands (normal a, b with ea + eb >= bias + 1, "
-                "ec >= 16) pass the per-block test in every warp")
+                "fast-domain cover: this workload's operands (finite normals, exponent fields 21..41: "
+                "1 <= ea, eb < 48, 32 <= ea + eb <= 91, 16 <= ec < 48) pass the per-block test in every warp")
     k_dom = max(range(len(jobs)), key=lambda k: res["kern_ms"][k])
     jd = jobs[k_dom]
     t_dom = None

@@ -140,11 +140,14 @@ bfp_status bfp_arith(int op, const bfp_format* f, const uint32_t* d_x, const uin
 #define BFP_INPUTS_READY 1u
 /* BFP_GENERAL_NETWORK: mul_add kernels carry two LOP3 covers -- the general
  * network and a smaller one valid when every element of a 1024-element block
- * has normal (or Inf / NaN) a and b whose product cannot land below the normal
- * range and a c of not-too-small exponent (csrc/bfp_circuits.cuh,
- * mul_add_fast_domain); each warp tests its block and picks one.  Results are
- * identical either way.  This flag forces the general cover (tests, A/B
- * measurement); it is ignored by the other operations. */
+ * lies in the "fast domain": a, b, c finite normals of moderate exponent whose
+ * product can neither leave the normal range nor come near overflow, and a c
+ * that is not tiny (exact bounds: csrc/bfp_circuits.cuh, mul_add_fast_domain;
+ * for 1/6/9: 1 <= ea, eb < 48, 32 <= ea + eb <= 91, 16 <= ec < 48 on the
+ * biased exponent fields).  Each warp tests its block and picks one cover;
+ * zeros, subnormals, Inf and NaN take the general one.  Results are identical
+ * either way.  This flag forces the general cover (tests, A/B measurement);
+ * it is ignored by the other operations. */
 #define BFP_GENERAL_NETWORK 2u
 bfp_status bfp_arith_ex(int op, const bfp_format* f, const uint32_t* d_x, const uint32_t* d_y,
                         const uint32_t* d_c, uint32_t* d_z, size_t count, void* stream,

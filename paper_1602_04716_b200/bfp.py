@@ -318,7 +318,8 @@ def _check_planes(v: bfp_vector, like: bfp_vector, what: str) -> None:
 
 
 def _binop(op: int, x: bfp_vector, y: bfp_vector, c: bfp_vector | None = None,
-           out: bfp_vector | None = None, inputs_ready: bool = False) -> bfp_vector:
+           out: bfp_vector | None = None, inputs_ready: bool = False,
+           general_network: bool = False) -> bfp_vector:
     require_same_shape(x.spec, y.spec)
     if c is not None:
         require_same_shape(x.spec, c.spec)
@@ -333,18 +334,20 @@ def _binop(op: int, x: bfp_vector, y: bfp_vector, c: bfp_vector | None = None,
     z = out if out is not None else empty(x.spec, x.count, x.planes.device)
     check(lib().bfp_arith_ex(op, x.spec.c, x.planes.data_ptr(), y.planes.data_ptr(),
                              c.planes.data_ptr() if c is not None else None, z.planes.data_ptr(),
-                             x.count, _stream(), 1 if inputs_ready else 0),
+                             x.count, _stream(), (1 if inputs_ready else 0) | (2 if general_network else 0)),
           ("add", "sub", "mul", "div", "mul_add")[op])
     return z
 
 
 def arith(op: int, x: bfp_vector, y: bfp_vector, c: bfp_vector | None = None,
-          out: bfp_vector | None = None, inputs_ready: bool = False) -> bfp_vector:
+          out: bfp_vector | None = None, inputs_ready: bool = False,
+          general_network: bool = False) -> bfp_vector:
     """bfp_arith_ex: op 0 add, 1 sub, 2 mul, 3 div, 4 mul_add.  inputs_ready
     (BFP_INPUTS_READY) asserts that no work still running on the stream
     writes x / y / c, letting the kernel's first loads overlap the previous
-    kernel's tail."""
-    return _binop(op, x, y, c, out, inputs_ready)
+    kernel's tail.  general_network (BFP_GENERAL_NETWORK) forces mul_add onto
+    its general LOP3 cover (same results; include/bfpgpu.h)."""
+    return _binop(op, x, y, c, out, inputs_ready, general_network)
 
 
 def bfp_add(x: bfp_vector, y: bfp_vector, out: bfp_vector | None = None) -> bfp_vector:

@@ -255,10 +255,11 @@ struct Gen {
 // ================================================================= ADD
 // Z = X + Y (SUB: X - Y).  bfp_add / bfp_sub semantics, arith.hpp:235-328.
 //
-// FAST: the caller guarantees (mul_add_fast_domain below) that both exponent
-// fields are nonzero and the larger one is >= 2^KN, so the hidden bits are
-// constant ones and the normaliser's budget never binds; every signal equals
-// the general network's on that domain.
+// FAST: the caller guarantees (mul_add_fast_domain below) that both operands
+// are finite normals, the larger exponent field is >= 2^KN and <= 2^E - 3: the
+// hidden bits are constant ones, the normaliser's budget never binds, nothing
+// is special and the sum cannot overflow; every signal replaced by a constant
+// here has that value in the general network on that domain.
 template <class F, bool SUB, bool FAST = false>
 BFP_HD void add_w(const w32* X, const w32* Y, w32* Z) {
   constexpr int E = F::E, S = F::S, M = E + S;
@@ -410,12 +411,14 @@ BFP_HD void add_w(const w32* X, const w32* Y, w32* Z) {
     bs &= B[S + i];
   }
   BFP_UNROLL for (int i = 0; i < S; ++i) afz |= A[i];
+  if constexpr (FAST) as = bs = 0;
   const w32 use_nan = as & (afz | (bs & eff));
 
   // Overflow: exponent sum >= 2^E - 1.
   w32 eall = ONES;
   BFP_UNROLL for (int i = 0; i < E; ++i) eall &= ex[i];
-  const w32 ovf = ex[E] | eall;
+  w32 ovf = ex[E] | eall;
+  if constexpr (FAST) ovf = ex[E] = 0;
 
   // Fraction mask: keep unless special, overflow (RN: Inf) or FTZ flush.
   w32 keep = ~as;
@@ -447,7 +450,8 @@ BFP_HD void add_w(const w32* X, const w32* Y, w32* Z) {
 // then overflow (Inf under RN, max-finite under RZ), FTZ after rounding
 // (still below the smallest normal) and the special-value overrides:
 // zero_res / inf_res force a signed zero / Inf, use_nan the canonical NaN.
-// FAST: ez >= 0 is guaranteed (no subnormal-range shift, no flush).
+// FAST: 0 <= ez <= 2^E - 4 is guaranteed (no subnormal-range shift, no flush,
+// no overflow).
 template <class F, int EW, bool FAST = false>
 BFP_HD void finish_round(w32* R, const w32* ez, w32 sign, w32 zero_res, w32 inf_res, w32 use_nan,
                          w32* Z) {
@@ -490,7 +494,8 @@ BFP_HD void finish_round(w32* R, const w32* ez, w32 sign, w32 zero_res, w32 inf_
   // ez bits above E (only when EW > E + 2): a positive ez >= 2^(E+1) overflows
   w32 high = 0;
   BFP_UNROLL for (int i = E + 1; i < EW - 1; ++i) high |= ez[i];
-  const w32 ovf = ex[E] | ex[E + 1] | eall | (high & ~sub);
+  w32 ovf = ex[E] | ex[E + 1] | eall | (high & ~sub);
+  if constexpr (FAST) ovf = 0;
 
   BFP_STAGE("fr.specials_out");
   w32 flush = 0;
@@ -746,10 +751,13 @@ BFP_HD void sig_product_best(const w32* a, const w32* b, w32* P) {
 // product, then in [2^2S, 2^(2S+2)), needs a single 1-bit normalise instead of
 // a log shifter over all 2S+2 product bits.
 //
-// FAST: both exponent fields are nonzero and their sum is >= 2^(E-1) = bias + 1
-// (mul_add_fast_domain), so neither operand needs normalising and the biased
-// result exponent minus one, ez, is >= 0: the pre-product normaliser and the
-// subnormal-range shifter of finish_round fold away.
+// FAST: both operands are finite normals and the sum of their exponent fields
+// lies in [2^(E-1), 2^E + 2^(E-1) - 5] (mul_add_fast_domain): neither operand
+// needs normalising, the biased result exponent minus one, ez = ea + eb - bias
+// - 1 + top, is >= 0 and the rounded result's field ez + 1 (+1 on a rounding
+// carry when top = 0) is <= 2^E - 3 -- the pre-product normaliser, the
+// subnormal-range shifter, the special-value masks and the overflow path of
+// finish_round fold away.
 template <class F, bool FAST = false>
 BFP_HD void mul_w(const w32* X, const w32* Y, w32* Z) {
   constexpr int E = F::E, S = F::S, M = E + S;
@@ -761,7 +769,7 @@ BFP_HD void mul_w(const w32* X, const w32* Y, w32* Z) {
   Classes cx = classify<F>(X), cy = classify<F>(Y);
   if constexpr (FAST) {
     cx.h = cy.h = ONES;
-    cx.z = cy.z = 0;
+    cx.z = cy.z = cx.s = cy.s = cx.inf = cy.inf = cx.nan = cy.nan = 0;
   }
 
   constexpr int WP = 2 * S + 2;
@@ -981,38 +989,54 @@ BFP_HD void mul_add_w(const w32* A, const w32* B, const w32* Cc, w32* Z) {
 }
 
 // ------------------------------------------------- mul_add: the fast domain
-// Most data never touches the subnormal machinery of the chain, which is a
-// fifth of its LUTs (operand normaliser, subnormal-range shifter, normaliser
-// budget).  A unit whose 32 elements ALL satisfy
-//   ea != 0, eb != 0            a, b normal (or Inf / NaN),
-//   ea + eb >= 2^(E-1)          the product cannot land below the normal range
-//                               (ez = ea + eb - bias - 1 + top >= 0),
-//   ec >= 2^KN                  the sum's exponent max(ep, ec) exceeds every
-//                               normalising shift, KN = clog2(S + 5),
-// may run mul_add_fast_w: the same network with those signals constant.  Inf
-// and NaN operands stay inside the domain (their masks are unchanged); zeros
-// and subnormals of a, b, and small c, fall back to the general network.  The
-// kernels evaluate the predicate per unit and vote per warp (bfp_kernels.cuh),
-// so a warp takes ONE of the two covers; results are identical either way
-// (tests: every triple of 1/4/3 inside the domain, and the GPU sweeps run
-// with the fast cover both enabled and disabled).
+// Most data never touches the subnormal, special-value and overflow machinery
+// of the chain, which is 30% of its LUTs (operand normaliser, subnormal-range
+// shifter, normaliser budget, Inf / NaN masks, overflow tests).  A unit whose
+// 32 elements ALL satisfy, with ea, eb, ec the biased exponent fields,
+//   1 <= ea, eb < 3 * 2^(E-2)       a, b finite normals (top two exponent bits
+//                                   not both set: magnitudes < 2^(2^(E-2)+1)),
+//   2^(E-1) <= ea + eb              the product cannot land below the normal
+//                                   range (ez = ea + eb - bias - 1 + top >= 0),
+//   ea + eb <= 2^E + 2^(E-1) - 5    nor reach the top two binades: the rounded
+//                                   product's field is <= ea + eb - bias + 1
+//                                   <= 2^E - 3,
+//   2^KN <= ec < 3 * 2^(E-2)        the sum's exponent max(ep, ec) exceeds every
+//                                   normalising shift (KN = clog2(S + 5)) and
+//                                   max(ep, ec) + 1 <= 2^E - 2 is finite,
+// may run mul_add_fast_w: the same network with those signals constant.
+// Zeros, subnormals, Inf, NaN, huge or tiny operands fall back to the general
+// network.  The kernels evaluate the predicate per unit and vote per warp
+// (bfp_kernels.cuh), so a warp takes ONE of the two covers; results are
+// identical either way (tests: every triple of 1/4/3 inside the domain, on the
+// host and on the GPU, and the GPU sweeps with the fast cover enabled and
+// disabled).
 template <class F>
 constexpr bool mul_add_fast_ok() {
-  return F::E > clog2(F::S + 5) && (1 - F::BIAS) <= -F::S - 1;
+  return F::E > clog2(F::S + 5) && F::E >= 4 && (1 - F::BIAS) <= -F::S - 1;
 }
 
 // Lanes of the unit inside the fast domain.
 template <class F>
 BFP_HD w32 mul_add_fast_domain(const w32* A, const w32* B, const w32* Cc) {
   constexpr int E = F::E, S = F::S, KN = clog2(S + 5);
-  w32 ha = 0, hb = 0, cbig = 0, cy = 0;
+  const w32* ea = A + S;
+  const w32* eb = B + S;
+  const w32* ec = Cc + S;
+  w32 ha = 0, hb = 0, cbig = 0;
   BFP_UNROLL for (int i = 0; i < E; ++i) {
-    ha |= A[S + i];
-    hb |= B[S + i];
+    ha |= ea[i];
+    hb |= eb[i];
   }
-  BFP_UNROLL for (int i = KN; i < E; ++i) cbig |= Cc[S + i];
-  BFP_UNROLL for (int i = 0; i < E - 1; ++i) cy = maj(A[S + i], B[S + i], cy);
-  return ha & hb & cbig & (cy | A[S + E - 1] | B[S + E - 1]);
+  BFP_UNROLL for (int i = KN; i < E; ++i) cbig |= ec[i];
+  const w32 small = ~(ea[E - 1] & ea[E - 2]) & ~(eb[E - 1] & eb[E - 2]) & ~(ec[E - 1] & ec[E - 2]);
+  // t = ea + eb (E+1 bits): in range iff exactly one of t[E], t[E-1] is set
+  // (2^(E-1) <= t < 2^E + 2^(E-1)) and not (t[E-1] = 0 with t[E-2..2] all ones:
+  // t >= 2^E + 2^(E-1) - 4)
+  w32 t[E + 1];
+  t[E] = add_k<E>(ea, eb, 0, t);
+  w32 top4 = ~t[E - 1];
+  BFP_UNROLL for (int i = 2; i <= E - 2; ++i) top4 &= t[i];
+  return ha & hb & cbig & small & (t[E] ^ t[E - 1]) & ~top4;
 }
 
 template <class F>

@@ -337,7 +337,7 @@ __global__ void __launch_bounds__(kThreads) k_arith_bulk(const w32* __restrict__
       phase ^= 1u;
     }
     w32 Z[N];
-    eval_unit<F, OP>(ops[0], ops[1], ops[NIN - 1], Z);
+    eval_unit_dyn<F, OP>(ops[0], ops[1], ops[NIN - 1], Z, 0u);  // the warp is converged here
     w32* zb = z + b * size_t(TW) + lane;
     BFP_UNROLL for (int j = 0; j < N; ++j) st_stream(zb + j * 32, Z[j]);
     pdl_release_if(b + tw >= nblocks);  // in-loop: see pdl_release_if (no per-access R2UR)

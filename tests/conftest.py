@@ -158,21 +158,25 @@ def related(x: np.ndarray, e: int, s: int, rng: np.random.Generator) -> np.ndarr
 
 # ------------------------------------------------- mul_add: the fast domain
 def fast_domain(e: int, s: int, a, b, c) -> np.ndarray:
-    """mul_add_fast_domain (csrc/bfp_circuits.cuh) restated on encodings: a, b
-    with nonzero exponent fields whose sum is >= 2^(e-1), c's exponent field
-    >= 2^KN, KN = clog2(s + 5)."""
+    """mul_add_fast_domain (csrc/bfp_circuits.cuh) restated on encodings, with
+    ea, eb, ec the exponent fields and KN = clog2(s + 5):
+    1 <= ea, eb < 3*2^(e-2);  2^(e-1) <= ea + eb <= 2^e + 2^(e-1) - 5;
+    2^KN <= ec < 3*2^(e-2)."""
     kn = int(np.ceil(np.log2(s + 5)))
     ea, eb, ec = ((np.asarray(v, dtype=np.uint64) >> np.uint64(s)) & np.uint64((1 << e) - 1) for v in (a, b, c))
-    return (ea != 0) & (eb != 0) & (ea + eb >= (1 << (e - 1))) & (ec >= (1 << kn))
+    cap = 3 << (e - 2)
+    return ((ea != 0) & (eb != 0) & (ea < cap) & (eb < cap) & (ea + eb >= (1 << (e - 1)))
+            & (ea + eb <= (1 << e) + (1 << (e - 1)) - 5) & (ec >= (1 << kn)) & (ec < cap))
 
 
 def fast_domain_operands(O, fmt, n: int, rng: np.random.Generator):
     """(a, b, c), all n triples inside the fast domain, weighted towards its
-    edges: exponent sums at the bound, Inf / NaN / max-finite operands, c a few
-    ulps from -(a*b) (massive cancellation) or at the smallest allowed exponent."""
+    edges: exponent sums at both bounds, all-ones / zero fractions, c a few ulps
+    from -(a*b) (massive cancellation) or at the ends of its exponent range."""
     e, s = fmt[:2]
-    emax, kn = (1 << e) - 1, int(np.ceil(np.log2(s + 5)))
-    half, sign, fm = 1 << (e - 1), np.uint64(1 << (e + s)), np.uint64((1 << s) - 1)
+    kn = int(np.ceil(np.log2(s + 5)))
+    cap, lo, hi = 3 << (e - 2), 1 << (e - 1), (1 << e) + (1 << (e - 1)) - 5
+    sign = np.uint64(1 << (e + s))
 
     def frac(k):
         f = rng.integers(0, 1 << s, size=k, dtype=np.uint64)
@@ -182,18 +186,17 @@ def fast_domain_operands(O, fmt, n: int, rng: np.random.Generator):
         f[edge == 2] = 1
         return f
 
-    ea = rng.integers(1, emax + 1, size=n, dtype=np.uint64)
-    ea[rng.integers(0, 8, size=n) == 0] = emax  # Inf / NaN stay inside the domain
-    need = np.maximum(np.int64(1), half - ea.astype(np.int64))  # smallest eb allowed
-    span = emax - need + 1
-    eb = need + (rng.integers(0, 1 << 30, size=n) % span)
-    k = rng.integers(0, 4, size=n)
-    eb = np.where(k == 0, need, np.where(k == 1, np.minimum(need + 1, emax), eb)).astype(np.uint64)
-    a = (rng.integers(0, 2, size=n, dtype=np.uint64) << np.uint64(e + s)) | (ea << np.uint64(s)) | frac(n)
-    b = (rng.integers(0, 2, size=n, dtype=np.uint64) << np.uint64(e + s)) | (eb << np.uint64(s)) | frac(n)
-    ec = rng.integers(1 << kn, emax + 1, size=n, dtype=np.uint64)
-    ec[rng.integers(0, 4, size=n) == 0] = 1 << kn
-    c = (rng.integers(0, 2, size=n, dtype=np.uint64) << np.uint64(e + s)) | (ec << np.uint64(s)) | frac(n)
+    ea = rng.integers(1, cap, size=n).astype(np.int64)
+    lo_b = np.maximum(1, lo - ea)            # smallest / largest eb allowed beside ea
+    hi_b = np.minimum(cap - 1, hi - ea)
+    eb = lo_b + (rng.integers(0, 1 << 30, size=n) % (hi_b - lo_b + 1))
+    k = rng.integers(0, 6, size=n)
+    eb = np.where(k == 0, lo_b, np.where(k == 1, hi_b, np.where(k == 2, np.minimum(lo_b + 1, hi_b), eb)))
+    ec = rng.integers(1 << kn, cap, size=n).astype(np.int64)
+    k = rng.integers(0, 6, size=n)
+    ec = np.where(k == 0, 1 << kn, np.where(k == 1, cap - 1, ec))
+    a, b, c = ((rng.integers(0, 2, size=n, dtype=np.uint64) << np.uint64(e + s)) | (x.astype(np.uint64) << np.uint64(s))
+               | frac(n) for x in (ea, eb, ec))
     # a quarter: c = -(a*b) +- a few ulps where that stays inside the domain
     q = n // 4
     p = (O.binop("mul", fmt, a[:q], b[:q]) ^ sign) + rng.integers(0, 5, size=q, dtype=np.uint64) - np.uint64(2)

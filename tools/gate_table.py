@@ -33,11 +33,16 @@ def table(modes=((1, 0), (0, 0))) -> list[dict]:
                 ref = O.ref_gate_count(op, (e, s, rn, ftz))["total"] if O.ref_available() else None
                 key = (f"k_arith<bfpg::Format<{e}, {s}, {'true' if rn else 'false'}, "
                        f"{'true' if ftz else 'false'}>, {code}>")
-                ours = next((r["LOP3"] for n, r in st.items() if key in n), None)
-                rows.append({"fmt": f"1/{e}/{s}", "mode": ("rn" if rn else "rz") + ("+ftz" if ftz else ""),
-                             "op": op, "ref_gates_per_elem": None if ref is None else ref / 32,
-                             "ours_lop3_per_elem": None if ours is None else ours / 32,
-                             "ratio": None if (ref is None or not ours) else ref / ours})
+                ent = next((r for n, r in st.items() if key in n), None)
+                # mul_add kernels hold two covers (sass_stats.cover_paths): one row per path
+                variants = ([(op, ent["LOP3"])] if not ent.get("paths") else
+                            [(op + " (general cover)", ent["paths"]["general"]),
+                             (op + " (fast-domain cover)", ent["paths"]["fast"])]) if ent else [(op, None)]
+                for name, ours in variants:
+                    rows.append({"fmt": f"1/{e}/{s}", "mode": ("rn" if rn else "rz") + ("+ftz" if ftz else ""),
+                                 "op": name, "ref_gates_per_elem": None if ref is None else ref / 32,
+                                 "ours_lop3_per_elem": None if ours is None else ours / 32,
+                                 "ratio": None if (ref is None or not ours) else ref / ours})
     return rows
 
 
