@@ -1247,8 +1247,9 @@ def build_line(cfg: str, res: dict, args, D: Dist, probes: dict, traffic: dict) 
             # the same kernel forced onto its general cover (BFP_GENERAL_NETWORK), same operands
             aent = op_entry(j, ams, nt, peaks, probes.get("lop3"), res["clocks"], path="general")
             per_format[j.fmt][f"{j.op} ({name.split(':')[1]})"] = dict(
+                # (no load-clock fraction: the clocks were sampled during the step, not this launch)
                 {key: aent[key] for key in ("gelem_s", "bound", "frac", "ms", "hbm_frac", "logic_frac",
-                                            "logic_frac_at_load_clock", "lop3_per_elem") if key in aent},
+                                            "lop3_per_elem") if key in aent},
                 config=cfg, note="same launch with BFP_GENERAL_NETWORK: every warp runs the general cover "
                                  "(the one taken when a block holds a zero, subnormal, Inf, NaN, huge or tiny operand); not part "
                                  "of the step")
