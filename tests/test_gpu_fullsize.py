@@ -9,7 +9,7 @@ tests/test_oracle.py) on all host threads (orc_verify):
   * C3: 1/5/10 pack_f32 of both operands, add, mul and unpack_f32 at 2^28;
   * C4: add and mul of every sweep format at 2^28;
   * the fused mul_add network (its own LOP3 cover, not the composition of the
-    mul and add covers): 1/6/9 over ALL 2^32 (a, b) pairs for 32 c values
+    mul and add covers): 1/6/9 over ALL 2^32 (a, b) pairs for 36 c values
     (signed zeros, subnormals, 1, max finite, Inf, NaN, random) -- RN +
     gradual by default, RZ + FTZ too with BFP_EXHAUSTIVE16=all (~4 min each)
     -- and ALL 2^24 (a, b, c) triples of 1/4/3 and 2^18 of 1/3/2 in every mode.
@@ -123,7 +123,10 @@ def test_c4_full_2e28(oracle, fmt2):
 # c values for the all-pairs sweep of 1/6/9 (sign 15, exponent 9..14, fraction 0..8)
 C_1_6_9 = [0x0000, 0x8000, 0x0001, 0x8001, 0x01FF, 0x81FF, 0x0200, 0x8200, 0x3E00, 0xBE00, 0x3E01, 0xBDFF,
            0x7DFF, 0xFDFF, 0x7C00, 0xFC01, 0x7E00, 0xFE00, 0x7F00, 0x7E01, 0xFF00, 0x0400, 0x0401, 0x2001,
-           0x5A5A, 0xA5A5, 0x1234, 0x9876, 0x4321, 0xC0DE, 0x3FFF, 0x0100]
+           0x5A5A, 0xA5A5, 0x1234, 0x9876, 0x4321, 0xC0DE, 0x3FFF, 0x0100,
+           # both ends of the fast domain's c range (exponent fields 16 and 47): with the 11 values above whose
+           # field lies in [16, 48), every block of (a, b) inside the domain runs the fast-domain cover
+           0x2000, 0xA1FF, 0x5FFF, 0xDE00]
 
 
 MODES_PAIRS = [(1, 0), (0, 1)] if os.environ.get("BFP_EXHAUSTIVE16") == "all" else [(1, 0)]
@@ -131,7 +134,7 @@ MODES_PAIRS = [(1, 0), (0, 1)] if os.environ.get("BFP_EXHAUSTIVE16") == "all" el
 
 @pytest.mark.parametrize("mode", MODES_PAIRS)
 def test_mul_add_all_pairs_1_6_9(oracle, mode):
-    """The fused cover over every (a, b) of 1/6/9 for 32 fixed c values."""
+    """The fused covers (general and fast-domain) over every (a, b) of 1/6/9 for 36 fixed c values."""
     rn, ftz = mode
     spec = bfp.make_spec(6, 9, rn, ftz)
     fmt = (6, 9, rn, ftz)

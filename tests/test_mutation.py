@@ -19,6 +19,11 @@ parity suite runs, against the oracle:
     with zero / subnormal / near-overflow / special weighting) must kill
     every mutant that a 64x larger uniform sample kills.
 
+  * the same for mul_add's SECOND cover (the fast-domain one, Gen<F, 5>), run
+    as the kernels run it -- inside the domain, the general cover elsewhere:
+    1/4/3 over all 2^24 triples, 1/6/9 with the suite's in-domain operand
+    generator against a 64x larger uniform in-domain sample.
+
 The unmutated copy passes, so the kills are the mutations'.
 Log of a run: profiles/r02_mutation.log.
 """
@@ -32,7 +37,7 @@ import subprocess
 import numpy as np
 import pytest
 
-from conftest import ROOT, operands
+from conftest import ROOT, fast_domain_operands, operands
 
 CSRC = ROOT / "paper_1602_04716_b200" / "csrc"
 HARNESS = ROOT / "tests" / "native" / "mutant_harness.cpp"
@@ -187,6 +192,57 @@ def test_cover_lut_mutants_6_9_mul_add(tmp_path, oracle):
         ks, kb = bool(suite.killed(L, 10)), bool(big.killed(L, 10))
         res.append((what, ks, kb))
         print(f"1/6/9 mul_add {what}: suite {'killed' if ks else 'survived'}, "
+              f"64x sample {'killed' if kb else 'survived'}")
+    assert not [r for r in res if r[2] and not r[1]], "a mutant escaped the suite's sample but not a larger one"
+    assert sum(r[1] for r in res) >= 0.6 * len(res)
+
+
+# ------------------------------------------- mul_add's fast-domain cover
+def test_fast_cover_lut_mutants_4_3(tmp_path, exhaustive_4_3):
+    """Gen<F, 5> of 1/4/3 over every triple (it runs on the 1.54 M inside the
+    domain): survivors are equivalent on the whole domain."""
+    rng = np.random.default_rng(0x5eed5)
+    src = (CSRC / "gen" / "gen_4_3.cuh").read_text()
+    L = _build(tmp_path, "clean_fast43")
+    assert exhaustive_4_3.killed(L, 15 - OPC["mul_add"], ["mul_add"]) == []
+    res = []
+    for k in range(8):
+        mutated, what = _flip_lut(src, (4, 3), 5, int(rng.integers(0, 10_000)), rng)
+        L = _build(tmp_path, f"fast43_{k}", mutate_gen=lambda s, m=mutated: m)
+        res.append((what, bool(exhaustive_4_3.killed(L, 15 - OPC["mul_add"], ["mul_add"]))))
+    for what, kd in res:
+        print(f"1/4/3 mul_add fast cover {what}: {'killed' if kd else 'equivalent on the whole domain'}")
+    assert sum(kd for _, kd in res) >= 0.6 * len(res)
+
+
+def test_fast_cover_lut_mutants_6_9(tmp_path, oracle):
+    """C5's cover: the suite's in-domain operand generator (2^16 triples,
+    edge-weighted) kills every mutant a 64x larger uniform in-domain sample kills."""
+    fmt = (6, 9, 1, 0)
+    rng = np.random.default_rng(17)
+    n = 1 << 16
+    suite = Cases(oracle, fmt, {"mul_add": fast_domain_operands(oracle, fmt, n, rng)})
+    br = np.random.default_rng(18)
+    m = 64 * n
+    sg = lambda: br.integers(0, 2, size=m, dtype=np.uint64) << np.uint64(15)
+    fr = lambda: br.integers(0, 512, size=m, dtype=np.uint64)
+    ea = br.integers(1, 48, size=m)
+    lo_b, hi_b = np.maximum(1, 32 - ea), np.minimum(47, 91 - ea)
+    eb = lo_b + br.integers(0, 1 << 30, size=m) % (hi_b - lo_b + 1)
+    ec = br.integers(16, 48, size=m)
+    big = Cases(oracle, fmt, {"mul_add": tuple(sg() | (x.astype(np.uint64) << np.uint64(9)) | fr()
+                                               for x in (ea, eb, ec))})
+    code = 15 - OPC["mul_add"]
+    L = _build(tmp_path, "clean_fast69", (6, 9))
+    assert suite.killed(L, code, ["mul_add"]) == [] and big.killed(L, code, ["mul_add"]) == []
+    src = (CSRC / "gen" / "gen_6_9.cuh").read_text()
+    res = []
+    for k in range(12):
+        mutated, what = _flip_lut(src, (6, 9), 5, int(rng.integers(0, 10_000)), rng)
+        L = _build(tmp_path, f"fast69_{k}", (6, 9), mutate_gen=lambda s, mm=mutated: mm)
+        ks, kb = bool(suite.killed(L, code, ["mul_add"])), bool(big.killed(L, code, ["mul_add"]))
+        res.append((what, ks, kb))
+        print(f"1/6/9 mul_add fast cover {what}: suite {'killed' if ks else 'survived'}, "
               f"64x sample {'killed' if kb else 'survived'}")
     assert not [r for r in res if r[2] and not r[1]], "a mutant escaped the suite's sample but not a larger one"
     assert sum(r[1] for r in res) >= 0.6 * len(res)
