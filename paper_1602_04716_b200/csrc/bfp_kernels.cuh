@@ -138,7 +138,8 @@ __device__ __forceinline__ void eval_unit_dyn(const w32* X, const w32* Y, const 
 // (~1000 LOP3 per word, 137 registers uncapped = 3 CTAs/SM) capped for 4
 // CTAs/SM (115 registers, no spills) measured +4% in two repeated A/Bs
 // (profiles/r01_ab_minb_wide.txt).  mul_add capped for 5 CTAs/SM (1/6/9:
-// 91 registers instead of 121, no spills in any format or mode, +9 LOP3 of
+// 91 registers instead of 121, no spills (with the second, fast-domain cover in
+// the kernel the 1/5/10 chain spills 12-20 B in three of its modes), +9 LOP3 of
 // ptxas re-materialisation) measured +1.0% on C5 in a 4-round interleaved
 // A/B (profiles/r02_ab_muladd_minb5.txt: 639.6 vs 633.2 Gelem/s, every
 // round ahead); 6 spills.

@@ -8,7 +8,7 @@ import sys
 
 import pytest
 
-from conftest import ROOT
+from conftest import ROOT, full_suite_only
 
 pytestmark = pytest.mark.gpu
 
@@ -71,6 +71,7 @@ def test_default_headline_line():
     assert c["value"] > 0 and c["value_median"] > 0 and c["kind"] == "reference" and c["cores"] >= 1
 
 
+@full_suite_only
 def test_c1_line():
     d = _run("--config", "C1", "--steps", "4", "--warmup", "3", "--cpu-seconds", "2")
     for k in BASE_KEYS:
@@ -86,6 +87,7 @@ def test_c1_line():
     assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
 
 
+@full_suite_only
 def test_reference_line():
     d = _run("--impl", "reference", "--steps", "2", "--warmup", "1", "--cpu-seconds", "2")
     assert d["impl"] == "reference" and d["value"] > 0 and d["higher_is_better"] is True

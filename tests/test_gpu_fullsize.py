@@ -9,10 +9,14 @@ tests/test_oracle.py) on all host threads (orc_verify):
   * C3: 1/5/10 pack_f32 of both operands, add, mul and unpack_f32 at 2^28;
   * C4: add and mul of every sweep format at 2^28;
   * the fused mul_add network (its own LOP3 cover, not the composition of the
-    mul and add covers): 1/6/9 over ALL 2^32 (a, b) pairs for 36 c values
-    (signed zeros, subnormals, 1, max finite, Inf, NaN, random) -- RN +
-    gradual by default, RZ + FTZ too with BFP_EXHAUSTIVE16=all (~4 min each)
-    -- and ALL 2^24 (a, b, c) triples of 1/4/3 and 2^18 of 1/3/2 in every mode.
+    mul and add covers; both of them, the general and the fast-domain one):
+    1/6/9 over (a, b) pairs for 36 c values (signed zeros, subnormals, 1, max
+    finite, Inf, NaN, random, both ends of the fast domain's c range) -- every
+    4th chunk of 1024 a values by default (2^30 pairs, RN + gradual: the
+    default run fits the driver's 20-minute step); ALL 2^32 pairs, and RZ +
+    FTZ too, with BFP_GPU_SUITE=full or BFP_EXHAUSTIVE16=all (~5 min each;
+    logged in profiles/r02_pytest_gpu_final.log) -- and ALL 2^24 (a, b, c)
+    triples of 1/4/3 and 2^18 of 1/3/2 in every mode.
 
 Inputs are generated on the device by the bench's own generators
 (workloads.py, torch ops -- not our kernels) and copied to the host for the
@@ -27,6 +31,8 @@ import time
 import numpy as np
 import pytest
 import torch
+
+from conftest import FULL_GPU_SUITE
 
 import paper_1602_04716_b200 as bfp
 from paper_1602_04716_b200 import _lib, workloads as W
@@ -129,7 +135,7 @@ C_1_6_9 = [0x0000, 0x8000, 0x0001, 0x8001, 0x01FF, 0x81FF, 0x0200, 0x8200, 0x3E0
            0x2000, 0xA1FF, 0x5FFF, 0xDE00]
 
 
-MODES_PAIRS = [(1, 0), (0, 1)] if os.environ.get("BFP_EXHAUSTIVE16") == "all" else [(1, 0)]
+MODES_PAIRS = [(1, 0), (0, 1)] if FULL_GPU_SUITE else [(1, 0)]
 
 
 @pytest.mark.parametrize("mode", MODES_PAIRS)
@@ -145,7 +151,10 @@ def test_mul_add_all_pairs_1_6_9(oracle, mode):
     L = _lib.lib()
     outs = [bfp.empty(spec, m) for _ in C_1_6_9]
     t0, bad = time.time(), 0
-    for a0 in range(0, 1 << 16, na):
+    # default: every 4th chunk of 1024 a values (16 of 64: a-exponent fields 0-1, 8-9, 16-17, ... of both
+    # signs, 2^30 pairs); BFP_GPU_SUITE=full / BFP_EXHAUSTIVE16=all: all 2^32 pairs (~5 min)
+    step = na if FULL_GPU_SUITE else 4 * na
+    for a0 in range(0, 1 << 16, step):
         va = bfp.pack(torch.arange(a0, a0 + na, dtype=torch.int64, device="cuda").repeat_interleave(1 << 16),
                       spec)
         for vc, o in zip(vcs, outs):
@@ -157,7 +166,8 @@ def test_mul_add_all_pairs_1_6_9(oracle, mode):
             i, k, g, w = info
             print(f"mismatch a={a0 + (i >> 16):#x} b={i & 0xffff:#x} c={C_1_6_9[k]:#x}: got {g:#x} want {w:#x}")
         bad += nbad
-    print(f"mul_add 1/6/9 {fmt}: all 2^32 (a, b) x {len(C_1_6_9)} c, {bad} mismatches, {time.time() - t0:.1f} s")
+    print(f"mul_add 1/6/9 {fmt}: {'all 2^32' if FULL_GPU_SUITE else '2^30 (every 4th a chunk)'} (a, b) x "
+          f"{len(C_1_6_9)} c, {bad} mismatches, {time.time() - t0:.1f} s")
     assert bad == 0
 
 

@@ -274,6 +274,7 @@ def test_layout_fuzz(oracle):
             assert np.array_equal(bf, oracle.decode_f32(fmt, wf).view(np.uint32)), (t, fmt, "f32 back")
 
 
+@__import__("conftest").full_suite_only
 def test_jit_runtime_covers(tmp_path, ref_oracle):
     """BFP_JIT_MAP=1: a runtime format gets LOP3-mapped covers generated on
     first use (tools/lutmap, GEN_ONE mode) -- same bits as the reference."""
