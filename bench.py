@@ -254,12 +254,13 @@ class Job:
     index: operand sets / outputs rotate with it).  `touch(i)` = (set id,
     bytes read from that set, bytes written) for the L2 reuse accounting."""
 
-    def __init__(self, label, op, spec, n, launch, algo_bytes, host=None, touch=None, aux=None):
+    def __init__(self, label, op, spec, n, launch, algo_bytes, host=None, touch=None, aux=None, info=None):
         self.label, self.op, self.spec, self.n = label, op, spec, n
         self.launch, self.algo_bytes, self.host = launch, algo_bytes, host
         # aux: {name: launch}: variants of this kernel timed on their own after the
         # step (same operands, never part of the step or of `value`)
         self.aux = aux or {}
+        self.info = info or {}  # facts about the operands, copied into the kernel's per_format entry
         self.touch = touch or (lambda i, lb=label, b=algo_bytes: (lb, b, 0))  # fixed operands
 
     @property
@@ -272,7 +273,7 @@ class JobMeta:
 
     def __init__(self, j: Job):
         self.label, self.op, self.spec, self.n, self.algo_bytes = j.label, j.op, j.spec, j.n, j.algo_bytes
-        self.fmt = j.fmt
+        self.fmt, self.info = j.fmt, dict(j.info)
 
 
 def _chunked_pack_f32(gen, n, spec, device, chunk=1 << 27):
@@ -337,13 +338,16 @@ def _arith_job(label, op, spec, n, sets, device, slot=0, stride=1):
     # the whole block is inside it: include/bfpgpu.h, BFP_GENERAL_NETWORK); the
     # general cover is timed on the same operands beside the step
     aux = {"general_network": lambda i, st: launch(i, st, 1 | 2)} if op == "mul_add" else None
+    info = {}
+    if op == "mul_add":  # which cover the launch's warps take: the library's own predicate + vote
+        info["fast_cover_blocks_frac"] = round(bfp.mul_add_fast_blocks(*sets[0]) / max(1, -(-n // 1024)), 6)
 
     nbits = spec.total_bits()
     a, b, c = sets[0]
     return Job(label, op, spec, n, launch, (nin + 1) * nbits / 8 * n,
                host={"kind": "arith", "op": op, "inputs": [a, b] + ([c] if c is not None else []),
                      "sets": len(sets)},
-               touch=lambda i: ((id(sets), idx(i)), nin * pb, pb), aux=aux)
+               touch=lambda i: ((id(sets), idx(i)), nin * pb, pb), aux=aux, info=info)
 
 
 def _clone_sets(first, k):
@@ -1241,6 +1245,7 @@ def build_line(cfg: str, res: dict, args, D: Dist, probes: dict, traffic: dict) 
                                       "traffic_over_algorithmic")
             if key in ent}
         per_format[j.fmt][j.op]["config"] = cfg
+        per_format[j.fmt][j.op].update(j.info)
         for name, ams in res.get("aux_ms", {}).items():
             if name.split(":")[0] != j.label:
                 continue
@@ -1254,8 +1259,10 @@ def build_line(cfg: str, res: dict, args, D: Dist, probes: dict, traffic: dict) 
                                  "(the one taken when a block holds a zero, subnormal, Inf, NaN, huge or tiny operand); not part "
                                  "of the step")
             per_format[j.fmt][j.op]["cover"] = (
-                "fast-domain cover: this workload's operands (finite normals, exponent fields 21..41: "
-                "1 <= ea, eb < 48, 32 <= ea + eb <= 91, 16 <= ec < 48) pass the per-block test in every warp")
+                "fast_cover_blocks_frac of this launch's 1024-element blocks pass the kernel's per-block test "
+                "(bfp_mul_add_fast_blocks: finite normals with 1 <= ea, eb < 48, 32 <= ea + eb <= 91, "
+                "16 <= ec < 48 for 1/6/9; C5's exponent fields are 21..41) and run the fast-domain cover, "
+                "the rest the general one")
     k_dom = max(range(len(jobs)), key=lambda k: res["kern_ms"][k])
     jd = jobs[k_dom]
     t_dom = None

@@ -203,6 +203,14 @@ void bfp_host_free(void* p);
  *         20 / 22 = fused float32 add / mul */
 bfp_status bfp_kernel_attrs(const bfp_format* f, int kernel, int* regs_per_thread,
                             int* ctas_per_sm, int* threads_per_cta);
+/* How many of the 1024-element blocks of bfp_mul_add(f, d_a, d_b, d_c, count)
+ * run the fast-domain cover (BFP_GENERAL_NETWORK above): the kernel's own
+ * predicate and warp vote, evaluated on the operands' exponent planes.
+ * *d_blocks (device memory, 8 bytes) is zeroed and then written on `stream`.
+ * Formats compiled at run time (NVRTC backend) return BFP_EUNSUPPORTED. */
+bfp_status bfp_mul_add_fast_blocks(const bfp_format* f, const uint32_t* d_a, const uint32_t* d_b,
+                                   const uint32_t* d_c, size_t count, unsigned long long* d_blocks,
+                                   void* stream);
 /* Number of kernel launches issued by this library in this process. */
 uint64_t bfp_launch_count(void);
 /* Measured LOP3 issue rate of this GPU (thread-ops/s): 8 independent chains

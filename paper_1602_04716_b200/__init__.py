@@ -16,6 +16,7 @@ from .bfp import (  # noqa: F401
     bfp_div,
     bfp_mul,
     bfp_mul_add,
+    mul_add_fast_blocks,
     bfp_sub,
     bfp_vector,
     bfpraw_stride,

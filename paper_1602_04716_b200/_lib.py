@@ -78,6 +78,8 @@ SIGNATURES = {
     "bfp_host_free": (None, [C.c_void_p]),
     "bfp_kernel_attrs": (C.c_int, [_F, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int),
                                    C.POINTER(C.c_int)]),
+    "bfp_mul_add_fast_blocks": (C.c_int, [_F, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p,
+                                          C.c_void_p]),
     "bfp_launch_count": (C.c_uint64, []),
     "bfp_probe_lop3": (C.c_int, [C.c_int, C.POINTER(C.c_float), C.POINTER(C.c_double)]),
 }

@@ -350,6 +350,21 @@ def arith(op: int, x: bfp_vector, y: bfp_vector, c: bfp_vector | None = None,
     return _binop(op, x, y, c, out, inputs_ready, general_network)
 
 
+def mul_add_fast_blocks(a: bfp_vector, b: bfp_vector, c: bfp_vector) -> int:
+    """bfp_mul_add_fast_blocks: how many 1024-element blocks of bfp_mul_add(a, b, c)
+    run the fast-domain cover; the rest run the general one."""
+    require_same_shape(a.spec, b.spec)
+    require_same_shape(a.spec, c.spec)
+    if not (a.count == b.count == c.count):
+        raise ValueError("operands must have the same element count")
+    for v, name in ((a, "a"), (b, "b"), (c, "c")):
+        _check_planes(v, a, name)
+    n = torch.zeros(1, dtype=torch.int64, device=a.planes.device)
+    check(lib().bfp_mul_add_fast_blocks(a.spec.c, a.planes.data_ptr(), b.planes.data_ptr(), c.planes.data_ptr(),
+                                        a.count, n.data_ptr(), _stream()), "mul_add_fast_blocks")
+    return int(n.item())
+
+
 def bfp_add(x: bfp_vector, y: bfp_vector, out: bfp_vector | None = None) -> bfp_vector:
     """arith.hpp:235-320."""
     return _binop(OP_ADD, x, y, out=out)

@@ -183,6 +183,23 @@ bfp_status bfp_arith_ex(int op, const bfp_format* f, const uint32_t* d_x, const 
                      "arith launch");
 }
 
+bfp_status bfp_mul_add_fast_blocks(const bfp_format* f, const uint32_t* d_a, const uint32_t* d_b,
+                                   const uint32_t* d_c, size_t count, unsigned long long* d_blocks,
+                                   void* stream) {
+  const Impl* impl = nullptr;
+  const bfp_status s = resolve(f, &impl);
+  if (s != BFP_OK) return s;
+  if (!d_blocks || (count && (!d_a || !d_b || !d_c))) return fail(BFP_EARG, "null operand");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const cudaError_t e = cudaMemsetAsync(d_blocks, 0, sizeof(unsigned long long), st);
+  if (e != cudaSuccess) return cuda_status(e, "fast_blocks memset");
+  if (count == 0) return BFP_OK;
+  const cudaError_t r = impl->fast_blocks(d_a, d_b, d_c, nblocks(count), d_blocks, st);
+  if (r == cudaErrorNotSupported) return fail(BFP_EUNSUPPORTED, "no compiled network for this format");
+  ++g_launches;
+  return cuda_status(r, "fast_blocks launch");
+}
+
 bfp_status bfp_arith(int op, const bfp_format* f, const uint32_t* d_x, const uint32_t* d_y,
                      const uint32_t* d_c, uint32_t* d_z, size_t count, void* stream) {
   return bfp_arith_ex(op, f, d_x, d_y, d_c, d_z, count, stream, 0);

@@ -124,6 +124,34 @@ __device__ __forceinline__ void eval_unit_dyn(const w32* X, const w32* Y, const 
   eval_unit<F, OP>(X, Y, Cc, Z);
 }
 
+// How many blocks of a mul_add call run the fast-domain cover: the same
+// predicate on the same planes and the same warp vote as k_arith (only the
+// exponent planes are read).  Introspection for callers, tests and the bench.
+template <class F>
+__global__ void __launch_bounds__(kThreads) k_fast_blocks(const w32* __restrict__ a,
+                                                          const w32* __restrict__ b,
+                                                          const w32* __restrict__ c, size_t units,
+                                                          unsigned long long* __restrict__ count) {
+  constexpr int N = F::N, S = F::S, E = F::E;
+  const size_t stride = size_t(gridDim.x) * kThreads;
+  unsigned long long mine = 0;
+  for (size_t u = size_t(blockIdx.x) * kThreads + threadIdx.x; u < units; u += stride) {
+    const size_t base = (u >> 5) * (size_t(N) * 32) + (u & 31);
+    bool in_domain = false;
+    if constexpr (has_fast_cover<F, OP_MUL_ADD>()) {
+      w32 A[N], B[N], Cc[N];
+      BFP_UNROLL for (int j = S; j < S + E; ++j) {
+        A[j] = a[base + j * 32];
+        B[j] = b[base + j * 32];
+        Cc[j] = c[base + j * 32];
+      }
+      in_domain = mul_add_fast_domain<F>(A, B, Cc) == ONES;
+    }
+    if (__all_sync(0xffffffffu, in_domain) && (threadIdx.x & 31) == 0) ++mine;
+  }
+  if (mine) atomicAdd(count, mine);
+}
+
 // One thread per unit, grid-stride.  (A register double-buffered variant --
 // next unit's loads issued before the current network -- measured slower on
 // the B200: the extra registers cost more occupancy than the overlap gained.)
@@ -852,6 +880,11 @@ struct Impl {
   virtual cudaError_t unpack_f64(const w32* planes, double* out, size_t n, cudaStream_t st) const = 0;
   virtual const void* kernel(int id) const = 0;  // device function handle (attribute queries)
   virtual bool compiled() const { return true; }
+  // blocks of a mul_add call that run the fast-domain cover (*d_count += them)
+  virtual cudaError_t fast_blocks(const w32*, const w32*, const w32*, size_t, unsigned long long*,
+                                  cudaStream_t) const {
+    return cudaErrorNotSupported;
+  }
 };
 
 template <class F>
@@ -1055,6 +1088,14 @@ struct FormatImpl {
       return FormatImpl::unpack_f64(p, o, n, st);
     }
     const void* kernel(int id) const override { return FormatImpl::kernel(id); }
+    cudaError_t fast_blocks(const w32* a, const w32* b, const w32* c, size_t nb, unsigned long long* d_count,
+                            cudaStream_t st) const override {
+      const size_t units = nb * 32;
+      if (!units) return cudaSuccess;
+      auto k = k_fast_blocks<F>;
+      static const int wave = wave_ctas(k);
+      return launch(k, grid_for(wave, units), st, a, b, c, units, d_count);
+    }
   };
   static const Impl* get() {
     static const Backend impl;

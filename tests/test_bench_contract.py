@@ -58,6 +58,7 @@ def test_default_headline_line():
     assert set(pf["1/6/9"]) == {"mul_add", "mul_add (general_network)"}
     fast, gen = pf["1/6/9"]["mul_add"], pf["1/6/9"]["mul_add (general_network)"]
     assert fast["lop3_per_elem"] < gen["lop3_per_elem"] and gen["gelem_s"] > 0
+    assert fast["fast_cover_blocks_frac"] == 1.0  # C5's operands: every block inside the fast domain
     # which cover ran, measured: executed ALU instructions per element (ncu, this run)
     assert fast["alu_inst_per_elem_measured"] < gen["lop3_per_elem"]
     for fmt in ("1/3/2", "1/5/3", "1/5/7", "1/8/7", "1/8/15"):

@@ -53,6 +53,19 @@ def gpu_arith(op: str, fmt, px, py, pc=None, flags: int = 0) -> np.ndarray:
     return dz.cpu().numpy().view(np.uint32)
 
 
+def fast_blocks(fmt, pa, pb, pc) -> int:
+    """bfp_mul_add_fast_blocks: blocks of the call that run the fast-domain cover."""
+    nb = 1 + fmt[0] + fmt[1]
+    count = (len(pa) // (nb * 32)) * 1024
+    da, db, dc = dev(pa), dev(pb), dev(pc)
+    out = torch.full((1,), -1, dtype=torch.int64, device="cuda")
+    f = cfmt(fmt)
+    rc = _lib.lib().bfp_mul_add_fast_blocks(C.byref(f), da.data_ptr(), db.data_ptr(), dc.data_ptr(), count,
+                                            out.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    assert rc == 0, _lib.lib().bfp_last_error()
+    return int(out.item())
+
+
 def check(O, op, fmt, x, y, c=None):
     nb = 1 + fmt[0] + fmt[1]
     px, py = O.pack_planes(x, nb), O.pack_planes(y, nb)
@@ -130,6 +143,7 @@ def test_mul_add_fast_and_general_covers(oracle, fmt2, mode):
     for flags in (0, 2):  # every block on the fast cover / the general cover forced
         got = oracle.unpack_planes(gpu_arith("mul_add", fmt, *planes, flags=flags), n, nb)
         assert np.array_equal(got, want), (fmt, flags, int((got != want).sum()))
+    assert fast_blocks(fmt, *planes) == n // 1024  # the kernel's own predicate + vote: every warp
     # every other block gets ONE element outside the domain (a zero, a
     # subnormal a, a tiny c): those warps take the general cover
     a2, b2, c2 = a.copy(), b.copy(), c.copy()
@@ -145,8 +159,25 @@ def test_mul_add_fast_and_general_covers(oracle, fmt2, mode):
     inside = fast_domain(e, s, a2, b2, c2).reshape(-1, 1024).all(axis=1)
     assert inside[1::2].all() and not inside[0::2].any()
     want2 = oracle.binop("mul_add", fmt, a2, b2, c2)
-    got2 = oracle.unpack_planes(gpu_arith("mul_add", fmt, *(oracle.pack_planes(v, nb) for v in (a2, b2, c2))), n, nb)
+    planes2 = [oracle.pack_planes(v, nb) for v in (a2, b2, c2)]
+    got2 = oracle.unpack_planes(gpu_arith("mul_add", fmt, *planes2), n, nb)
     assert np.array_equal(got2, want2), (fmt, int((got2 != want2).sum()))
+    assert fast_blocks(fmt, *planes2) == n // 2048
+    # special-weighted random operands: the device count equals the restated predicate's
+    x, y, z = (operands(e, s, 1 << 16, rng) for _ in range(3))
+    x[: 1 << 15], y[: 1 << 15], z[: 1 << 15] = a[: 1 << 15], b[: 1 << 15], c[: 1 << 15]
+    perm = rng.permutation(64)  # whole blocks shuffled
+    x, y, z = (v.reshape(64, 1024)[perm].ravel() for v in (x, y, z))
+    want_blocks = int(fast_domain(e, s, x, y, z).reshape(-1, 1024).all(axis=1).sum())
+    assert 16 <= want_blocks < 64
+    assert fast_blocks(fmt, *(oracle.pack_planes(v, nb) for v in (x, y, z))) == want_blocks
+
+
+def test_fast_blocks_without_a_fast_cover(oracle):
+    """1/3/2 has no fast-domain cover (E = KN): every block runs the general one."""
+    rng = np.random.default_rng(3)
+    planes = [oracle.pack_planes(rng.integers(0, 64, size=4096, dtype=np.uint64), 6) for _ in range(3)]
+    assert fast_blocks((3, 2, 1, 0), *planes) == 0
 
 
 @pytest.mark.parametrize("mode", MODES)
