@@ -93,6 +93,32 @@ def test_mul_add_fast_domain_exhaustive_1_4_3(oracle, host, mode):
     _check_fast(oracle, host, (4, 3) + mode, a, b, c, min_inside=1 << 19)
 
 
+@pytest.mark.parametrize("mode", MODES)
+def test_mul_add_fast_cover_exhaustive_1_5_3(oracle, host, mode):
+    """The generated fast-domain cover of 1/5/3 on EVERY (a, b, c) inside its
+    domain (27.4 M triples of the 2^27), enumerated from the exponent ranges."""
+    e, s = 5, 3
+    fmt = (e, s) + mode
+    v = np.arange(1 << 9, dtype=np.uint64)
+    ex = (v >> np.uint64(s)) & np.uint64(31)
+    A, Cv = v[(ex >= 1) & (ex < 24)], v[(ex >= 8) & (ex < 24)]
+    total = 0
+    for a8 in A.reshape(-1, 8):
+        a, b, c = (g.ravel() for g in np.meshgrid(a8, A, Cv, indexing="ij"))
+        keep = fast_domain(e, s, a, b, c)
+        a, b, c = a[keep], b[keep], c[keep]
+        if not len(a):
+            continue
+        total += len(a)
+        pad = -len(a) % 1024
+        a, b, c = (np.concatenate([x, np.repeat(x[-1:], pad)]) for x in (a, b, c))
+        want = oracle.binop("mul_add", fmt, a, b, c)
+        got = oracle.unpack_planes(host.binop("mul_add_fast", fmt, *(oracle.pack_planes(x, 9) for x in (a, b, c)),
+                                              True), len(a), 9)
+        assert np.array_equal(got, want), (fmt, int((got != want).sum()))
+    assert total == 27394048
+
+
 @pytest.mark.parametrize("fmt2", [f for f in FORMATS if 1 + f[0] + f[1] > 8])
 @pytest.mark.parametrize("mode", MODES)
 def test_mul_add_fast_domain_random(oracle, host, fmt2, mode):
