@@ -22,12 +22,12 @@ MODES = [(1, 0), (0, 0), (1, 1), (0, 1)]  # (rn, ftz)
 
 # The default `-m gpu` run is sized for the driver's 20-minute step (~9 min on a
 # B200); BFP_GPU_SUITE=full (or BFP_EXHAUSTIVE16=all) adds the longest sweeps.
-# A full run is logged in profiles/r02_pytest_gpu_final.log (379 passed, 17.6 min).
+# A full run is logged in profiles/r02_pytest_gpu_full_all.log (with BFP_EXHAUSTIVE16=all too: 424 passed, 34 min).
 import os as _os  # noqa: E402
 
 FULL_GPU_SUITE = _os.environ.get("BFP_GPU_SUITE") == "full" or _os.environ.get("BFP_EXHAUSTIVE16") == "all"
 full_suite_only = pytest.mark.skipif(
-    not FULL_GPU_SUITE, reason="set BFP_GPU_SUITE=full (full run logged in profiles/r02_pytest_gpu_final.log)")
+    not FULL_GPU_SUITE, reason="set BFP_GPU_SUITE=full (full run logged in profiles/r02_pytest_gpu_full_all.log)")
 
 
 def pytest_configure(config):

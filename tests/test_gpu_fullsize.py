@@ -15,7 +15,7 @@ tests/test_oracle.py) on all host threads (orc_verify):
     4th chunk of 1024 a values by default (2^30 pairs, RN + gradual: the
     default run fits the driver's 20-minute step); ALL 2^32 pairs, and RZ +
     FTZ too, with BFP_GPU_SUITE=full or BFP_EXHAUSTIVE16=all (~5 min each;
-    logged in profiles/r02_pytest_gpu_final.log) -- and ALL 2^24 (a, b, c)
+    logged in profiles/r02_pytest_gpu_full_all.log) -- and ALL 2^24 (a, b, c)
     triples of 1/4/3 and 2^18 of 1/3/2 in every mode.
 
 Inputs are generated on the device by the bench's own generators
