@@ -167,7 +167,9 @@ bfp_status bfp_arith_f32(int op, const bfp_format* f, const float* d_x, const fl
  * (arith.hpp:235-444), so the result equals that sequence of calls; the
  * intermediates stay in registers (one kernel, HBM traffic = the inputs
  * once + the output).  Compiled for the format and program by NVRTC on first
- * use and cached (BFP_EUNSUPPORTED without NVRTC).  Replaces chains of the
+ * use and cached (BFP_EUNSUPPORTED without NVRTC); programs that are one of
+ * the ahead-of-time kernels -- "xy+", "xy-", "xy*", "xy/" and "xy*z+" (the
+ * fused mul_add with its two covers) -- are sent to it.  Replaces chains of the
  * reference's bfp_* calls ("longer chains"). */
 bfp_status bfp_chain(const bfp_format* f, const char* program, int n_inputs,
                      const uint32_t* const* d_in, uint32_t* d_z, size_t count, void* stream);

@@ -239,6 +239,18 @@ bfp_status chain_common(const bfp_format* f, const char* program, int n_inputs, 
   if (!d_z || !d_in) return fail(BFP_EARG, "null operand");
   for (int i = 0; i < n_inputs; ++i)
     if (used[i] && !d_in[i]) return fail(BFP_EARG, "null operand");
+  // Programs that ARE one of the ahead-of-time kernels go to it (no NVRTC; the
+  // fused chain keeps its two covers): "xy<op>" and "xy*z+".
+  if (!f32) {
+    auto in = [&](char ch) { return static_cast<const uint32_t*>(d_in[ch - 'a']); };
+    auto is_in = [](char ch) { return ch >= 'a' && ch <= 'h'; };
+    if (prog.size() == 3 && is_in(prog[0]) && is_in(prog[1])) {
+      const int op = prog[2] == '+' ? 0 : prog[2] == '-' ? 1 : prog[2] == '*' ? 2 : 3;
+      return bfp_arith(op, f, in(prog[0]), in(prog[1]), nullptr, static_cast<uint32_t*>(d_z), count, stream);
+    }
+    if (prog.size() == 5 && is_in(prog[0]) && is_in(prog[1]) && prog[2] == '*' && is_in(prog[3]) && prog[4] == '+')
+      return bfp_arith(4, f, in(prog[0]), in(prog[1]), in(prog[3]), static_cast<uint32_t*>(d_z), count, stream);
+  }
   if (!bfpg::jit_available()) return fail(BFP_EUNSUPPORTED, "bfp_chain needs NVRTC");
   ++g_launches;
   return cuda_status(bfpg::chain_launch(f->exp_bits, f->sig_bits, f->rounding == 1, f->subnormals == 1,
