@@ -106,9 +106,12 @@ __device__ __forceinline__ void eval_unit(const w32* X, const w32* Y, const w32*
 // a warp are in the loop together (units is a multiple of 32 and a warp owns
 // 32 consecutive units), so the full-mask vote is safe.
 constexpr int OP_MUL_ADD_FAST = 5;
+// Formats without generated covers (the NVRTC backend's runtime formats) use
+// the fast-domain TEMPLATE the same way.
 template <class F, int OP>
 constexpr bool has_fast_cover() {
-  if constexpr (OP == OP_MUL_ADD) return Gen<F, OP_MUL_ADD_FAST>::ok;
+  if constexpr (OP == OP_MUL_ADD)
+    return Gen<F, OP_MUL_ADD_FAST>::ok || (!Gen<F, OP_MUL_ADD>::ok && mul_add_fast_ok<F>());
   return false;
 }
 template <class F, int OP>
@@ -117,7 +120,10 @@ __device__ __forceinline__ void eval_unit_dyn(const w32* X, const w32* Y, const 
   if constexpr (has_fast_cover<F, OP>()) {
     const bool in_domain = mul_add_fast_domain<F>(X, Y, Cc) == ONES;
     if (__all_sync(0xffffffffu, in_domain) && !(flags & 2u)) {
-      Gen<F, OP_MUL_ADD_FAST>::run(X, Y, Cc, Z);
+      if constexpr (Gen<F, OP_MUL_ADD_FAST>::ok)
+        Gen<F, OP_MUL_ADD_FAST>::run(X, Y, Cc, Z);
+      else
+        mul_add_fast_w<F>(X, Y, Cc, Z);
       return;
     }
   }

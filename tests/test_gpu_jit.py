@@ -60,6 +60,36 @@ def test_jit_arith_vs_reference(ref_oracle, fmt2, mode):
         assert np.array_equal(got, want), (op, fmt)
 
 
+@pytest.mark.parametrize("fmt2", [(6, 3), (7, 20), (11, 20), (10, 40)])
+@pytest.mark.parametrize("mode", [(1, 0), (0, 1)])
+def test_jit_mul_add_fast_domain(ref_oracle, oracle, fmt2, mode):
+    """Runtime formats run mul_add's fast-domain TEMPLATE on blocks inside the
+    domain (csrc/bfp_kernels.cuh, has_fast_cover): operands generated inside it,
+    every other block with one element outside, and the general network forced
+    -- all equal the reference's bfp_add(bfp_mul(a, b), c)."""
+    from conftest import fast_domain, fast_domain_operands
+    e, s = fmt2
+    fmt = fmt2 + mode
+    nb = 1 + e + s
+    rng = np.random.default_rng(900 + nb + mode[0])
+    n = 1 << 13
+    a, b, c = fast_domain_operands(oracle, fmt, n, rng)
+    pos = np.arange(0, n // 1024, 2) * 1024 + rng.integers(0, 1024, size=n // 2048)
+    a[pos[0::2]] = 0
+    c[pos[1::2]] &= np.uint64((1 << s) - 1)
+    assert fast_domain(e, s, a, b, c).reshape(-1, 1024).all(axis=1).sum() == n // 2048
+    pa, pb, pc = (ref_oracle.pack_planes(v, nb) for v in (a, b, c))
+    want = ref_oracle.ref_binop_planes("mul_add", fmt, pa, pb, pc)
+    L = _lib.lib()
+    f = _lib.BfpFormat(e, s, mode[0], mode[1], b"")
+    da, db, dc = (torch.from_numpy(p.view(np.int32)).cuda() for p in (pa, pb, pc))
+    for flags in (0, 2):
+        dz = torch.empty_like(da)
+        assert L.bfp_arith_ex(4, C.byref(f), da.data_ptr(), db.data_ptr(), dc.data_ptr(), dz.data_ptr(), n,
+                              torch.cuda.current_stream().cuda_stream, flags) == 0, L.bfp_last_error()
+        assert np.array_equal(dz.cpu().numpy().view(np.uint32), want), (fmt, flags)
+
+
 @pytest.mark.parametrize("fmt2", [(2, 1), (6, 3), (7, 16), (2, 5), (3, 11), (2, 20), (4, 22)])
 def test_jit_codec(oracle, fmt2):
     e, s = fmt2
