@@ -24,8 +24,12 @@ fi
 if [ "${NCU:-1}" = 1 ]; then
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $S/launches_default.csv \
     python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-ncu > $S/launches_default.log 2>&1; echo "launch list rc=$?"
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_arith -c 1 -o $S/c5_full -f \
+  # the report goes to /tmp first: gpurun_out/ is size-capped, so the raw page is exported here and the
+  # .ncu-rep only copied when it is small enough
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_arith -c 1 -o /tmp/c5_full -f \
     python tools/profile_kernels.py --config C5 --iters 1 > $S/c5_full.log 2>&1; echo "ncu full C5 rc=$?"
+  ncu -i /tmp/c5_full.ncu-rep --page raw --csv > $S/c5_full_raw.csv 2>/dev/null
+  [ "$(stat -c %s /tmp/c5_full.ncu-rep 2>/dev/null || echo 99999999)" -lt 40000000 ] && cp /tmp/c5_full.ncu-rep $S/c5_full.ncu-rep
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_arith --launch-skip 9 -c 1 -o $S/c4_mul815_full -f \
     python tools/profile_kernels.py --config C4 --iters 1 > $S/c4_full.log 2>&1; echo "ncu full C4 1/8/15 mul rc=$?"
 fi
