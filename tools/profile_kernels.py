@@ -3,7 +3,7 @@ bench.py does) and runs a few steps of its kernels, nothing else, so launch
 lists and --set full captures see only the hot path.
 
     python tools/profile_kernels.py [--config C5] [--iters 1] [--ops add_1/8/15,...]
-                                    [--rounding rn|rz] [--subnormals gradual|ftz] [--marker]
+                                    [--rounding rn|rz] [--subnormals gradual|ftz] [--marker] [--aux]
 
 --marker prints "TIMED <k>" before the timed launches (k = kernels per
 iteration x iters): bench.py's in-run traffic measurement takes the last k
@@ -27,6 +27,8 @@ def main() -> None:
     ap.add_argument("--rounding", choices=["rn", "rz"], default="rn")
     ap.add_argument("--subnormals", choices=["gradual", "ftz"], default="gradual")
     ap.add_argument("--marker", action="store_true")
+    ap.add_argument("--aux", action="store_true",
+                    help="run the kernels' timed variants instead (mul_add forced onto its general cover)")
     ap.add_argument("--rank", type=int, default=0, help="build rank r's shard of a --world run (bench's sizes)")
     ap.add_argument("--world", type=int, default=1)
     a = ap.parse_args()
@@ -34,7 +36,9 @@ def main() -> None:
     dev = torch.device("cuda", 0)
     import bench
     bench.MODE = (int(a.rounding == "rn"), int(a.subnormals == "ftz"))
-    jobs = [(j.label, j.launch) for j in bench.make_jobs(a.config, a.rank, a.world, dev)]
+    made = bench.make_jobs(a.config, a.rank, a.world, dev)
+    jobs = ([(f"{j.label}:{name}", fn) for j in made for name, fn in j.aux.items()] if a.aux
+            else [(j.label, j.launch) for j in made])
     if a.ops:
         keep = set(a.ops.split(","))
         jobs = [j for j in jobs if j[0] in keep]
